@@ -1,0 +1,22 @@
+/* cqg_diag.h — diagnostic entry points of libcqg.so used by the parity tests
+ * to check the device numerics exhaustively (no reference interface is
+ * replaced by these; they expose the scalar device functions of
+ * csrc/numerics.cuh over ranges of FP32 bit patterns). */
+#ifndef CQG_DIAG_H
+#define CQG_DIAG_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* E4M3 codes of the floats with bit patterns lo .. lo+count-1
+ * (== cq::encode_f8, proj/src/numerics.cpp:41-64). */
+int cqg_diag_e4m3_range(uint32_t lo, uint64_t count, uint8_t* out_host);
+/* BF16 codes (== cq::encode_bf16, numerics.cpp:84-94). */
+int cqg_diag_bf16_range(uint32_t lo, uint64_t count, uint16_t* out_host);
+/* which: 0 glibc-exact expf, 1 glibc-exact erff, 2 reference gelu
+ * (kernels.cpp:226). */
+int cqg_diag_libm_range(int which, uint32_t lo, uint64_t count, float* out_host);
+#ifdef __cplusplus
+}
+#endif
+#endif

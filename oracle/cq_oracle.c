@@ -829,3 +829,28 @@ int cqo_run_acdc(const cqo_model* m, const int* clean, const int* corrupt, const
   free(mask), free(order), free(raw);
   return rc;
 }
+
+/* Host glibc values over a range of float bit patterns (the libm the
+ * reference calls): which 0 expf, 1 erff, 2 the reference gelu
+ * (kernels.cpp:226). Used to check the device restatements exhaustively. */
+void cqo_libm_range(int which, uint32_t lo, uint64_t count, float* out) {
+  for (uint64_t i = 0; i < count; ++i) {
+    uint32_t u = lo + (uint32_t)i;
+    float x;
+    memcpy(&x, &u, 4);
+    if (which == 0) out[i] = expf(x);
+    else if (which == 1) out[i] = erff(x);
+    else out[i] = 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+  }
+}
+
+/* encode_f8 / encode_bf16 over a range of float bit patterns. */
+void cqo_codes_range(uint32_t lo, uint64_t count, uint8_t* f8, uint16_t* bf16) {
+  for (uint64_t i = 0; i < count; ++i) {
+    uint32_t u = lo + (uint32_t)i;
+    float x;
+    memcpy(&x, &u, 4);
+    if (f8) f8[i] = cqo_encode_f8((double)x);
+    if (bf16) bf16[i] = cqo_encode_bf16(x);
+  }
+}

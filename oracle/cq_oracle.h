@@ -84,6 +84,9 @@ int cqo_run_acdc(const cqo_model* m, const int* clean, const int* corrupt, const
 
 const char* cqo_last_error(void);
 
+void cqo_libm_range(int which, uint32_t lo, uint64_t count, float* out);
+void cqo_codes_range(uint32_t lo, uint64_t count, uint8_t* f8, uint16_t* bf16);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,1284 @@
+// engine.cu — host orchestration of the patched-forward hot path + C ABI.
+// See engine.h for the execution strategy; SURVEY.md §8 for the mapping to
+// the reference (proj/src/patching.cpp, model.cpp, acdc.cpp).
+#include "engine.h"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <set>
+
+namespace cqg {
+
+static thread_local std::string g_err;
+
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      throw Error(e_ == cudaErrorMemoryAllocation ? 3 : 2,                                      \
+                  std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" #x ") at " +      \
+                      __FILE__ + ":" + std::to_string(__LINE__));                               \
+  } while (0)
+
+#define NK(x)                                                                                   \
+  do {                                                                                          \
+    ncclResult_t r_ = (x);                                                                      \
+    if (r_ != ncclSuccess) throw Error(2, std::string("NCCL error: ") + ncclGetErrorString(r_)); \
+  } while (0)
+
+// ===========================================================================
+// Graph / policy / trie
+// ===========================================================================
+static int node_stage(int kind, int layer, int L) {
+  switch (kind) {
+    case kEmbed: return 0;
+    case kHead: return 1 + 2 * layer;
+    case kMlp: return 2 + 2 * layer;
+    default: return 1 + 2 * L;
+  }
+}
+
+Graph::Graph(const cqg_config& c) {
+  // ModelConfig::validate (model.cpp:144-155), batch fixed to 1
+  if (c.n_layers < 1) throw Error(1, "ModelConfig: n_layers must be >= 1");
+  if (c.n_heads < 1) throw Error(1, "ModelConfig: n_heads must be >= 1");
+  if (c.d_model < 1 || c.d_k < 1) throw Error(1, "ModelConfig: d_model and d_k must be >= 1");
+  if (c.n_heads * c.d_k != c.d_model) throw Error(1, "ModelConfig: n_heads * d_k must equal d_model");
+  if (c.vocab < 2) throw Error(1, "ModelConfig: vocab must be >= 2");
+  if (c.seq_len < 1) throw Error(1, "ModelConfig: seq_len must be >= 1");
+  if (c.has_mlp > 1) throw Error(1, "ModelConfig: has_mlp must be 0 or 1");
+  L = (int)c.n_layers, H = (int)c.n_heads, D = (int)c.d_model, dk = (int)c.d_k;
+  V = (int)c.vocab, S = (int)c.seq_len, mlp = (int)c.has_mlp;
+  // nodes (model.cpp:184-190)
+  auto add = [&](int k, int l, int h) {
+    kind.push_back(k), layer.push_back(l), head.push_back(h), stage.push_back(node_stage(k, l, L));
+  };
+  add(kEmbed, -1, -1);
+  for (int l = 0; l < L; ++l) {
+    for (int h = 0; h < H; ++h) add(kHead, l, h);
+    if (mlp) add(kMlp, l, -1);
+  }
+  add(kUnembed, -1, -1);
+  N = (int)kind.size();
+  unembed = N - 1;
+  n_stages = 2 + 2 * L;
+  stage_nodes.resize(n_stages);
+  for (int i = 0; i < N; ++i) stage_nodes[stage[i]].push_back(i);
+  // edges (model.cpp:192-201)
+  in_edges.resize(N);
+  for (int j = 0; j < N; ++j)
+    for (int i = 0; i < j; ++i) {
+      if (stage[i] >= stage[j]) continue;
+      in_edges[j].push_back((int)esrc.size());
+      esrc.push_back(i);
+      edst.push_back(j);
+    }
+  E = (int)esrc.size();
+}
+
+int Graph::mat(int which, int l) const {
+  const int per = 6 + (mlp ? 4 : 0);
+  switch (which) {
+    case 0: return 0;
+    case 1: return 1;
+    case 12: return 2 + L * per;
+    case 13: return 3 + L * per;
+    case 14: return 4 + L * per;
+    default: return 2 + l * per + (which - 2);
+  }
+}
+
+std::vector<int> Graph::sweep_order(const std::vector<uint8_t>& mask) const {
+  // model.cpp:238-246
+  std::vector<int> o;
+  for (int j = N - 1; j >= 0; --j)
+    for (auto it = in_edges[j].rbegin(); it != in_edges[j].rend(); ++it)
+      if (mask[*it]) o.push_back(*it);
+  return o;
+}
+
+Policy Policy::from(const cqg_policy& p) {
+  Policy q;
+  q.att = p.attention_default, q.mlp = p.mlp_default, q.emb = p.embed_precision;
+  q.unemb = p.unembed_precision, q.mode = p.low_mode;
+  q.th_l = p.target_head_layer, q.th_h = p.target_head_layer >= 0 ? p.target_head_head : -1;
+  q.tm = p.target_mlp;
+  for (int v : {q.att, q.mlp, q.emb, q.unemb})
+    if (v < 0 || v > 2) throw Error(1, "policy: precision must be 0 (P8), 1 (P16) or 2 (P32)");
+  if (q.mode < 0 || q.mode > 1) throw Error(1, "policy: low_mode must be 0 (E4m3) or 1 (Rtn4)");
+  return q;
+}
+
+int Policy::precision_of(const Graph& g, int n) const {
+  switch (g.kind[n]) {
+    case kEmbed: return emb;
+    case kUnembed: return unemb;
+    case kHead: return (th_l >= 0 && th_l == g.layer[n] && th_h == g.head[n]) ? 2 : att;
+    default: return (tm >= 0 && tm == g.layer[n]) ? 2 : mlp;
+  }
+}
+
+bool Policy::operator==(const Policy& o) const {
+  return att == o.att && mlp == o.mlp && emb == o.emb && unemb == o.unemb && mode == o.mode &&
+         th_l == o.th_l && th_h == o.th_h && tm == o.tm;
+}
+bool Policy::operator<(const Policy& o) const {
+  auto t = [](const Policy& p) {
+    return std::vector<int>{p.att, p.mlp, p.emb, p.unemb, p.mode, p.th_l, p.th_h, p.tm};
+  };
+  return t(*this) < t(o);
+}
+
+Policy policy_for_edge(const Graph& g, int e, const Policy& base) {
+  Policy p = base;
+  p.th_l = p.th_h = p.tm = -1;
+  const int s = g.esrc[e];
+  if (g.kind[s] == kHead) p.th_l = g.layer[s], p.th_h = g.head[s];
+  if (g.kind[s] == kMlp) p.tm = g.layer[s];
+  return p;
+}
+
+void Trie::build(const Graph& g, const uint8_t* mask) {
+  parent.assign(1, -1);
+  src.assign(1, -1);
+  rec_in.assign(g.N, 0);
+  std::map<std::pair<int, int>, int> child;
+  for (int w = 1; w < g.N; ++w) {
+    int cur = 0;
+    for (int e : g.in_edges[w]) {
+      if (mask && !mask[e]) continue;
+      const int s = g.esrc[e];
+      auto it = child.find({cur, s});
+      if (it == child.end()) {
+        const int id = (int)parent.size();
+        parent.push_back(cur);
+        src.push_back(s);
+        child[{cur, s}] = id;
+        cur = id;
+      } else {
+        cur = it->second;
+      }
+    }
+    rec_in[w] = cur;
+  }
+  by_stage.assign(g.n_stages, {});
+  for (int t = 1; t < size(); ++t) by_stage[g.stage[src[t]]].push_back(t);
+  for (auto& v : by_stage)
+    std::sort(v.begin(), v.end(), [&](int a, int b) { return src[a] != src[b] ? src[a] < src[b] : a < b; });
+}
+
+// ===========================================================================
+// device buffers
+// ===========================================================================
+DeviceBuf::~DeviceBuf() {
+  if (p) cudaFree(p);
+}
+
+void DeviceBuf::ensure(size_t n) {
+  if (n <= bytes) return;
+  if (p) {
+    cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  n = (n + 255) & ~size_t(255);
+  CK(cudaMalloc(&p, n));
+  bytes = n;
+}
+
+// ===========================================================================
+// Engine
+// ===========================================================================
+struct Run {  // one evaluation context (a baseline) over nb items
+  int nb = 0;
+  size_t seg = 0;  // floats per node activation
+  DeviceBuf out, trie, logits, lse;
+  float* o(int n) const { return out.as<float>() + (size_t)n * seg; }
+  float* t(int n) const { return trie.as<float>() + (size_t)n * seg; }
+};
+
+struct HeadIO {
+  const float* in;
+  int head;
+  float* out;
+};
+struct SegIO {
+  const float* in;
+  float* out;
+};
+
+struct Engine {
+  Graph g;
+  int device = 0;
+  cudaStream_t st = nullptr;
+  std::vector<std::unique_ptr<DeviceBuf>> master;
+  std::vector<int64_t> msize;
+  std::map<int, std::vector<std::unique_ptr<DeviceBuf>>> img;  // 0 e4m3, 1 bf16, 2 rtn4
+  // dataset
+  int B = 0, item_off = 0, item_total = 0, metric = 0;
+  DeviceBuf d_clean, d_corrupt, d_ans, d_dis;
+  // scratch
+  std::map<std::string, std::unique_ptr<DeviceBuf>> pool;
+  DeviceBuf zero;
+  // job staging
+  char* h_stage = nullptr;
+  size_t stage_cap = 0, stage_off = 0;
+  DeviceBuf d_stage;
+  // caches
+  Run base_run;                    // masked baseline (per call)
+  Run patch_run;                   // full-graph run that supplies patch values
+  bool patch_valid = false;
+  Policy patch_policy;
+  int patch_tokens = -1;           // 0 clean, 1 corrupt
+  std::map<int, std::unique_ptr<DeviceBuf>> target_cache;  // per source node (per-edge policies)
+  Trie full;
+  // comm
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  // stats/options
+  cqg_stats stats{};
+  int64_t opt_exact = 0;
+  int64_t opt_mem_budget = 0;
+
+  Engine(const cqg_config& c) : g(c) {}
+  ~Engine() {
+    if (comm) ncclCommDestroy(comm);
+    if (h_stage) cudaFreeHost(h_stage);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  size_t segf(int nb) const { return (size_t)nb * g.S * g.D; }
+
+  float* scratch(const std::string& name, size_t floats) {
+    auto& b = pool[name];
+    if (!b) b = std::make_unique<DeviceBuf>();
+    b->ensure(std::max<size_t>(floats, 1) * sizeof(float));
+    return b->as<float>();
+  }
+
+  const float* zeros(size_t floats) {
+    if (zero.bytes < floats * 4) {
+      zero.ensure(floats * 4);
+      CK(cudaMemsetAsync(zero.p, 0, zero.bytes, st));
+    }
+    return zero.as<float>();
+  }
+
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    const size_t bytes = ((std::max<size_t>(v.size(), 1) * sizeof(T)) + 15) & ~size_t(15);
+    if (bytes > stage_cap) {
+      CK(cudaStreamSynchronize(st));
+      if (h_stage) cudaFreeHost(h_stage);
+      stage_cap = std::max(bytes, stage_cap * 2);
+      CK(cudaMallocHost(&h_stage, stage_cap));
+      d_stage.ensure(stage_cap);
+      stage_off = 0;
+    }
+    if (stage_off + bytes > stage_cap) {
+      CK(cudaStreamSynchronize(st));
+      stage_off = 0;
+    }
+    if (!v.empty()) std::memcpy(h_stage + stage_off, v.data(), v.size() * sizeof(T));
+    CK(cudaMemcpyAsync(d_stage.as<char>() + stage_off, h_stage + stage_off, bytes,
+                       cudaMemcpyHostToDevice, st));
+    stats.h2d_bytes += (int64_t)bytes;
+    T* d = reinterpret_cast<T*>(d_stage.as<char>() + stage_off);
+    stage_off += bytes;
+    return d;
+  }
+
+  void launched(int n = 1) { stats.kernel_launches += n; }
+
+  // ---- weights -------------------------------------------------------------
+  const float* W(int m, int prec, int mode) {
+    if (prec == 2) return master[m]->as<float>();
+    const int key = prec == 1 ? 1 : (mode == 0 ? 0 : 2);
+    auto& v = img[key];
+    if (v.empty()) v.resize(master.size());
+    if (!v[m]) {
+      v[m] = std::make_unique<DeviceBuf>();
+      v[m]->ensure(msize[m] * 4);
+      build_image(m, key, v[m]->as<float>());
+    }
+    return v[m]->as<float>();
+  }
+
+  int mat_kind(int m) const {  // returns which-index (see Graph::mat)
+    const int per = 6 + (g.mlp ? 4 : 0);
+    if (m == 0) return 0;
+    if (m == 1) return 1;
+    const int n = g.n_mats();
+    if (m == n - 3) return 12;
+    if (m == n - 2) return 13;
+    if (m == n - 1) return 14;
+    return 2 + (m - 2) % per;
+  }
+
+  void build_image(int m, int key, float* out) {
+    const float* in = master[m]->as<float>();
+    if (key == 0) launch_quantize(in, out, msize[m], 0, st);
+    else if (key == 1) launch_quantize(in, out, msize[m], 1, st);
+    else {
+      // quantize_rtn4_matrix (model.cpp:445-469)
+      const int w = mat_kind(m);
+      if (w == 4 || w == 5 || w == 6)
+        launch_rtn_groups(in, out, g.H, g.dk, g.D, g.dk, g.D, 4, st);
+      else if (w == 7)
+        launch_rtn_groups(in, out, g.H, (int64_t)g.dk * g.D, g.dk, g.D, g.D, 4, st);
+      else
+        launch_rtn_groups(in, out, 1, 0, 1, (int)msize[m], (int)msize[m], 4, st);
+    }
+    launched();
+  }
+
+  // ---- launch helpers --------------------------------------------------------
+  void fold(const std::vector<FoldOp>& ops, const std::vector<FoldProg>& progs, size_t elems) {
+    if (progs.empty()) return;
+    launch_fold(upload(ops), upload(progs), (int)progs.size(), (int64_t)elems, st);
+    launched();
+  }
+  void ln(const std::vector<LnJob>& jobs, int l_gamma, int l_beta, int prec) {
+    if (jobs.empty()) return;
+    int mx = 0;
+    for (auto& j : jobs) mx = std::max(mx, j.rows);
+    launch_layernorm(upload(jobs), (int)jobs.size(), mx, master[l_gamma]->as<float>(),
+                     master[l_beta]->as<float>(), g.D, prec, st);
+    launched();
+  }
+  void gemm(const std::vector<GemmJob>& jobs) {
+    if (jobs.empty()) return;
+    std::vector<int> ts(jobs.size());
+    int total = 0;
+    for (size_t i = 0; i < jobs.size(); ++i) {
+      ts[i] = total;
+      total += gemm_exact_tiles(jobs[i].M, jobs[i].N);
+    }
+    launch_gemm_exact(upload(jobs), upload(ts), (int)jobs.size(), total, st);
+    launched();
+  }
+  void attn(const std::vector<AttnJob>& jobs, int nb) {
+    if (jobs.empty()) return;
+    launch_attention(upload(jobs), (int)jobs.size(), nb, g.S, g.dk, st);
+    launched();
+  }
+
+  void check_policy(const Policy& P) {
+    if (P.mode == 1 && (P.att == 0 || P.mlp == 0 || P.emb == 0 || P.unemb == 0))
+      throw Error(1, "low_mode Rtn4 activations are not supported on the GPU path yet");
+    if (P.th_l >= g.L || P.th_h >= g.H || (P.th_l >= 0 && P.th_h < 0))
+      throw Error(1, "forward: target head out of range");
+    if (P.tm >= 0 && (!g.mlp || P.tm >= g.L)) throw Error(1, "forward: target mlp out of range");
+  }
+
+  // ---- node computations ----------------------------------------------------
+  // attention layer (model.cpp:622-718) for a list of (input, head, output)
+  void run_heads(int l, const Policy& P, const std::vector<HeadIO>& jobs, int nb) {
+    if (jobs.empty()) return;
+    const int RB = nb * g.S, D = g.D, dk = g.dk;
+    const size_t SEG = segf(nb);
+    const int p_low = P.att;
+    std::map<const float*, int> uidx;
+    std::vector<const float*> uin;
+    std::vector<int> u_of(jobs.size()), xln_of;
+    std::vector<char> need_xln;
+    for (size_t j = 0; j < jobs.size(); ++j) {
+      auto it = uidx.find(jobs[j].in);
+      if (it == uidx.end()) {
+        it = uidx.emplace(jobs[j].in, (int)uin.size()).first;
+        uin.push_back(jobs[j].in);
+        need_xln.push_back(0);
+      }
+      u_of[j] = it->second;
+      if (P.th_l == l && P.th_h == jobs[j].head) need_xln[it->second] = 1;
+    }
+    xln_of.assign(uin.size(), -1);
+    int n_xln = 0;
+    for (size_t u = 0; u < uin.size(); ++u)
+      if (need_xln[u]) xln_of[u] = n_xln++;
+    float* xq = scratch("h_xq", uin.size() * SEG);
+    float* xln = scratch("h_xln", std::max(n_xln, 1) * SEG);
+    std::vector<LnJob> lj;
+    for (size_t u = 0; u < uin.size(); ++u)
+      lj.push_back({uin[u], xln_of[u] >= 0 ? xln + xln_of[u] * SEG : nullptr, xq + u * SEG, RB, D});
+    ln(lj, g.mat(2, l), g.mat(3, l), p_low);
+
+    const size_t per = (size_t)RB * dk;
+    float* qkv = scratch("h_qkv", jobs.size() * 3 * per);
+    float* z = scratch("h_z", jobs.size() * per);
+    std::vector<GemmJob> gj;
+    std::vector<AttnJob> aj;
+    for (size_t j = 0; j < jobs.size(); ++j) {
+      const int h = jobs[j].head;
+      const bool target = P.th_l == l && P.th_h == h;
+      for (int c = 0; c < 3; ++c) {
+        const int m = g.mat(4 + c, l);
+        GemmJob q{};
+        q.A = target ? xln + xln_of[u_of[j]] * SEG : xq + u_of[j] * SEG;
+        q.B = (target ? master[m]->as<float>() : W(m, p_low, P.mode)) + h * dk;
+        q.C = qkv + (j * 3 + c) * per;
+        q.M = RB, q.N = dk, q.K = D, q.lda = D, q.ldb = D, q.ldc = dk;
+        q.prec = target ? 2 : p_low, q.epi = 0;
+        gj.push_back(q);
+      }
+      aj.push_back({qkv + (j * 3) * per, qkv + (j * 3 + 1) * per, qkv + (j * 3 + 2) * per,
+                    z + j * per, dk, target ? 2 : p_low});
+    }
+    gemm(gj);
+    attn(aj, nb);
+    const float* wo = W(g.mat(7, l), P.wo_precision(l), P.mode);
+    gj.clear();
+    for (size_t j = 0; j < jobs.size(); ++j) {
+      const int h = jobs[j].head;
+      const bool target = P.th_l == l && P.th_h == h;
+      GemmJob o{};
+      o.A = z + j * per, o.B = wo + (size_t)h * dk * D, o.C = jobs[j].out;
+      o.M = RB, o.N = D, o.K = dk, o.lda = dk, o.ldb = D, o.ldc = D;
+      o.prec = target ? 2 : p_low, o.epi = 0;
+      gj.push_back(o);
+    }
+    gemm(gj);
+  }
+
+  // MLP (model.cpp:720-739)
+  void run_mlp(int l, const Policy& P, const std::vector<SegIO>& jobs, int nb) {
+    if (jobs.empty()) return;
+    const int RB = nb * g.S, D = g.D;
+    const size_t SEG = segf(nb);
+    const int node = g.stage_nodes[2 + 2 * l][0];
+    const int p = P.precision_of(g, node);
+    float* xq = scratch("m_xq", jobs.size() * SEG);
+    float* hid = scratch("m_hid", jobs.size() * SEG * 4);
+    std::vector<LnJob> lj;
+    for (size_t j = 0; j < jobs.size(); ++j) lj.push_back({jobs[j].in, nullptr, xq + j * SEG, RB, D});
+    ln(lj, g.mat(8, l), g.mat(9, l), p);
+    const float* win = W(g.mat(10, l), p, P.mode);
+    const float* wout = W(g.mat(11, l), p, P.mode);
+    std::vector<GemmJob> g1, g2;
+    for (size_t j = 0; j < jobs.size(); ++j) {
+      GemmJob a{};
+      a.A = xq + j * SEG, a.B = win, a.C = hid + j * SEG * 4;
+      a.M = RB, a.N = 4 * D, a.K = D, a.lda = D, a.ldb = 4 * D, a.ldc = 4 * D, a.prec = p, a.epi = 1;
+      g1.push_back(a);
+      GemmJob b{};
+      b.A = hid + j * SEG * 4, b.B = wout, b.C = jobs[j].out;
+      b.M = RB, b.N = D, b.K = 4 * D, b.lda = 4 * D, b.ldb = D, b.ldc = D, b.prec = p, b.epi = 0;
+      g2.push_back(b);
+    }
+    gemm(g1);
+    gemm(g2);
+  }
+
+  // unembed (model.cpp:741-753): all_rows=false computes only row S-1 of
+  // each item (the only row patched_divergence reads, patching.cpp:155-157).
+  void run_unembed(const Policy& P, const std::vector<SegIO>& jobs, int nb, bool all_rows) {
+    if (jobs.empty()) return;
+    const int rows = all_rows ? nb * g.S : nb, D = g.D, V = g.V;
+    const int p = P.unemb;
+    float* xq = scratch("u_xq", jobs.size() * (size_t)rows * D);
+    std::vector<LnJob> lj;
+    for (size_t j = 0; j < jobs.size(); ++j)
+      lj.push_back({jobs[j].in + (all_rows ? 0 : (size_t)(g.S - 1) * D), nullptr,
+                    xq + j * (size_t)rows * D, rows, all_rows ? D : g.S * D});
+    ln(lj, g.mat(12, 0), g.mat(13, 0), p);
+    const float* wu = W(g.mat(14, 0), p, P.mode);
+    std::vector<GemmJob> gj;
+    for (size_t j = 0; j < jobs.size(); ++j) {
+      GemmJob a{};
+      a.A = xq + j * (size_t)rows * D, a.B = wu, a.C = jobs[j].out;
+      a.M = rows, a.N = V, a.K = D, a.lda = D, a.ldb = V, a.ldc = V, a.prec = p, a.epi = 0;
+      gj.push_back(a);
+    }
+    gemm(gj);
+  }
+
+  void run_embed(const Policy& P, const int* d_tok, float* out, int nb) {
+    launch_embed(d_tok, W(g.mat(0, 0), P.emb, P.mode), W(g.mat(1, 0), P.emb, P.mode), out, nb, g.S,
+                 g.D, P.emb, st);
+    launched();
+  }
+
+  // ---- a full (or suffix) forward over a trie: the baseline runs ----------
+  void prepare_run(Run& R, const Trie& T, int nb, bool all_rows) {
+    R.nb = nb;
+    R.seg = segf(nb);
+    R.out.ensure((size_t)g.N * R.seg * 4);
+    R.trie.ensure((size_t)T.size() * R.seg * 4);
+    R.logits.ensure((size_t)(all_rows ? nb * g.S : nb) * g.V * 4);
+    R.lse.ensure((size_t)nb * 8);
+  }
+
+  const float* input_of(const Trie& T, const Run& R, int w) {
+    return T.rec_in[w] == 0 ? zeros(R.seg) : R.t(T.rec_in[w]);
+  }
+
+  void forward_run(Run& R, const Trie& T, const Policy& P, const int* d_tok, int sigma0,
+                   bool all_rows, int* d_nan) {
+    for (int s = sigma0; s < g.n_stages; ++s) {
+      const auto& nodes = g.stage_nodes[s];
+      const int k = g.kind[nodes[0]];
+      if (k == kEmbed) {
+        run_embed(P, d_tok, R.o(0), R.nb);
+      } else if (k == kHead) {
+        std::vector<HeadIO> hj;
+        for (int w : nodes) hj.push_back({input_of(T, R, w), g.head[w], R.o(w)});
+        run_heads(g.layer[nodes[0]], P, hj, R.nb);
+      } else if (k == kMlp) {
+        run_mlp(g.layer[nodes[0]], P, {{input_of(T, R, nodes[0]), R.o(nodes[0])}}, R.nb);
+      } else {
+        run_unembed(P, {{input_of(T, R, g.unembed), R.logits.as<float>()}}, R.nb, all_rows);
+        if (!all_rows) {
+          launch_lse(R.logits.as<float>(), R.nb, g.V, R.lse.as<double>(), d_nan, st);
+          launched();
+        }
+      }
+      // trie values whose last source is at this stage
+      std::vector<FoldOp> ops;
+      const float* prev = nullptr;
+      for (int t : T.by_stage[s]) {
+        const int p = T.parent[t];
+        const float* a = p == 0 ? nullptr : R.t(p);
+        if (a && a == prev) a = CQG_REG_PREV;
+        ops.push_back({a, R.o(T.src[t]), R.t(t)});
+        prev = R.t(t);
+      }
+      if (!ops.empty()) fold(ops, {{0, (int)ops.size()}}, R.seg);
+    }
+  }
+
+  // ---- patch values (prepare_policy's full-graph runs, patching.cpp:171-185)
+  const int* tokens(int which) const { return which == 0 ? d_clean.as<int>() : d_corrupt.as<int>(); }
+
+  void ensure_patch_run(const Policy& base, int which, int* d_nan) {
+    if (patch_valid && patch_policy == base && patch_tokens == which) return;
+    prepare_run(patch_run, full, B, false);
+    forward_run(patch_run, full, base, tokens(which), 0, false, d_nan);
+    patch_valid = true;
+    patch_policy = base;
+    patch_tokens = which;
+    target_cache.clear();
+  }
+
+  // out[s] of the full-graph run under policy_for_edge (target = s)
+  const float* patch_value(int s, const Policy& ps, bool per_edge) {
+    if (!per_edge || g.kind[s] == kEmbed) return patch_run.o(s);
+    auto& c = target_cache[s];
+    if (c) return c->as<float>();
+    c = std::make_unique<DeviceBuf>();
+    c->ensure(patch_run.seg * 4);
+    const float* in = input_of(full, patch_run, s);
+    if (g.kind[s] == kHead) run_heads(g.layer[s], ps, {{in, g.head[s], c->as<float>()}}, B);
+    else run_mlp(g.layer[s], ps, {{in, c->as<float>()}}, B);
+    return c->as<float>();
+  }
+
+  // ---- the patched passes of one policy group -------------------------------
+  struct EdgePlan {
+    int e, s, v, sv;
+    const float* pv;
+    std::vector<int8_t> nchg, tchg, virt;
+    std::vector<int> nslot, tslot;
+    int n_slots = 0;
+    float* base_ptr = nullptr;  // sval then slots
+    float* sval() const { return base_ptr; }
+    float* slot(int k, size_t seg) const { return base_ptr + (size_t)(1 + k) * seg; }
+  };
+
+  void plan_edge(EdgePlan& P, const Trie& T, bool loss) {
+    const int N = g.N, TS = T.size();
+    P.nchg.assign(N, 0);
+    P.tchg.assign(TS, 0);
+    P.virt.assign(TS, 0);
+    P.nslot.assign(N, -1);
+    P.tslot.assign(TS, -1);
+    P.nchg[P.v] = 1;
+    const int last = loss ? g.n_stages - 1 : P.sv;
+    for (int s = P.sv; s <= last; ++s) {
+      if (s > P.sv)
+        for (int w : g.stage_nodes[s]) {
+          const int ri = T.rec_in[w];
+          P.nchg[w] = (ri != 0 && P.tchg[ri]) ? 1 : 0;
+        }
+      if (s < last || loss)
+        for (int t : T.by_stage[s])
+          P.tchg[t] = (P.nchg[T.src[t]] || (T.parent[t] != 0 && P.tchg[T.parent[t]])) ? 1 : 0;
+    }
+    if (!loss) {  // act_diff: only the destination's output is needed
+      std::fill(P.tchg.begin(), P.tchg.end(), 0);
+      std::fill(P.nchg.begin(), P.nchg.end(), 0);
+      P.nchg[P.v] = 1;
+    }
+    // consumers of changed trie values
+    std::vector<int> ncons(TS, 0), only_child(TS, -1);
+    for (int t = 1; t < TS; ++t)
+      if (P.tchg[t] && T.parent[t] != 0 && P.tchg[T.parent[t]]) {
+        ncons[T.parent[t]]++;
+        only_child[T.parent[t]] = t;
+      }
+    for (int w = 0; w < N; ++w)
+      if (P.nchg[w] && g.stage[w] > P.sv && T.rec_in[w] != 0) ncons[T.rec_in[w]] += 2;  // never virtual
+    // program order per stage -> virtual (register-only) values
+    for (int s = P.sv; s <= last && loss; ++s) {
+      int prev = -1;
+      for (int t : T.by_stage[s]) {
+        if (!P.tchg[t]) continue;
+        if (prev >= 0 && ncons[prev] == 1 && only_child[prev] == t) P.virt[prev] = 1;
+        prev = t;
+      }
+    }
+    // liveness over time 2*stage (node compute) / 2*stage+1 (fold)
+    struct Val { int def, last, kind, id; };
+    std::vector<Val> vals;
+    for (int w = 0; w < N; ++w) {
+      if (!P.nchg[w] || w == g.unembed) continue;
+      vals.push_back({2 * g.stage[w], loss ? 2 * g.stage[w] + 1 : 2 * g.stage[w], 0, w});
+    }
+    std::vector<int> lastuse(TS, -1);
+    for (int t = 1; t < TS; ++t)
+      if (P.tchg[t] && T.parent[t] != 0 && P.tchg[T.parent[t]])
+        lastuse[T.parent[t]] = std::max(lastuse[T.parent[t]], 2 * g.stage[T.src[t]] + 1);
+    for (int w = 0; w < N; ++w)
+      if (P.nchg[w] && g.stage[w] > P.sv && T.rec_in[w] != 0)
+        lastuse[T.rec_in[w]] = std::max(lastuse[T.rec_in[w]], 2 * g.stage[w]);
+    for (int t = 1; t < TS; ++t) {
+      if (!P.tchg[t] || P.virt[t]) continue;
+      const int def = 2 * g.stage[T.src[t]] + 1;
+      vals.push_back({def, std::max(def, lastuse[t]), 1, t});
+    }
+    std::sort(vals.begin(), vals.end(), [](const Val& a, const Val& b) { return a.def < b.def; });
+    std::vector<std::pair<int, int>> busy;  // (last, slot)
+    std::vector<int> freel;
+    int n = 0;
+    for (const Val& x : vals) {
+      for (size_t i = 0; i < busy.size();) {
+        if (busy[i].first < x.def) {
+          freel.push_back(busy[i].second);
+          busy[i] = busy.back();
+          busy.pop_back();
+        } else {
+          ++i;
+        }
+      }
+      int sl;
+      if (!freel.empty()) {
+        sl = freel.back();
+        freel.pop_back();
+      } else {
+        sl = n++;
+      }
+      busy.push_back({x.last, sl});
+      (x.kind == 0 ? P.nslot[x.id] : P.tslot[x.id]) = sl;
+    }
+    P.n_slots = n;
+  }
+
+  // Scores (sum over local items, item order) for the edges of one group.
+  void run_passes(const Trie& T, const Policy& P, const Run& R, std::vector<EdgePlan>& plans,
+                  bool loss, double* d_d /* [n][nb] */, int* d_nan) {
+    const int nb = R.nb;
+    const size_t SEG = R.seg;
+    const int V = g.V;
+    // arena: sval + slots per edge
+    size_t total = 0;
+    for (auto& p : plans) total += (size_t)(1 + p.n_slots) * SEG;
+    float* arena = scratch("p_arena", total);
+    size_t off = 0;
+    for (auto& p : plans) {
+      p.base_ptr = arena + off;
+      off += (size_t)(1 + p.n_slots) * SEG;
+    }
+    // 1) patched receiver inputs: fold along v's source path with s -> pv
+    {
+      std::vector<FoldOp> ops;
+      std::vector<FoldProg> progs;
+      for (auto& p : plans) {
+        std::vector<int> path;
+        for (int t = T.rec_in[p.v]; t != 0; t = T.parent[t]) path.push_back(t);
+        std::reverse(path.begin(), path.end());
+        size_t k = 0;
+        while (k < path.size() && T.src[path[k]] != p.s) ++k;
+        if (k == path.size()) throw Error(2, "internal: source missing from receiver path");
+        const int b = (int)ops.size();
+        for (size_t i = k; i < path.size(); ++i) {
+          const int t = path[i];
+          const float* a;
+          if (i == k) a = T.parent[t] == 0 ? nullptr : R.t(T.parent[t]);
+          else a = CQG_REG_PREV;
+          const float* bsrc = (i == k) ? p.pv : R.o(T.src[t]);
+          ops.push_back({a, bsrc, i + 1 == path.size() ? p.sval() : nullptr});
+        }
+        progs.push_back({b, (int)ops.size()});
+      }
+      fold(ops, progs, SEG);
+    }
+    int smin = g.n_stages, smax = 0;
+    for (auto& p : plans) smin = std::min(smin, p.sv), smax = std::max(smax, p.sv);
+    const int last = loss ? g.n_stages - 1 : smax;
+    float* logits = nullptr;
+    std::vector<int> unembed_edges;  // plan indices whose logits were computed
+    for (int s = smin; s <= last; ++s) {
+      const auto& nodes = g.stage_nodes[s];
+      const int k = g.kind[nodes[0]];
+      std::vector<HeadIO> hj;
+      std::vector<SegIO> mj;
+      std::vector<int> uj;
+      for (size_t pi = 0; pi < plans.size(); ++pi) {
+        auto& p = plans[pi];
+        if (p.sv > s) continue;
+        for (int w : nodes) {
+          if (!p.nchg[w]) continue;
+          const float* in = (w == p.v) ? p.sval() : p.slot(p.tslot[T.rec_in[w]], SEG);
+          if (k == kHead) hj.push_back({in, g.head[w], p.slot(p.nslot[w], SEG)});
+          else if (k == kMlp) mj.push_back({in, p.slot(p.nslot[w], SEG)});
+          else if (k == kUnembed) {
+            uj.push_back((int)pi);
+            mj.push_back({in, nullptr});
+          }
+        }
+      }
+      if (k == kHead) run_heads(g.layer[nodes[0]], P, hj, nb);
+      else if (k == kMlp) run_mlp(g.layer[nodes[0]], P, mj, nb);
+      else if (k == kUnembed && !mj.empty()) {
+        const bool all_rows = !loss;
+        const size_t rows = all_rows ? (size_t)nb * g.S : (size_t)nb;
+        logits = scratch("p_logits", mj.size() * rows * V);
+        for (size_t j = 0; j < mj.size(); ++j) mj[j].out = logits + j * rows * V;
+        run_unembed(P, mj, nb, all_rows);
+        unembed_edges = uj;
+      }
+      if (!loss) {  // act_diff for edges starting here (patching.cpp:249-256)
+        std::vector<RmsJob> rj;
+        for (size_t pi = 0; pi < plans.size(); ++pi) {
+          auto& p = plans[pi];
+          if (p.sv != s) continue;
+          for (int i = 0; i < nb; ++i) {
+            RmsJob r{};
+            if (p.v == g.unembed) {
+              size_t j = std::find(unembed_edges.begin(), unembed_edges.end(), (int)pi) - unembed_edges.begin();
+              const size_t n = (size_t)g.S * V;
+              r.a = logits + j * (size_t)nb * n + i * n;
+              r.b = R.logits.as<float>() + i * n;
+              r.n = (int64_t)n;
+            } else {
+              r.a = p.slot(p.nslot[p.v], SEG) + (size_t)i * g.S * g.D;
+              r.b = R.o(p.v) + (size_t)i * g.S * g.D;
+              r.n = (int64_t)g.S * g.D;
+            }
+            r.out = d_d + pi * nb + i;
+            rj.push_back(r);
+          }
+        }
+        if (!rj.empty()) {
+          launch_rms(upload(rj), (int)rj.size(), st);
+          launched();
+        }
+        continue;
+      }
+      // fold: changed trie values whose last source is at this stage
+      std::vector<FoldOp> ops;
+      std::vector<FoldProg> progs;
+      for (auto& p : plans) {
+        if (p.sv > s) continue;
+        const int b = (int)ops.size();
+        const float* prev = nullptr;
+        for (int t : T.by_stage[s]) {
+          if (!p.tchg[t]) continue;
+          const int pa = T.parent[t];
+          const float* a;
+          if (pa == 0) a = nullptr;
+          else if (p.tchg[pa]) a = p.virt[pa] ? CQG_REG_PREV : p.slot(p.tslot[pa], SEG);
+          else a = R.t(pa);
+          if (a != nullptr && a != CQG_REG_PREV && a == prev) a = CQG_REG_PREV;
+          const int sn = T.src[t];
+          const float* bsrc = p.nchg[sn] ? p.slot(p.nslot[sn], SEG) : R.o(sn);
+          float* dst = p.virt[t] ? nullptr : p.slot(p.tslot[t], SEG);
+          ops.push_back({a, bsrc, dst});
+          prev = dst;
+        }
+        if ((int)ops.size() > b) progs.push_back({b, (int)ops.size()});
+      }
+      fold(ops, progs, SEG);
+    }
+    if (loss) {
+      // zero for edges whose change never reaches the unembed
+      CK(cudaMemsetAsync(d_d, 0, sizeof(double) * plans.size() * nb, st));
+      if (!unembed_edges.empty()) {
+        const int rows = (int)unembed_edges.size() * nb;
+        std::vector<int> item_of(rows);
+        for (int r = 0; r < rows; ++r) item_of[r] = r % nb;
+        double* tmp = reinterpret_cast<double*>(scratch("p_kl", (size_t)rows * 2));
+        if (metric == 0)
+          launch_kl(logits, R.logits.as<float>(), R.lse.as<double>(), upload(item_of), rows, V, tmp,
+                    d_nan, st);
+        else
+          launch_logitdiff(logits, R.logits.as<float>(), upload(item_of), d_ans.as<int>(),
+                           d_dis.as<int>(), rows, V, tmp, d_nan, st);
+        launched();
+        for (size_t j = 0; j < unembed_edges.size(); ++j)
+          CK(cudaMemcpyAsync(d_d + (size_t)unembed_edges[j] * nb, tmp + j * nb, sizeof(double) * nb,
+                             cudaMemcpyDeviceToDevice, st));
+      }
+    }
+  }
+
+  size_t mem_budget() {
+    if (opt_mem_budget > 0) return (size_t)opt_mem_budget;
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    return fr / 3;
+  }
+
+  size_t edge_bytes(const EdgePlan& p, int nb) const {
+    const size_t SEG = segf(nb);
+    // arena + per-edge scratch of the widest step (heads: xq + qkv + z; mlp: xq + hid; logits)
+    size_t scratch_b = std::max({SEG + (size_t)g.H * 4 * nb * g.S * g.dk, 5 * SEG,
+                                 (size_t)nb * g.S * g.V});
+    return ((size_t)(1 + p.n_slots) * SEG + scratch_b) * 4;
+  }
+
+  // ---- public operations ------------------------------------------------------
+  void set_dataset(const int* clean, const int* corrupt, const int* ans, const int* dis, int n,
+                   int off, int total, int met) {
+    // validate_dataset (patching.cpp:64-81)
+    if (n < 1) throw Error(1, "validate_dataset: empty dataset");
+    if (met != 0 && met != 1) throw Error(1, "metric must be 0 (kl) or 1 (logitdiff)");
+    for (int i = 0; i < n; ++i) {
+      const std::string at = "validate_dataset: item " + std::to_string(off + i);
+      for (int t = 0; t < g.S; ++t) {
+        if (clean[i * g.S + t] < 0 || clean[i * g.S + t] >= g.V)
+          throw Error(1, at + ": clean token out of range");
+        if (corrupt[i * g.S + t] < 0 || corrupt[i * g.S + t] >= g.V)
+          throw Error(1, at + ": corrupt token out of range");
+      }
+      if (ans[i] < 0 || ans[i] >= g.V || dis[i] < 0 || dis[i] >= g.V)
+        throw Error(1, at + ": answer tokens out of range");
+      if (ans[i] == dis[i]) throw Error(1, at + ": answer equals distractor");
+    }
+    if (total < n || off < 0 || off + n > total) throw Error(1, "set_dataset: bad shard bounds");
+    B = n, item_off = off, item_total = total, metric = met;
+    d_clean.ensure((size_t)n * g.S * 4);
+    d_corrupt.ensure((size_t)n * g.S * 4);
+    d_ans.ensure((size_t)n * 4);
+    d_dis.ensure((size_t)n * 4);
+    CK(cudaMemcpyAsync(d_clean.p, clean, (size_t)n * g.S * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_corrupt.p, corrupt, (size_t)n * g.S * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_ans.p, ans, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_dis.p, dis, (size_t)n * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    patch_valid = false;
+    target_cache.clear();
+  }
+
+  void score_edges(const uint8_t* mask, const int* edge_ids, int n, const Policy& base,
+                   bool per_edge, int mode, double* out) {
+    auto t0 = std::chrono::steady_clock::now();
+    stats = cqg_stats{};
+    if (B == 0) throw Error(1, "score_edges: no dataset (call cqg_set_dataset)");
+    if (mode != 0 && mode != 1) throw Error(1, "score_mode must be 0 (loss) or 1 (act)");
+    check_policy(base);
+    for (int i = 0; i < n; ++i) {
+      if (edge_ids[i] < 0 || edge_ids[i] >= g.E) throw Error(1, "forward: patch references unknown edge");
+      if (!mask[edge_ids[i]])
+        throw Error(1, "forward: patch references masked edge " + std::to_string(edge_ids[i]));
+    }
+    const bool loss = mode == 0;
+    DeviceBuf& nanbuf = *pool_buf("nan", 4);
+    int* d_nan = nanbuf.as<int>();
+    CK(cudaMemsetAsync(d_nan, 0, 4, st));
+    Trie T;
+    T.build(g, mask);
+    if (full.size() == 0) full.build(g, nullptr);
+    const int base_tok = loss ? 0 : 1, patch_tok = loss ? 1 : 0;
+    ensure_patch_run(base, patch_tok, d_nan);
+
+    // groups
+    std::map<int, std::vector<int>> by_src;  // source -> indices into edge_ids
+    for (int i = 0; i < n; ++i) by_src[per_edge ? g.esrc[edge_ids[i]] : -1].push_back(i);
+    std::vector<int> order;
+    for (auto& kv : by_src) order.push_back(kv.first);
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+      const int sa = a < 0 ? 0 : g.stage[a], sb = b < 0 ? 0 : g.stage[b];
+      return sa != sb ? sa > sb : a > b;
+    });
+    bool need_all_rows = false;
+    if (!loss)
+      for (int i = 0; i < n; ++i) need_all_rows |= g.edst[edge_ids[i]] == g.unembed;
+    prepare_run(base_run, T, B, need_all_rows);
+    auto tb = std::chrono::steady_clock::now();
+    forward_run(base_run, T, base, tokens(base_tok), 0, need_all_rows, d_nan);
+    double ms_base = 0, ms_pass = 0;
+    std::vector<double> sums(n, 0.0);
+    std::vector<double> hd;
+    DeviceBuf& dd = *pool_buf("d_scores", 8);
+    for (int src : order) {
+      const auto& idx = by_src[src];
+      const Policy P = per_edge ? policy_for_edge(g, edge_ids[idx[0]], base) : base;
+      check_policy(P);
+      if (per_edge && !(P == base)) {
+        tb = std::chrono::steady_clock::now();
+        forward_run(base_run, T, P, tokens(base_tok), g.stage[src], need_all_rows, d_nan);
+      } else if (per_edge && src >= 0 && g.kind[src] == kEmbed) {
+        forward_run(base_run, T, P, tokens(base_tok), 0, need_all_rows, d_nan);
+      }
+      CK(cudaStreamSynchronize(st));
+      auto tp = std::chrono::steady_clock::now();
+      ms_base += std::chrono::duration<double, std::milli>(tp - tb).count();
+      // plans, batched under the memory budget
+      std::vector<EdgePlan> plans(idx.size());
+      for (size_t k = 0; k < idx.size(); ++k) {
+        const int e = edge_ids[idx[k]];
+        plans[k].e = e, plans[k].s = g.esrc[e], plans[k].v = g.edst[e], plans[k].sv = g.stage[g.edst[e]];
+        plans[k].pv = patch_value(plans[k].s, policy_for_edge(g, e, base), per_edge);
+        plan_edge(plans[k], T, loss);
+      }
+      std::vector<size_t> ord(idx.size());
+      std::iota(ord.begin(), ord.end(), 0);
+      std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return plans[a].sv < plans[b].sv; });
+      const size_t budget = mem_budget();
+      size_t k0 = 0;
+      while (k0 < ord.size()) {
+        size_t bytes = 0, k1 = k0;
+        while (k1 < ord.size() && (k1 == k0 || bytes + edge_bytes(plans[ord[k1]], B) <= budget)) {
+          bytes += edge_bytes(plans[ord[k1]], B);
+          ++k1;
+        }
+        std::vector<EdgePlan> batch;
+        for (size_t k = k0; k < k1; ++k) batch.push_back(std::move(plans[ord[k]]));
+        dd.ensure(sizeof(double) * batch.size() * B);
+        run_passes(T, P, base_run, batch, loss, dd.as<double>(), d_nan);
+        hd.resize(batch.size() * B);
+        CK(cudaMemcpyAsync(hd.data(), dd.p, sizeof(double) * hd.size(), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        stats.d2h_bytes += (int64_t)(sizeof(double) * hd.size());
+        for (size_t k = k0; k < k1; ++k) {
+          double acc = 0.0;  // delta_l's sequential item sum (patching.cpp:229-238)
+          for (int i = 0; i < B; ++i) acc += hd[(k - k0) * B + i];
+          sums[idx[ord[k]]] = acc;
+        }
+        stats.passes += (int64_t)(k1 - k0) * B;
+        k0 = k1;
+      }
+      tb = std::chrono::steady_clock::now();
+      ms_pass += std::chrono::duration<double, std::milli>(tb - tp).count();
+    }
+    int h_nan = 0;
+    CK(cudaMemcpyAsync(&h_nan, d_nan, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h_nan) throw Error(2, metric == 0 ? "metric_kl: NaN logits" : "metric_logit_diff: NaN logits");
+    if (world > 1) {
+      DeviceBuf& ar = *pool_buf("allreduce", sizeof(double) * std::max(n, 1));
+      CK(cudaMemcpyAsync(ar.p, sums.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+      NK(ncclAllReduce(ar.p, ar.p, (size_t)n, ncclDouble, ncclSum, comm, st));
+      CK(cudaMemcpyAsync(sums.data(), ar.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    for (int i = 0; i < n; ++i) out[i] = sums[i] / (double)item_total;
+    stats.ms_baseline = ms_base;
+    stats.ms_passes = ms_pass;
+    stats.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+
+  DeviceBuf* pool_buf(const std::string& name, size_t bytes) {
+    auto& b = pool[name];
+    if (!b) b = std::make_unique<DeviceBuf>();
+    b->ensure(bytes);
+    return b.get();
+  }
+
+  // Debug forward of one item (model.cpp:556-757) with direct per-receiver
+  // folds (independent of the trie planner; used to cross-check it).
+  void forward_single(const int* tok_host, const uint8_t* mask, const Policy& P, int patch_edge,
+                      const float* patch_host, float* outs_host) {
+    check_policy(P);
+    for (int i = 0; i < g.S; ++i)
+      if (tok_host[i] < 0 || tok_host[i] >= g.V) throw Error(1, "forward: token id out of range");
+    if (patch_edge >= 0) {
+      if (patch_edge >= g.E) throw Error(1, "forward: patch references unknown edge");
+      if (mask && !mask[patch_edge]) throw Error(1, "forward: patch references masked edge " + std::to_string(patch_edge));
+    }
+    const size_t SEG = segf(1);
+    DeviceBuf& outs = *pool_buf("f_outs", (size_t)g.N * SEG * 4);
+    DeviceBuf& ins = *pool_buf("f_ins", (size_t)g.N * SEG * 4);
+    DeviceBuf& lg = *pool_buf("f_logits", (size_t)g.S * g.V * 4);
+    DeviceBuf& tk = *pool_buf("f_tok", (size_t)g.S * 4);
+    DeviceBuf& pv = *pool_buf("f_patch", SEG * 4);
+    CK(cudaMemcpyAsync(tk.p, tok_host, (size_t)g.S * 4, cudaMemcpyHostToDevice, st));
+    if (patch_edge >= 0) CK(cudaMemcpyAsync(pv.p, patch_host, SEG * 4, cudaMemcpyHostToDevice, st));
+    float* O = outs.as<float>();
+    float* I = ins.as<float>();
+    auto input = [&](int w) {
+      std::vector<FoldOp> ops;
+      for (int e : g.in_edges[w]) {
+        if (mask && !mask[e]) continue;
+        const float* b = e == patch_edge ? pv.as<float>() : O + (size_t)g.esrc[e] * SEG;
+        ops.push_back({ops.empty() ? nullptr : CQG_REG_PREV, b, nullptr});
+      }
+      if (ops.empty()) {
+        CK(cudaMemsetAsync(I + (size_t)w * SEG, 0, SEG * 4, st));
+      } else {
+        ops.back().dst = I + (size_t)w * SEG;
+        fold(ops, {{0, (int)ops.size()}}, SEG);
+      }
+      return (const float*)(I + (size_t)w * SEG);
+    };
+    for (int s = 0; s < g.n_stages; ++s) {
+      const auto& nodes = g.stage_nodes[s];
+      const int k = g.kind[nodes[0]];
+      if (k == kEmbed) run_embed(P, tk.as<int>(), O, 1);
+      else if (k == kHead) {
+        std::vector<HeadIO> hj;
+        for (int w : nodes) hj.push_back({input(w), g.head[w], O + (size_t)w * SEG});
+        run_heads(g.layer[nodes[0]], P, hj, 1);
+      } else if (k == kMlp) run_mlp(g.layer[nodes[0]], P, {{input(nodes[0]), O + (size_t)nodes[0] * SEG}}, 1);
+      else run_unembed(P, {{input(g.unembed), lg.as<float>()}}, 1, true);
+    }
+    CK(cudaMemcpyAsync(outs_host, O, (size_t)(g.N - 1) * SEG * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(outs_host + (size_t)(g.N - 1) * SEG, lg.p, (size_t)g.S * g.V * 4,
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+
+  void run_acdc(const cqg_prune& c, int* steps, uint8_t* final_mask, double* last_score, int* n_rec,
+                int* rs, int* re, double* rsc, uint8_t* rk, int cap) {
+    // PruneConfig::validate (acdc.cpp:14-21)
+    if (!(c.tau >= 0.0)) throw Error(1, "PruneConfig: tau must be >= 0");
+    if (c.max_steps < 1) throw Error(1, "PruneConfig: max_steps must be >= 1");
+    if (!(c.min_change_rate >= 0.0)) throw Error(1, "PruneConfig: min_change_rate must be >= 0");
+    if (!(c.act_floor >= 0.0)) throw Error(1, "PruneConfig: act_floor must be >= 0");
+    const Policy base = Policy::from(c.base);
+    std::vector<uint8_t> mask(g.E, 1);
+    std::fill(last_score, last_score + g.E, 0.0);
+    int t = 0, k = 0;
+    bool keep_going = true;
+    do {
+      std::vector<int> order = g.sweep_order(mask);
+      if (c.heads_only)
+        order.erase(std::remove_if(order.begin(), order.end(),
+                                   [&](int e) { return g.kind[g.esrc[e]] != kHead; }),
+                    order.end());
+      if (order.empty()) break;
+      std::vector<double> raw(order.size());
+      score_edges(mask.data(), order.data(), (int)order.size(), base, c.per_edge_policy != 0, c.mode,
+                  raw.data());
+      int removed = 0;
+      for (size_t i = 0; i < order.size(); ++i) {
+        double s = raw[i];
+        if (c.mode == 1 && s < c.act_floor) s = 0.0;
+        const bool keep = !(s < c.tau);
+        if (k < cap) rs[k] = t, re[k] = order[i], rsc[k] = s, rk[k] = keep ? 1 : 0;
+        ++k;
+        last_score[order[i]] = s;
+        if (!keep) {
+          mask[order[i]] = 0;
+          ++removed;
+        }
+      }
+      ++t;
+      const double change_rate = (double)removed / (double)order.size();
+      keep_going = removed > 0 && change_rate > c.min_change_rate;
+    } while (t < c.max_steps && std::count(mask.begin(), mask.end(), 1) > 0 && keep_going);
+    std::copy(mask.begin(), mask.end(), final_mask);
+    *steps = t;
+    *n_rec = k;
+  }
+};
+
+std::unique_ptr<Engine> make_engine(const cqg_config& cfg, const float* const* mats, int device) {
+  auto E = std::make_unique<Engine>(cfg);
+  E->device = device;
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&E->st, cudaStreamNonBlocking));
+  const Graph& g = E->g;
+  const int64_t D = g.D, V = g.V, S = g.S;
+  for (int m = 0; m < g.n_mats(); ++m) {
+    const int w = E->mat_kind(m);
+    int64_t n;
+    switch (w) {
+      case 0: n = V * D; break;
+      case 1: n = S * D; break;
+      case 2: case 3: case 8: case 9: case 12: case 13: n = D; break;
+      case 10: case 11: n = 4 * D * D; break;
+      case 14: n = D * V; break;
+      default: n = D * D;
+    }
+    E->msize.push_back(n);
+    E->master.push_back(std::make_unique<DeviceBuf>());
+    E->master.back()->ensure(n * 4);
+    CK(cudaMemcpy(E->master.back()->p, mats[m], n * 4, cudaMemcpyHostToDevice));
+  }
+  return E;
+}
+
+}  // namespace cqg
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using cqg::Engine;
+using cqg::Error;
+
+struct cqg_ctx {
+  std::unique_ptr<Engine> e;
+};
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    cqg::g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    cqg::g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    cqg::g_err = e.what();
+    return 2;
+  }
+}
+
+extern "C" {
+
+const char* cqg_last_error(void) { return cqg::g_err.c_str(); }
+
+uint64_t cqg_fnv1a64(const void* data, size_t n) {
+  const uint8_t* p = static_cast<const uint8_t*>(data);
+  uint64_t h = 14695981039346656037ull;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+int cqg_create(const cqg_config* cfg, const float* const* mats, int device, cqg_ctx** out) {
+  return guarded([&] {
+    if (!cfg || !mats || !out) throw Error(1, "cqg_create: null argument");
+    auto* c = new cqg_ctx;
+    try {
+      c->e = cqg::make_engine(*cfg, mats, device);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void cqg_destroy(cqg_ctx* ctx) { delete ctx; }
+
+int cqg_set_dataset(cqg_ctx* ctx, const int32_t* clean, const int32_t* corrupt, const int32_t* answer,
+                    const int32_t* distractor, int n_items, int item_offset, int item_total, int metric) {
+  return guarded([&] {
+    if (!ctx) throw Error(1, "null context");
+    ctx->e->set_dataset(clean, corrupt, answer, distractor, n_items, item_offset,
+                        item_total > 0 ? item_total : n_items, metric);
+  });
+}
+
+int cqg_get_unique_id(void* out128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof id);
+  });
+}
+
+int cqg_init_comm(cqg_ctx* ctx, const void* unique_id, int rank, int world) {
+  return guarded([&] {
+    if (!ctx) throw Error(1, "null context");
+    if (world < 1 || rank < 0 || rank >= world) throw Error(1, "cqg_init_comm: bad rank/world");
+    auto& E = *ctx->e;
+    E.rank = rank, E.world = world;
+    if (world == 1) return;
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof id);
+    CK(cudaSetDevice(E.device));
+    NK(ncclCommInitRank(&E.comm, world, id, rank));
+  });
+}
+
+int cqg_score_edges(cqg_ctx* ctx, const uint8_t* mask, const int32_t* edge_ids, int n,
+                    const cqg_policy* base, int per_edge_policy, int score_mode, double* scores_out) {
+  return guarded([&] {
+    if (!ctx || !mask || (!edge_ids && n > 0) || !base || (!scores_out && n > 0))
+      throw Error(1, "cqg_score_edges: null argument");
+    CK(cudaSetDevice(ctx->e->device));
+    ctx->e->score_edges(mask, edge_ids, n, cqg::Policy::from(*base), per_edge_policy != 0, score_mode,
+                        scores_out);
+  });
+}
+
+int cqg_run_acdc(cqg_ctx* ctx, const cqg_prune* cfg, int* steps, uint8_t* final_mask, double* last_score,
+                 int* n_rec, int32_t* rec_step, int32_t* rec_edge, double* rec_score, uint8_t* rec_kept,
+                 int rec_cap) {
+  return guarded([&] {
+    if (!ctx || !cfg) throw Error(1, "cqg_run_acdc: null argument");
+    CK(cudaSetDevice(ctx->e->device));
+    ctx->e->run_acdc(*cfg, steps, final_mask, last_score, n_rec, rec_step, rec_edge, rec_score,
+                     rec_kept, rec_cap);
+  });
+}
+
+int cqg_quantize_matrix(cqg_ctx* ctx, int matrix_index, int precision, int low_mode, float* out_host) {
+  return guarded([&] {
+    if (!ctx) throw Error(1, "null context");
+    auto& E = *ctx->e;
+    if (matrix_index < 0 || matrix_index >= E.g.n_mats()) throw Error(1, "cqg_quantize_matrix: bad matrix index");
+    if (precision < 0 || precision > 2 || low_mode < 0 || low_mode > 1)
+      throw Error(1, "cqg_quantize_matrix: bad precision/mode");
+    CK(cudaSetDevice(E.device));
+    const float* d = E.W(matrix_index, precision, low_mode);
+    CK(cudaMemcpyAsync(out_host, d, E.msize[matrix_index] * 4, cudaMemcpyDeviceToHost, E.st));
+    CK(cudaStreamSynchronize(E.st));
+  });
+}
+
+int cqg_forward(cqg_ctx* ctx, const int32_t* tokens, const uint8_t* mask, const cqg_policy* pol,
+                int patch_edge, const float* patch_value, float* outs_host) {
+  return guarded([&] {
+    if (!ctx || !tokens || !pol || !outs_host) throw Error(1, "cqg_forward: null argument");
+    CK(cudaSetDevice(ctx->e->device));
+    ctx->e->forward_single(tokens, mask, cqg::Policy::from(*pol), patch_edge, patch_value, outs_host);
+  });
+}
+
+int cqg_graph_info(const cqg_config* cfg, int* n_nodes, int* n_edges) {
+  return guarded([&] {
+    cqg::Graph g(*cfg);
+    *n_nodes = g.N;
+    *n_edges = g.E;
+  });
+}
+
+int cqg_graph_edges(const cqg_config* cfg, int32_t* src, int32_t* dst) {
+  return guarded([&] {
+    cqg::Graph g(*cfg);
+    for (int e = 0; e < g.E; ++e) src[e] = g.esrc[e], dst[e] = g.edst[e];
+  });
+}
+
+int cqg_last_stats(cqg_ctx* ctx, cqg_stats* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw Error(1, "null argument");
+    *out = ctx->e->stats;
+  });
+}
+
+int cqg_set_option(cqg_ctx* ctx, const char* key, int64_t value) {
+  return guarded([&] {
+    if (!ctx || !key) throw Error(1, "null argument");
+    std::string k(key);
+    if (k == "exact") ctx->e->opt_exact = value;
+    else if (k == "mem_budget") ctx->e->opt_mem_budget = value;
+    else throw Error(1, "cqg_set_option: unknown key " + k);
+  });
+}
+
+}  // extern "C"

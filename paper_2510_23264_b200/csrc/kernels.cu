@@ -1,0 +1,533 @@
+// kernels.cu — exact-semantics sm_100a kernels of the patched forward.
+//
+// Every kernel reproduces the reference's FP32 operation order (no FMA
+// contraction: explicit _rn intrinsics) so that its outputs are bit-equal to
+// proj/src/kernels.cpp + model.cpp on the same inputs. These are the building
+// blocks of the exact path and the fallback of the tensor-core GEMMs
+// (gemm_tc.cu).
+#include <float.h>
+#include <math.h>
+
+#include "kernels.h"
+#include "numerics.cuh"
+
+namespace cqg {
+
+// ---------------------------------------------------------------------------
+// K2a: fold (sum_inputs, model.cpp:537-552). HBM-bound, float4-vectorised.
+// ---------------------------------------------------------------------------
+template <bool VEC>
+__global__ void __launch_bounds__(256) fold_kernel(const FoldOp* __restrict__ ops,
+                                                   const FoldProg* __restrict__ progs,
+                                                   int64_t n_elems) {
+  const FoldProg p = progs[blockIdx.y];
+  if (VEC) {
+    const int64_t n4 = n_elems >> 2;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int o = p.op_begin; o < p.op_end; ++o) {
+        const float* a = ops[o].a;
+        const float* b = ops[o].b;
+        float* d = ops[o].dst;
+        float4 av;
+        if (a == CQG_REG_PREV) av = r;
+        else if (a == nullptr) av = make_float4(0.f, 0.f, 0.f, 0.f);
+        else av = __ldg(reinterpret_cast<const float4*>(a) + i);
+        float4 bv = __ldg(reinterpret_cast<const float4*>(b) + i);
+        r.x = __fadd_rn(av.x, bv.x);
+        r.y = __fadd_rn(av.y, bv.y);
+        r.z = __fadd_rn(av.z, bv.z);
+        r.w = __fadd_rn(av.w, bv.w);
+        if (d) reinterpret_cast<float4*>(d)[i] = r;
+      }
+    }
+  } else {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_elems;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      float r = 0.f;
+      for (int o = p.op_begin; o < p.op_end; ++o) {
+        const float* a = ops[o].a;
+        float av = (a == CQG_REG_PREV) ? r : (a == nullptr ? 0.f : a[i]);
+        r = __fadd_rn(av, ops[o].b[i]);
+        if (ops[o].dst) ops[o].dst[i] = r;
+      }
+    }
+  }
+}
+
+void launch_fold(const FoldOp* d_ops, const FoldProg* d_progs, int n_progs, int64_t n_elems,
+                 cudaStream_t st) {
+  if (n_progs <= 0) return;
+  const bool vec = (n_elems % 4) == 0;
+  int64_t work = vec ? n_elems / 4 : n_elems;
+  int gx = (int)((work + 255) / 256);
+  if (gx > 4096) gx = 4096;
+  for (int y0 = 0; y0 < n_progs; y0 += 65535) {
+    dim3 grid(gx, (unsigned)std::min(65535, n_progs - y0));
+    if (vec) fold_kernel<true><<<grid, 256, 0, st>>>(d_ops, d_progs + y0, n_elems);
+    else fold_kernel<false><<<grid, 256, 0, st>>>(d_ops, d_progs + y0, n_elems);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2b: layer norm (kernels.cpp:127-142): one thread per row, sequential FP32
+// sums over the row, staged through padded shared-memory tiles so global
+// loads stay coalesced.
+// ---------------------------------------------------------------------------
+constexpr int kLnRows = 128, kLnCh = 32;
+
+__global__ void __launch_bounds__(kLnRows) ln_kernel(const LnJob* __restrict__ jobs,
+                                                     const float* __restrict__ gamma,
+                                                     const float* __restrict__ beta, int D,
+                                                     int prec) {
+  const LnJob j = jobs[blockIdx.y];
+  const int r0 = blockIdx.x * kLnRows;
+  if (r0 >= j.rows) return;
+  __shared__ float tile[kLnRows][kLnCh + 1];
+  __shared__ float s_mean[kLnRows], s_inv[kLnRows];
+  const int tid = threadIdx.x;
+  const int nr = min(kLnRows, j.rows - r0);
+  float acc = 0.f;
+  for (int pass = 0; pass < 2; ++pass) {
+    const float mean = acc;
+    acc = 0.f;
+    for (int c0 = 0; c0 < D; c0 += kLnCh) {
+      __syncthreads();
+      for (int idx = tid; idx < kLnRows * kLnCh; idx += kLnRows) {
+        const int rr = idx / kLnCh, cc = idx % kLnCh;
+        tile[rr][cc] = (rr < nr && c0 + cc < D)
+                           ? j.in[(int64_t)(r0 + rr) * j.in_stride + c0 + cc]
+                           : 0.f;
+      }
+      __syncthreads();
+      const int lim = min(kLnCh, D - c0);
+      if (pass == 0) {
+        for (int cc = 0; cc < lim; ++cc) acc = __fadd_rn(acc, tile[tid][cc]);
+      } else {
+        for (int cc = 0; cc < lim; ++cc) {
+          const float c = __fsub_rn(tile[tid][cc], mean);
+          acc = __fadd_rn(acc, __fmul_rn(c, c));
+        }
+      }
+    }
+    acc = __fdiv_rn(acc, (float)D);  // mean /= d  |  var /= d
+    if (pass == 0) s_mean[tid] = acc;
+  }
+  s_inv[tid] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(acc, 1e-5f)));
+  __syncthreads();
+  for (int idx = tid; idx < nr * D; idx += kLnRows) {
+    const int rr = idx / D, col = idx % D;
+    const int64_t row = r0 + rr;
+    const float x = j.in[row * j.in_stride + col];
+    const float y = __fadd_rn(__fmul_rn(gamma[col], __fmul_rn(__fsub_rn(x, s_mean[rr]), s_inv[rr])),
+                              beta[col]);
+    if (j.xln) j.xln[row * D + col] = y;
+    if (j.xq) j.xq[row * D + col] = round_p(y, prec);
+  }
+}
+
+void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float* gamma,
+                      const float* beta, int D, int prec, cudaStream_t st) {
+  if (n_jobs <= 0 || max_rows <= 0) return;
+  for (int y0 = 0; y0 < n_jobs; y0 += 65535) {
+    dim3 grid((max_rows + kLnRows - 1) / kLnRows, (unsigned)std::min(65535, n_jobs - y0));
+    ln_kernel<<<grid, kLnRows, 0, st>>>(d_jobs + y0, gamma, beta, D, prec);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exact SIMT GEMM: per output element the k-ascending chain
+// acc = fl(acc + fl(a*b)) of dot_col (kernels.cpp:44-52). 64x64 tiles,
+// 256 threads, 4x4 micro-tiles, one launch for a whole job list.
+// ---------------------------------------------------------------------------
+constexpr int kBM = 64, kBN = 64, kBK = 16;
+
+int gemm_exact_tiles(int M, int N) { return ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN); }
+
+__global__ void __launch_bounds__(256) gemm_exact_kernel(const GemmJob* __restrict__ jobs,
+                                                         const int* __restrict__ tile_start,
+                                                         int n_jobs) {
+  // locate the job owning this tile
+  int lo = 0, hi = n_jobs - 1;
+  const int t = blockIdx.x;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_start[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmJob jb = jobs[lo];
+  const int local = t - tile_start[lo];
+  const int tiles_n = (jb.N + kBN - 1) / kBN;
+  const int m0 = (local / tiles_n) * kBM, n0 = (local % tiles_n) * kBN;
+
+  __shared__ __align__(16) float As[kBK][kBM];
+  __shared__ __align__(16) float Bs[kBK][kBN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) acc[i][jj] = 0.f;
+
+  for (int k0 = 0; k0 < jb.K; k0 += kBK) {
+    // A tile: 64 rows x 16 k -> As[k][m]
+    for (int idx = tid; idx < kBM * kBK; idx += 256) {
+      const int mm = idx / kBK, kk = idx % kBK;
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < jb.M && gk < jb.K) ? jb.A[(int64_t)gm * jb.lda + gk] : 0.f;
+    }
+    for (int idx = tid; idx < kBK * kBN; idx += 256) {
+      const int kk = idx / kBN, nn = idx % kBN;
+      const int gk = k0 + kk, gn = n0 + nn;
+      Bs[kk][nn] = (gk < jb.K && gn < jb.N) ? jb.B[(int64_t)gk * jb.ldb + gn] : 0.f;
+    }
+    __syncthreads();
+    const int kl = min(kBK, jb.K - k0);
+    for (int kk = 0; kk < kl; ++kk) {
+      const float4 a4 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w};
+      const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = __fadd_rn(acc[i][jj], __fmul_rn(a[i], b[jj]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty * 4 + i;
+    if (gm >= jb.M) continue;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int gn = n0 + tx * 4 + jj;
+      if (gn >= jb.N) continue;
+      float v = round_p(acc[i][jj], jb.prec);
+      if (jb.epi == 1) v = round_p(gelu_ref(v), jb.prec);
+      jb.C[(int64_t)gm * jb.ldc + gn] = v;
+    }
+  }
+}
+
+void launch_gemm_exact(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs, int total_tiles,
+                       cudaStream_t st) {
+  if (n_jobs <= 0 || total_tiles <= 0) return;
+  gemm_exact_kernel<<<total_tiles, 256, 0, st>>>(d_jobs, d_tile_start, n_jobs);
+}
+
+// ---------------------------------------------------------------------------
+// K5: causal attention, one CTA per (item, head job), one thread per query
+// row; reference order (kernels.cpp:167-190) with glibc-exact expf.
+// ---------------------------------------------------------------------------
+__global__ void attention_kernel(const AttnJob* __restrict__ jobs, int S, int dk) {
+  extern __shared__ float sm[];
+  const AttnJob jb = jobs[blockIdx.y];
+  const int item = blockIdx.x;
+  const int ldk = dk + 1, lds = S + 1;
+  float* q = sm;
+  float* k = q + S * ldk;
+  float* v = k + S * ldk;
+  float* pr = v + S * ldk;
+  const int64_t base = (int64_t)item * S;
+  for (int idx = threadIdx.x; idx < S * dk; idx += blockDim.x) {
+    const int r = idx / dk, c = idx % dk;
+    const int64_t g = (base + r) * jb.ld + c;
+    q[r * ldk + c] = jb.q[g];
+    k[r * ldk + c] = jb.k[g];
+    v[r * ldk + c] = jb.v[g];
+  }
+  __syncthreads();
+  const float scale = __fdiv_rn(1.0f, __fsqrt_rn((float)dk));
+  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+    float* p = pr + i * lds;
+    float mx = -INFINITY;
+    for (int jj = 0; jj <= i; ++jj) {
+      float acc = 0.f;
+      for (int t = 0; t < dk; ++t) acc = __fadd_rn(acc, __fmul_rn(q[i * ldk + t], k[jj * ldk + t]));
+      p[jj] = __fmul_rn(acc, scale);
+      mx = (mx < p[jj]) ? p[jj] : mx;
+    }
+    float den = 0.f;
+    for (int jj = 0; jj <= i; ++jj) {
+      p[jj] = glibc_expf(__fsub_rn(p[jj], mx));
+      den = __fadd_rn(den, p[jj]);
+    }
+    for (int jj = 0; jj <= i; ++jj) p[jj] = __fdiv_rn(p[jj], den);
+    for (int t = 0; t < dk; ++t) {
+      float acc = 0.f;
+      for (int jj = 0; jj <= i; ++jj) acc = __fadd_rn(acc, __fmul_rn(p[jj], v[jj * ldk + t]));
+      jb.z[(base + i) * jb.ld + t] = round_p(acc, jb.prec);
+    }
+  }
+}
+
+void launch_attention(const AttnJob* d_jobs, int n_jobs, int B, int S, int dk, cudaStream_t st) {
+  if (n_jobs <= 0) return;
+  const size_t smem = sizeof(float) * (size_t)(3 * S * (dk + 1) + S * (S + 1));
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  int threads = ((S + 31) / 32) * 32;
+  if (threads > 1024) threads = 1024;
+  for (int y0 = 0; y0 < n_jobs; y0 += 65535) {
+    dim3 grid(B, (unsigned)std::min(65535, n_jobs - y0));
+    attention_kernel<<<grid, threads, smem, st>>>(d_jobs + y0, S, dk);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// embed (model.cpp:608-620)
+// ---------------------------------------------------------------------------
+__global__ void embed_kernel(const int* __restrict__ tok, const float* __restrict__ we,
+                             const float* __restrict__ wpos, float* __restrict__ out, int B, int S,
+                             int D, int prec) {
+  const int64_t n = (int64_t)B * S * D;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % D);
+    const int64_t row = i / D;
+    const int pos = (int)(row % S);
+    const int t = tok[row];
+    out[i] = round_p(__fadd_rn(we[(int64_t)t * D + j], wpos[(int64_t)pos * D + j]), prec);
+  }
+}
+
+void launch_embed(const int* tokens, const float* we, const float* wpos, float* out, int B, int S,
+                  int D, int prec, cudaStream_t st) {
+  const int64_t n = (int64_t)B * S * D;
+  int grid = (int)std::min<int64_t>((n + 255) / 256, 8192);
+  embed_kernel<<<grid, 256, 0, st>>>(tokens, we, wpos, out, B, S, D, prec);
+}
+
+// ---------------------------------------------------------------------------
+// K8: KL / logit diff in FP64 (patching.cpp:108-161).
+// ---------------------------------------------------------------------------
+template <typename T, typename Op>
+__device__ T block_reduce(T v, Op op, T* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  v = (threadIdx.x < nw) ? sh[threadIdx.x] : sh[0];
+  if (w == 0)
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (threadIdx.x == 0) sh[0] = v;
+  __syncthreads();
+  return sh[0];
+}
+
+struct MaxOp {
+  __device__ double operator()(double a, double b) const { return a > b ? a : b; }
+};
+struct SumOp {
+  __device__ double operator()(double a, double b) const { return a + b; }
+};
+struct OrOp {
+  __device__ int operator()(int a, int b) const { return a | b; }
+};
+
+__device__ double row_lse(const float* x, int V, int* nan_flag, double* sh, int* shi) {
+  double mx = -INFINITY;
+  int nan = 0;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float f = x[i];
+    if (f != f) nan = 1;
+    mx = fmax(mx, (double)f);
+  }
+  nan = block_reduce(nan, OrOp(), shi);
+  if (nan && threadIdx.x == 0) atomicOr(nan_flag, 1);
+  mx = block_reduce(mx, MaxOp(), sh);
+  double s = 0.0;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) s += exp((double)x[i] - mx);
+  s = block_reduce(s, SumOp(), sh);
+  return mx + log(s);
+}
+
+__global__ void lse_kernel(const float* __restrict__ base, int V, double* lse, int* nan_flag) {
+  __shared__ double sh[32];
+  __shared__ int shi[32];
+  const double l = row_lse(base + (int64_t)blockIdx.x * V, V, nan_flag, sh, shi);
+  if (threadIdx.x == 0) lse[blockIdx.x] = l;
+}
+
+void launch_lse(const float* base, int rows, int V, double* lse, int* nan_flag, cudaStream_t st) {
+  if (rows > 0) lse_kernel<<<rows, 256, 0, st>>>(base, V, lse, nan_flag);
+}
+
+__global__ void kl_kernel(const float* __restrict__ logits, const float* __restrict__ base,
+                          const double* __restrict__ base_lse, const int* __restrict__ item_of,
+                          int V, double* out, int* nan_flag) {
+  __shared__ double sh[32];
+  __shared__ int shi[32];
+  const int r = blockIdx.x;
+  const float* q = logits + (int64_t)r * V;
+  const int it = item_of[r];
+  const float* c = base + (int64_t)it * V;
+  const double lse_c = base_lse[it];
+  const double lse_q = row_lse(q, V, nan_flag, sh, shi);
+  double kl = 0.0;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const double lp = (double)c[i] - lse_c;
+    const double lq = (double)q[i] - lse_q;
+    kl += exp(lp) * (lp - lq);
+  }
+  kl = block_reduce(kl, SumOp(), sh);
+  if (threadIdx.x == 0) out[r] = kl;
+}
+
+void launch_kl(const float* logits, const float* base, const double* base_lse, const int* item_of,
+               int rows, int V, double* out, int* nan_flag, cudaStream_t st) {
+  if (rows > 0) kl_kernel<<<rows, 256, 0, st>>>(logits, base, base_lse, item_of, V, out, nan_flag);
+}
+
+__global__ void logitdiff_kernel(const float* __restrict__ logits, const float* __restrict__ base,
+                                 const int* __restrict__ item_of, const int* __restrict__ ans,
+                                 const int* __restrict__ dis, int V, double* out, int* nan_flag) {
+  __shared__ int shi[32];
+  const int r = blockIdx.x;
+  const float* q = logits + (int64_t)r * V;
+  const int it = item_of[r];
+  const float* c = base + (int64_t)it * V;
+  int nan = 0;
+  for (int i = threadIdx.x; i < V; i += blockDim.x)
+    if (q[i] != q[i] || c[i] != c[i]) nan = 1;
+  nan = block_reduce(nan, OrOp(), shi);
+  if (threadIdx.x == 0) {
+    if (nan) atomicOr(nan_flag, 1);
+    const int a = ans[it], d = dis[it];
+    const double ldp = (double)q[a] - (double)q[d];
+    const double ldc = (double)c[a] - (double)c[d];
+    out[r] = fabs(ldp - ldc);
+  }
+}
+
+void launch_logitdiff(const float* logits, const float* base, const int* item_of,
+                      const int* answer, const int* distractor, int rows, int V, double* out,
+                      int* nan_flag, cudaStream_t st) {
+  if (rows > 0)
+    logitdiff_kernel<<<rows, 256, 0, st>>>(logits, base, item_of, answer, distractor, V, out,
+                                           nan_flag);
+}
+
+// ---------------------------------------------------------------------------
+// act_diff RMS (patching.cpp:249-256)
+// ---------------------------------------------------------------------------
+__global__ void rms_kernel(const RmsJob* __restrict__ jobs) {
+  __shared__ double sh[32];
+  const RmsJob j = jobs[blockIdx.x];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < j.n; i += blockDim.x) {
+    const double d = (double)j.a[i] - (double)j.b[i];
+    acc += d * d;
+  }
+  acc = block_reduce(acc, SumOp(), sh);
+  if (threadIdx.x == 0) *j.out = sqrt(acc / (double)j.n);
+}
+
+void launch_rms(const RmsJob* d_jobs, int n_jobs, cudaStream_t st) {
+  if (n_jobs > 0) rms_kernel<<<n_jobs, 256, 0, st>>>(d_jobs);
+}
+
+// ---------------------------------------------------------------------------
+// K1: weight images.
+// ---------------------------------------------------------------------------
+__global__ void quantize_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t n,
+                                int prec) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = round_p(in[i], prec);
+}
+
+void launch_quantize(const float* in, float* out, int64_t n, int prec, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>((n + 255) / 256, 16384);
+  quantize_kernel<<<grid, 256, 0, st>>>(in, out, n, prec);
+}
+
+__global__ void pack_e4m3_kernel(const float* __restrict__ in, uint8_t* __restrict__ out,
+                                 int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = enc_e4m3(in[i]);
+}
+
+void launch_pack_e4m3(const float* in, uint8_t* out, int64_t n, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>((n + 255) / 256, 16384);
+  pack_e4m3_kernel<<<grid, 256, 0, st>>>(in, out, n);
+}
+
+__global__ void pack_bf16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out,
+                                 int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = enc_bf16(in[i]);
+}
+
+void launch_pack_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st) {
+  int grid = (int)std::min<int64_t>((n + 255) / 256, 16384);
+  pack_bf16_kernel<<<grid, 256, 0, st>>>(in, out, n);
+}
+
+__global__ void rtn_groups_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                  int64_t group_off, int rows, int cols, int ld, int bits) {
+  __shared__ double sh[32];
+  const int64_t g0 = (int64_t)blockIdx.x * group_off;
+  const int64_t n = (int64_t)rows * cols;
+  double mx = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t off = g0 + (i / cols) * ld + (i % cols);
+    const double a = fabs((double)in[off]);
+    mx = (a > mx) ? a : mx;
+  }
+  mx = block_reduce(mx, MaxOp(), sh);
+  const double delta = (mx == 0.0) ? 0.0 : __ddiv_rn(mx, ldexp(1.0, bits - 1));
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t off = g0 + (i / cols) * ld + (i % cols);
+    out[off] = rtn_apply(in[off], delta);
+  }
+}
+
+void launch_rtn_groups(const float* in, float* out, int n_groups, int64_t group_off, int rows,
+                       int cols, int ld, int bits, cudaStream_t st) {
+  if (n_groups > 0)
+    rtn_groups_kernel<<<n_groups, 256, 0, st>>>(in, out, group_off, rows, cols, ld, bits);
+}
+
+// ---------------------------------------------------------------------------
+// exhaustive scalar checks (tests)
+// ---------------------------------------------------------------------------
+__global__ void e4m3_all_kernel(uint8_t* out, uint32_t lo, uint64_t count) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = enc_e4m3(__uint_as_float(lo + (uint32_t)i));
+}
+__global__ void bf16_all_kernel(uint16_t* out, uint32_t lo, uint64_t count) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = enc_bf16(__uint_as_float(lo + (uint32_t)i));
+}
+__global__ void libm_all_kernel(float* out, uint32_t lo, uint64_t count, int which) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const float x = __uint_as_float(lo + (uint32_t)i);
+    out[i] = which == 0 ? glibc_expf(x) : (which == 1 ? glibc_erff(x) : gelu_ref(x));
+  }
+}
+void launch_e4m3_all(uint8_t* out, uint32_t lo, uint64_t count, cudaStream_t st) {
+  e4m3_all_kernel<<<4096, 256, 0, st>>>(out, lo, count);
+}
+void launch_bf16_all(uint16_t* out, uint32_t lo, uint64_t count, cudaStream_t st) {
+  bf16_all_kernel<<<4096, 256, 0, st>>>(out, lo, count);
+}
+void launch_libm_all(float* out, uint32_t lo, uint64_t count, int which, cudaStream_t st) {
+  libm_all_kernel<<<4096, 256, 0, st>>>(out, lo, count, which);
+}
+
+}  // namespace cqg

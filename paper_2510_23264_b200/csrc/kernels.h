@@ -1,0 +1,104 @@
+// kernels.h — job descriptors and launchers for the sm_100a kernels.
+//
+// Activation layout in HBM: a "segment" is one evaluation context (the
+// baseline, or one patched edge) over the local item batch: [B][S][D] FP32,
+// contiguous. Kernels take flat job lists so one launch covers every segment
+// of a step (no per-edge launches).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cqg {
+
+// ---- K2a: receiver-input fold (sum_inputs, model.cpp:537-552) -------------
+// dst = (a ? a : 0.0f) + b elementwise, ops of a program run in order per
+// element (so a later op may read an earlier op's dst). a == kRegPrev reuses
+// the previous op's result held in a register; dst == nullptr keeps it there.
+struct FoldOp {
+  const float* a;
+  const float* b;
+  float* dst;
+};
+struct FoldProg {
+  int op_begin, op_end;
+};
+#define CQG_REG_PREV (reinterpret_cast<const float*>(uintptr_t(1)))
+void launch_fold(const FoldOp* d_ops, const FoldProg* d_progs, int n_progs, int64_t n_elems,
+                 cudaStream_t st);
+
+// ---- K2b: layer norm + precision rounding (kernels.cpp:127-163) -----------
+// Exact reference order: sequential FP32 sums per row.
+struct LnJob {
+  const float* in;  // rows selected as in + r*in_stride
+  float* xln;       // [rows][D] (may be null)
+  float* xq;        // [rows][D] rounded at prec (may be null)
+  int rows;
+  int in_stride;
+};
+void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float* gamma,
+                      const float* beta, int D, int prec, cudaStream_t st);
+
+// ---- exact SIMT GEMM (dot_col, kernels.cpp:44-52) --------------------------
+// C[M][N] = round_prec(sum_k A[m][k]*B[k][n]) with k ascending, every product
+// rounded then added (no FMA), as the reference. epi=1: C = round(gelu(round(acc))).
+struct GemmJob {
+  const float* A;
+  const float* B;
+  float* C;
+  int M, N, K, lda, ldb, ldc;
+  int prec, epi;
+};
+void launch_gemm_exact(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs, int total_tiles,
+                       cudaStream_t st);
+int gemm_exact_tiles(int M, int N);
+
+// ---- K5: causal attention (kernels.cpp:167-219) + z rounding ---------------
+struct AttnJob {
+  const float* q;
+  const float* k;
+  const float* v;
+  float* z;
+  int ld;    // row stride of q/k/v/z (elements)
+  int prec;  // rounding of z (model.cpp:688-689)
+};
+void launch_attention(const AttnJob* d_jobs, int n_jobs, int B, int S, int dk, cudaStream_t st);
+
+// ---- embed (model.cpp:608-620) ---------------------------------------------
+void launch_embed(const int* tokens, const float* we, const float* wpos, float* out, int B, int S,
+                  int D, int prec, cudaStream_t st);
+
+// ---- K8: KL / logit-diff against the baseline (patching.cpp:108-161) -------
+// logits: [rows][V] (patched last rows), row r belongs to item item_of[r];
+// base: [B][V] baseline last-row logits; base_lse[B]. out[r] (double).
+void launch_kl(const float* logits, const float* base, const double* base_lse, const int* item_of,
+               int rows, int V, double* out, int* nan_flag, cudaStream_t st);
+void launch_lse(const float* base, int rows, int V, double* lse, int* nan_flag, cudaStream_t st);
+void launch_logitdiff(const float* logits, const float* base, const int* item_of,
+                      const int* answer, const int* distractor, int rows, int V, double* out,
+                      int* nan_flag, cudaStream_t st);
+
+// ---- act_diff RMS (patching.cpp:241-259) -----------------------------------
+// out[j] = sqrt(sum((a-b)^2)/n) per job over n contiguous floats.
+struct RmsJob {
+  const float* a;
+  const float* b;
+  int64_t n;
+  double* out;
+};
+void launch_rms(const RmsJob* d_jobs, int n_jobs, cudaStream_t st);
+
+// ---- K1: weight images (ImageBank, model.cpp:473-491) ----------------------
+void launch_quantize(const float* in, float* out, int64_t n, int prec, cudaStream_t st);
+void launch_pack_e4m3(const float* in, uint8_t* out, int64_t n, cudaStream_t st);
+void launch_pack_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st);
+// Rtn4 per group: groups are `n_groups` blocks of rows x cols taken with a
+// row stride `ld` starting at base + g*group_off (model.cpp:445-469).
+void launch_rtn_groups(const float* in, float* out, int n_groups, int64_t group_off, int rows,
+                       int cols, int ld, int bits, cudaStream_t st);
+
+// ---- tests: exhaustive scalar checks on the device --------------------------
+void launch_e4m3_all(uint8_t* out, uint32_t lo, uint64_t count, cudaStream_t st);
+void launch_bf16_all(uint16_t* out, uint32_t lo, uint64_t count, cudaStream_t st);
+void launch_libm_all(float* out, uint32_t lo, uint64_t count, int which, cudaStream_t st);
+
+}  // namespace cqg

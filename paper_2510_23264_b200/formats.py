@@ -99,27 +99,22 @@ class ModelConfig:
 
 
 def fnv1a64(data: bytes, seed: int = 14695981039346656037) -> int:
-    """model.cpp:324-332, vectorised over 8-byte-free chunks in numpy."""
+    """FNV-1a-64 (model.cpp:324-332), pure Python (small files only)."""
     h = seed
-    mv = memoryview(data)
-    # Pure-Python loop is too slow for 500 MB files; process with numpy in
-    # blocks while keeping the exact sequential xor-multiply recurrence.
-    arr = np.frombuffer(mv, dtype=np.uint8)
-    prime = 1099511628211
-    mask = (1 << 64) - 1
-    # The recurrence is inherently sequential; use a small C-speed loop via
-    # Python ints on chunks (fast enough: ~50 MB/s).
-    for b in arr.tobytes():
-        h = ((h ^ b) * prime) & mask
+    for b in data:
+        h = ((h ^ b) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
     return h
 
 
 def _fnv_fast(data: bytes) -> int:
-    try:
-        from ._native import fnv1a64 as native  # optional C helper
-        return native(data)
-    except Exception:
-        return fnv1a64(data)
+    """Same hash via libcqg.so's host helper when available (large files)."""
+    if len(data) > (1 << 20):
+        try:
+            from .engine import fnv1a64 as native
+            return native(data)
+        except Exception:
+            pass
+    return fnv1a64(data)
 
 
 @dataclass

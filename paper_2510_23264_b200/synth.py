@@ -161,6 +161,8 @@ def docstring_dataset(cfg: ModelConfig, items: int, seed: int) -> Dataset:
         def prompt(p, q, r):
             seq = [def_, f, lpar, p, comma, q, comma, r, rpar, colon, quote, desc, desc,
                    param, a, colon, desc, desc, param, b, colon, desc, desc, param]
+            if len(seq) > S:  # compact form for short contexts
+                seq = [def_, p, q, r, quote, param, a, desc, param, b, desc, param]
             seq = [quote] * max(0, S - len(seq)) + seq
             return np.asarray(seq[-S:], np.int32)
 

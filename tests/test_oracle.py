@@ -1,0 +1,216 @@
+"""The CPU oracle (oracle/cq_oracle.c) pinned to the reference.
+
+* against the reference's own frozen values (proj/tests/test_numerics.cpp,
+  test_patching.cpp, test_acdc.cpp, test_eval.cpp) via tests/golden/;
+* bit-for-bit against the reference library compiled in place (oracle/_ref)
+  when it is present (build container and GPU box).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import KL, LOGITDIFF, Policy, Port, Prune
+from paper_2510_23264_b200 import formats, synth
+from paper_2510_23264_b200.engine import PrecisionPolicy, method_prune_config, threshold_grid
+from helpers import GOLDEN, SMALL, TINY, TOY, bits, make, random_mask, write
+
+G = json.load(open(os.path.join(GOLDEN, "golden.json")))
+
+
+def port_for(cfg, wseed, items, dseed):
+    w, ds = make(cfg, wseed, items, dseed)
+    return Port(cfg, w.mats), w, ds
+
+
+# --- numerics (proj/tests/test_numerics.cpp) -------------------------------
+def test_e4m3_landmarks():
+    p, _, _ = port_for(TINY, 1, 1, 1)
+    lib = p.lib
+    enc = lambda x: lib.cqo_encode_f8(x)  # noqa: E731
+    assert enc(448.0) == 0x7E and enc(1000.0) == 0x7E and enc(-1000.0) == 0xFE
+    assert enc(0.015625) == 0x08
+    assert enc(0.3) == enc(0.3125)
+    assert enc(0.0) == 0x00
+    assert enc(float("nan")) == 0x7F
+    assert enc(2.0 ** -11) == 0 and enc(2.0 ** -10) == 0
+    assert enc(1.5 * 2.0 ** -10) == 0x01
+
+
+def test_e4m3_decode_table_all_patterns():
+    p, _, _ = port_for(TINY, 1, 1, 1)
+    import ctypes as C
+    p.lib.cqo_decode_f8.restype = C.c_double
+    p.lib.cqo_decode_f8.argtypes = [C.c_uint8]
+    vals = [p.lib.cqo_decode_f8(b) for b in range(256)]
+    nans = [b for b, v in enumerate(vals) if math.isnan(v)]
+    assert nans == [0x7F, 0xFF]
+    pos = {v for b, v in enumerate(vals) if not (b & 0x80) and not math.isnan(v)}
+    assert len(pos) == 127 and max(pos) == 448.0
+    for b in range(256):  # encode(decode(p)) round trip
+        if b in nans:
+            continue
+        assert p.lib.cqo_encode_f8(vals[b]) == b or (b == 0x80)  # -0 encodes to 0x80
+
+
+def test_rtn_frozen_examples():
+    # test_numerics.cpp:221-244
+    from oracle.oracle import Ref, ref_available
+    x = np.array([1.0, -2.0, 0.3], np.float32)
+    import ctypes as C
+    p, _, _ = port_for(TINY, 1, 1, 1)
+    d = C.c_double()
+    y = x.copy()
+    p.lib.cqo_quantize_rtn(y.ctypes.data_as(C.c_void_p), C.c_int64(3), 8, C.byref(d))
+    assert d.value == 2.0 / 128.0 and y[0] == 1.0 and y[1] == -2.0 and y[2] == np.float32(0.296875)
+
+
+def test_kl_frozen_value():
+    # test_patching.cpp:53-73, acceptance_tests.cpp:553-558
+    import ctypes as C
+    p, _, _ = port_for(TINY, 1, 1, 1)
+    f = np.array([0.0, 0.0], np.float32)
+    t = np.array([0.0, 1.0], np.float32)
+    kl = p.lib.cqo_metric_kl(f.ctypes.data_as(C.c_void_p), t.ctypes.data_as(C.c_void_p), 2)
+    assert abs(kl - 0.12011450695827752) <= 1e-12 * 0.12011450695827752
+    assert p.lib.cqo_metric_kl(f.ctypes.data_as(C.c_void_p), f.ctypes.data_as(C.c_void_p), 2) == 0.0
+    l3 = np.array([0.0, np.float32(math.log(3.0))], np.float32)
+    kl3 = p.lib.cqo_metric_kl(f.ctypes.data_as(C.c_void_p), l3.ctypes.data_as(C.c_void_p), 2)
+    assert abs(kl3 - 0.5 * math.log(4.0 / 3.0)) <= 1e-6
+
+
+def test_threshold_grid_frozen():
+    # test_acdc.cpp:277-294
+    g = threshold_grid(0.001, 3.16, 21)
+    assert g[0] == 0.001 and g[-1] == 3.16
+    assert abs(g[1] - 0.0014961817537620622) <= 1e-12 * g[1]
+    assert abs(g[2] - 0.002238559840290518) <= 1e-12 * g[2]
+    assert abs(g[19] - 2.112042866486218) <= 1e-12 * g[19]
+    assert [float(x).hex() for x in g] == G["threshold_grid"]
+
+
+# --- graph (model.cpp:166-246) ---------------------------------------------
+@pytest.mark.parametrize("cfg,n_nodes,n_edges", [(TOY, 10, 33), (TINY, 8, 26)])
+def test_graph_counts(cfg, n_nodes, n_edges):
+    p = Port(cfg, synth.random_weights(cfg, 1).mats)
+    assert (p.n_nodes, p.n_edges) == (n_nodes, n_edges)
+
+
+def test_gpt2_graph_edge_count():
+    # SURVEY.md §0.7 (measured with the reference's ComputationalGraph)
+    from paper_2510_23264_b200.engine import graph_edges
+    from helpers import GPT2S
+    n, src, dst = graph_edges(GPT2S)
+    assert n == 158 and len(src) == 11611
+    med = formats.ModelConfig(24, 16, 1024, 64, 50257, 16, 1, 1)
+    assert len(graph_edges(med)[1]) == 80965
+
+
+# --- scores / ACDC against the reference's recorded outputs -----------------
+def test_tiny_scores_match_golden():
+    p, w, ds = port_for(TINY, 101, 3, 7)
+    pols = {"fp32": (Policy.all_fp32(), False), "hq": (Policy.head_quantized(), False),
+            "pahq": (Policy.head_quantized(), True), "low": (Policy.all_low(), False)}
+    for key, rec in G["tiny"].items():
+        metric = int(key[1])
+        mask_seed = key.split("_")[1][4:]
+        mask = None if mask_seed == "None" else (
+            np.random.RandomState(int(mask_seed)).rand(p.n_edges) < 0.6)
+        pname = key.split("_")[2]
+        mode = int(key[-1])
+        pol, per = pols[pname]
+        got = p.score_edges(ds, rec["edges"], pol, per_edge=per, metric=metric, mode=mode,
+                            mask=mask)
+        assert [float(x).hex() for x in got] == rec["scores"], key
+
+
+def test_toy_pahq_acdc_matches_golden():
+    p, w, ds = port_for(TOY, 1, 16, 2)
+    pr = Prune()
+    pr.tau, pr.max_steps, pr.min_change_rate, pr.mode, pr.act_floor = 0.01, 10, 0.0, 0, 0.0
+    pr.per_edge_policy, pr.heads_only = 1, 0
+    pr.base = Policy.head_quantized()
+    r = p.run_acdc(ds, pr, KL)
+    g = G["toy_pahq"]
+    assert r.steps == g["steps"]
+    assert r.final_mask.astype(int).tolist() == g["final_mask"]
+    assert [[s, e, float(sc).hex(), k] for s, e, sc, k in r.records] == g["records"]
+
+
+@pytest.mark.parametrize("preset", ["standard", "underflow", "two_hop"])
+def test_planted_auc_known_answers(preset):
+    """roc_sweep (eval.cpp:1193-1226) restated over the oracle reproduces the
+    reference's exact AUCs (test_eval.cpp:174-294)."""
+    d = os.path.join(GOLDEN, f"planted_{preset}_s1")
+    w = formats.load_weights(os.path.join(d, "weights.bin"))
+    ds = formats.load_dataset_jsonl(os.path.join(d, "dataset.jsonl"))
+    gt = set(json.load(open(os.path.join(d, "task.json")))["ground_truth"])
+    p = Port(w.cfg, w.mats)
+    taus = threshold_grid(0.001, 3.16, 21)
+    for mname, mid in (("acdc", 0), ("rtn8", 1), ("pahq", 2)):
+        cfg = method_prune_config(mid)
+        pts = []
+        for tau in taus:
+            pr = Prune()
+            pr.tau, pr.max_steps, pr.min_change_rate, pr.mode = tau, cfg.max_steps, 0.0, 0
+            pr.act_floor, pr.per_edge_policy, pr.heads_only = 0.0, int(cfg.per_edge_policy), 0
+            b = cfg.base_policy
+            pr.base = Policy.make(b.attention_default, b.mlp_default, b.embed_precision,
+                                  b.unembed_precision, b.low_mode)
+            r = p.run_acdc(ds, pr, LOGITDIFF)
+            kept = np.nonzero(r.final_mask)[0]
+            tp = sum(1 for e in kept if e in gt)
+            pts.append((tp / len(gt), (len(kept) - tp) / (p.n_edges - len(gt))))
+        auc = auc_from_points(pts)
+        assert float(auc).hex() == G["planted"][preset][mname]["auc"], (preset, mname, auc)
+
+
+def auc_from_points(pts):
+    """eval.cpp:1149-1166"""
+    ps = sorted(pts, key=lambda p: (p[1], p[0]))
+    x = y = area = 0.0
+    for tpr, fpr in ps:
+        if tpr <= y:
+            continue
+        if fpr > x:
+            area += (fpr - x) * y
+            x = fpr
+        y = tpr
+    return area + (1.0 - x) * y
+
+
+# --- bit-for-bit against the compiled reference ------------------------------
+@pytest.mark.parametrize("cfg", [TINY, SMALL, TOY])
+def test_port_forward_equals_reference(ref, cfg, tmp_path):
+    w, ds = make(cfg, 3, 2, 4)
+    wp, dp = write(str(tmp_path), w, ds)
+    rm = ref.open(wp, dp, 0)
+    p = Port(cfg, w.mats)
+    L, H = cfg.n_layers, cfg.n_heads
+    pols = [Policy.all_fp32(), Policy.head_quantized(), Policy.all_low(),
+            Policy.make(th=(L - 1, H - 1)), Policy.head_quantized(mode=1),
+            Policy.make(att=1), Policy.make(mode=1, th=(0, 0))]
+    if cfg.has_mlp:
+        pols.append(Policy.make(tm=0))
+    for i, pol in enumerate(pols):
+        mask = random_mask(p.n_edges, i, 0.7) if i % 2 else None
+        a = rm.forward(ds.clean[0], pol, mask=mask)
+        b = p.forward(ds.clean[0], pol, mask=mask)
+        assert np.array_equal(bits(a), bits(b)), i
+    rm.close()
+
+
+def test_port_run_acdc_equals_reference_small(ref, tmp_path):
+    w, ds = make(SMALL, 5, 3, 6)
+    wp, dp = write(str(tmp_path), w, ds)
+    rm = ref.open(wp, dp, 0)
+    p = Port(SMALL, w.mats)
+    pr = ref.method_config(2, 8)
+    pr.tau, pr.max_steps = 0.002, 3
+    a = rm.run_acdc(pr)
+    b = p.run_acdc(ds, pr, KL)
+    assert a.steps == b.steps and np.array_equal(a.final_mask, b.final_mask)
+    assert a.records == b.records
+    rm.close()
