@@ -269,21 +269,30 @@ struct Engine {
     return zero.as<float>();
   }
 
-  template <class T>
-  T* upload(const std::vector<T>& v) {
-    const size_t bytes = ((std::max<size_t>(v.size(), 1) * sizeof(T)) + 15) & ~size_t(15);
-    if (bytes > stage_cap) {
+  // Job arrays travel through a pinned ring. reserve() must be called once per
+  // launch with the total bytes of all its arrays so that no later upload of
+  // the same launch can wrap (or grow) the ring under an earlier one.
+  static size_t up_bytes(size_t n, size_t sz) { return ((std::max<size_t>(n, 1) * sz) + 15) & ~size_t(15); }
+
+  void reserve(size_t total) {
+    if (total > stage_cap) {
       CK(cudaStreamSynchronize(st));
       if (h_stage) cudaFreeHost(h_stage);
-      stage_cap = std::max(bytes, stage_cap * 2);
+      stage_cap = std::max<size_t>({total, stage_cap * 2, size_t(16) << 20});
       CK(cudaMallocHost(&h_stage, stage_cap));
       d_stage.ensure(stage_cap);
       stage_off = 0;
     }
-    if (stage_off + bytes > stage_cap) {
+    if (stage_off + total > stage_cap) {
       CK(cudaStreamSynchronize(st));
       stage_off = 0;
     }
+  }
+
+  template <class T>
+  T* upload(const std::vector<T>& v) {
+    const size_t bytes = up_bytes(v.size(), sizeof(T));
+    if (stage_off + bytes > stage_cap) throw Error(2, "internal: staging upload without reserve()");
     if (!v.empty()) std::memcpy(h_stage + stage_off, v.data(), v.size() * sizeof(T));
     CK(cudaMemcpyAsync(d_stage.as<char>() + stage_off, h_stage + stage_off, bytes,
                        cudaMemcpyHostToDevice, st));
@@ -340,6 +349,7 @@ struct Engine {
   // ---- launch helpers --------------------------------------------------------
   void fold(const std::vector<FoldOp>& ops, const std::vector<FoldProg>& progs, size_t elems) {
     if (progs.empty()) return;
+    reserve(up_bytes(ops.size(), sizeof(FoldOp)) + up_bytes(progs.size(), sizeof(FoldProg)));
     launch_fold(upload(ops), upload(progs), (int)progs.size(), (int64_t)elems, st);
     launched();
   }
@@ -347,6 +357,7 @@ struct Engine {
     if (jobs.empty()) return;
     int mx = 0;
     for (auto& j : jobs) mx = std::max(mx, j.rows);
+    reserve(up_bytes(jobs.size(), sizeof(LnJob)));
     launch_layernorm(upload(jobs), (int)jobs.size(), mx, master[l_gamma]->as<float>(),
                      master[l_beta]->as<float>(), g.D, prec, st);
     launched();
@@ -359,11 +370,13 @@ struct Engine {
       ts[i] = total;
       total += gemm_exact_tiles(jobs[i].M, jobs[i].N);
     }
+    reserve(up_bytes(jobs.size(), sizeof(GemmJob)) + up_bytes(ts.size(), sizeof(int)));
     launch_gemm_exact(upload(jobs), upload(ts), (int)jobs.size(), total, st);
     launched();
   }
   void attn(const std::vector<AttnJob>& jobs, int nb) {
     if (jobs.empty()) return;
+    reserve(up_bytes(jobs.size(), sizeof(AttnJob)));
     launch_attention(upload(jobs), (int)jobs.size(), nb, g.S, g.dk, st);
     launched();
   }
@@ -521,6 +534,7 @@ struct Engine {
                    bool all_rows, int* d_nan) {
     for (int s = sigma0; s < g.n_stages; ++s) {
       const auto& nodes = g.stage_nodes[s];
+      if (nodes.empty()) continue;  // MLP stages of attention-only models
       const int k = g.kind[nodes[0]];
       if (k == kEmbed) {
         run_embed(P, d_tok, R.o(0), R.nb);
@@ -723,6 +737,7 @@ struct Engine {
     std::vector<int> unembed_edges;  // plan indices whose logits were computed
     for (int s = smin; s <= last; ++s) {
       const auto& nodes = g.stage_nodes[s];
+      if (nodes.empty()) continue;  // MLP stages of attention-only models
       const int k = g.kind[nodes[0]];
       std::vector<HeadIO> hj;
       std::vector<SegIO> mj;
@@ -774,6 +789,7 @@ struct Engine {
           }
         }
         if (!rj.empty()) {
+          reserve(up_bytes(rj.size(), sizeof(RmsJob)));
           launch_rms(upload(rj), (int)rj.size(), st);
           launched();
         }
@@ -812,6 +828,7 @@ struct Engine {
         std::vector<int> item_of(rows);
         for (int r = 0; r < rows; ++r) item_of[r] = r % nb;
         double* tmp = reinterpret_cast<double*>(scratch("p_kl", (size_t)rows * 2));
+        reserve(up_bytes(item_of.size(), sizeof(int)));
         if (metric == 0)
           launch_kl(logits, R.logits.as<float>(), R.lse.as<double>(), upload(item_of), rows, V, tmp,
                     d_nan, st);
@@ -1028,6 +1045,7 @@ struct Engine {
     };
     for (int s = 0; s < g.n_stages; ++s) {
       const auto& nodes = g.stage_nodes[s];
+      if (nodes.empty()) continue;  // MLP stages of attention-only models
       const int k = g.kind[nodes[0]];
       if (k == kEmbed) run_embed(P, tk.as<int>(), O, 1);
       else if (k == kHead) {

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256) fold_kernel(const FoldOp* __restrict__ op
         float4 av;
         if (a == CQG_REG_PREV) av = r;
         else if (a == nullptr) av = make_float4(0.f, 0.f, 0.f, 0.f);
-        else av = __ldg(reinterpret_cast<const float4*>(a) + i);
+        else av = reinterpret_cast<const float4*>(a)[i];
         float4 bv = __ldg(reinterpret_cast<const float4*>(b) + i);
         r.x = __fadd_rn(av.x, bv.x);
         r.y = __fadd_rn(av.y, bv.y);
@@ -307,15 +307,16 @@ void launch_embed(const int* tokens, const float* we, const float* wpos, float* 
 // ---------------------------------------------------------------------------
 // K8: KL / logit diff in FP64 (patching.cpp:108-161).
 // ---------------------------------------------------------------------------
+// Block-wide reduction; `ident` is the identity of op (0 for sums).
 template <typename T, typename Op>
-__device__ T block_reduce(T v, Op op, T* sh) {
+__device__ T block_reduce(T v, Op op, T* sh, T ident) {
   for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   __syncthreads();
   if (l == 0) sh[w] = v;
   __syncthreads();
   const int nw = (blockDim.x + 31) >> 5;
-  v = (threadIdx.x < nw) ? sh[threadIdx.x] : sh[0];
+  v = (threadIdx.x < nw) ? sh[threadIdx.x] : ident;
   if (w == 0)
     for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
   __syncthreads();
@@ -342,12 +343,12 @@ __device__ double row_lse(const float* x, int V, int* nan_flag, double* sh, int*
     if (f != f) nan = 1;
     mx = fmax(mx, (double)f);
   }
-  nan = block_reduce(nan, OrOp(), shi);
+  nan = block_reduce(nan, OrOp(), shi, 0);
   if (nan && threadIdx.x == 0) atomicOr(nan_flag, 1);
-  mx = block_reduce(mx, MaxOp(), sh);
+  mx = block_reduce(mx, MaxOp(), sh, (double)-INFINITY);
   double s = 0.0;
   for (int i = threadIdx.x; i < V; i += blockDim.x) s += exp((double)x[i] - mx);
-  s = block_reduce(s, SumOp(), sh);
+  s = block_reduce(s, SumOp(), sh, 0.0);
   return mx + log(s);
 }
 
@@ -379,7 +380,7 @@ __global__ void kl_kernel(const float* __restrict__ logits, const float* __restr
     const double lq = (double)q[i] - lse_q;
     kl += exp(lp) * (lp - lq);
   }
-  kl = block_reduce(kl, SumOp(), sh);
+  kl = block_reduce(kl, SumOp(), sh, 0.0);
   if (threadIdx.x == 0) out[r] = kl;
 }
 
@@ -399,7 +400,7 @@ __global__ void logitdiff_kernel(const float* __restrict__ logits, const float* 
   int nan = 0;
   for (int i = threadIdx.x; i < V; i += blockDim.x)
     if (q[i] != q[i] || c[i] != c[i]) nan = 1;
-  nan = block_reduce(nan, OrOp(), shi);
+  nan = block_reduce(nan, OrOp(), shi, 0);
   if (threadIdx.x == 0) {
     if (nan) atomicOr(nan_flag, 1);
     const int a = ans[it], d = dis[it];
@@ -428,7 +429,7 @@ __global__ void rms_kernel(const RmsJob* __restrict__ jobs) {
     const double d = (double)j.a[i] - (double)j.b[i];
     acc += d * d;
   }
-  acc = block_reduce(acc, SumOp(), sh);
+  acc = block_reduce(acc, SumOp(), sh, 0.0);
   if (threadIdx.x == 0) *j.out = sqrt(acc / (double)j.n);
 }
 
@@ -486,7 +487,7 @@ __global__ void rtn_groups_kernel(const float* __restrict__ in, float* __restric
     const double a = fabs((double)in[off]);
     mx = (a > mx) ? a : mx;
   }
-  mx = block_reduce(mx, MaxOp(), sh);
+  mx = block_reduce(mx, MaxOp(), sh, (double)-INFINITY);
   const double delta = (mx == 0.0) ? 0.0 : __ddiv_rn(mx, ldexp(1.0, bits - 1));
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const int64_t off = g0 + (i / cols) * ld + (i % cols);
