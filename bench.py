@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the PAHQ-ACDC patched-forward hot path (BASELINE.json metric:
+"patched forward passes/sec and ACDC end-to-end s").
+
+One STEP = scoring every present edge of ACDC iteration 1 (full mask; the
+run_acdc scoring block, proj/src/acdc.cpp:42-60) over the whole prompt batch,
+i.e. n_edges x items patched passes, through the C-ABI cqg_score_edges.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt2s]
+    python bench.py --impl reference ...    # reference CPU path on host cores
+
+Multi-GPU (torchrun, one rank per GPU): the prompt batch is sharded over
+ranks, per-edge partial KL sums are NCCL-allreduced inside libcqg.so; value
+is whole-job passes/s over the max-over-ranks device time ("strong" scaling:
+the total batch is fixed).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2510_23264_b200 import formats, synth  # noqa: E402
+
+CONFIGS = {
+    # BASELINE.json configs[1]: GPT-2-small shape, IOI-shaped prompts, batch 64
+    "gpt2s": dict(cfg=formats.ModelConfig(12, 12, 768, 64, 50257, 16, 1, 1), items=64,
+                  data="ioi"),
+    # configs[0]: toy attention-only transformer, batch 16
+    "toy": dict(cfg=formats.ModelConfig(2, 4, 128, 32, 512, 16, 1, 0), items=16, data="random"),
+    # configs[3]: GPT-2-medium shape, batch 256
+    "gpt2m": dict(cfg=formats.ModelConfig(24, 16, 1024, 64, 50257, 16, 1, 1), items=256,
+                  data="ioi"),
+}
+METRIC = "patched forward passes/sec and ACDC end-to-end s (1/2/4/8 B200 vs host CPU)"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def make_inputs(name):
+    c = CONFIGS[name]
+    cfg = c["cfg"]
+    w = synth.random_weights(cfg, 1)
+    if c["data"] == "ioi":
+        ds = synth.ioi_dataset(cfg, c["items"], 1)
+    else:
+        ds = synth.random_dataset(cfg, c["items"], 2)
+    return cfg, w, ds
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.index, self.proc, self.lines = index, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ------------------------------------------------------------------------------
+# reference CPU arm
+# ------------------------------------------------------------------------------
+def cpu_sample(cfg, w, ds, steps, warmup, threads=None):
+    """delta_l of the reference library (oracle/_ref) over a bounded sample:
+    the out-edges of head a0.0 (one policy) x 1 prompt, one pass per host
+    thread, in the reference's own OpenMP parallel-for (acdc.cpp:55-60)."""
+    os.environ.setdefault("CQREF_NO_RTN4", "1")
+    from oracle.oracle import Policy, Ref, ref_available
+    kind = "reference"
+    ref = Ref()
+    nthreads = threads or ref.max_threads()
+    ref.set_threads(nthreads)
+    with tempfile.TemporaryDirectory() as t:
+        wp, dp = os.path.join(t, "w.bin"), os.path.join(t, "d.jsonl")
+        formats.save_weights(w, wp)
+        formats.save_dataset_jsonl(ds.subset([0]), dp)
+        m = ref.open(wp, dp, 0)
+        from paper_2510_23264_b200.engine import graph_edges
+        _, src, dst = graph_edges(cfg)
+        cand = np.nonzero(src == 1)[0]  # node 1 = head a0.0
+        n = int(min(len(cand), max(8, nthreads)))
+        edges = cand[:n]
+        times = []
+        for i in range(warmup + steps):
+            _, ms_refresh, ms_score = m.time_delta_l(edges, Policy.head_quantized(), True)
+            if i >= warmup:
+                times.append(ms_score / 1e3)
+        m.close()
+    passes = n * 1
+    value = passes * len(times) / sum(times)
+    return {"value": value, "unit": "passes/s", "cores": nthreads, "kind": kind,
+            "sample": f"delta_l of {n} out-edges of a0.0 x 1 IOI prompt per step "
+                      f"(reference library compiled in place, OpenMP {nthreads} threads; "
+                      f"refresh_baselines excluded), {len(times)} steps",
+            "s_per_step": float(np.mean(times))}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg, w, ds = make_inputs(args.config)
+    try:
+        cb = cpu_sample(cfg, w, ds, args.steps, args.warmup)
+    except Exception as e:  # the oracle library always exists in-tree
+        print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}))
+        return
+    out = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "passes/s",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": cb["s_per_step"] * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "fp32-emulated e4m3/bf16", "data": "synthetic",
+           "config": config_block(args), "cpu_baseline": cb,
+           "e2e": {"value": cb["value"], "unit": "passes/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def config_block(args):
+    c = CONFIGS[args.config]
+    cfg = c["cfg"]
+    return {"workload": f"{args.config}: L{cfg.n_layers} H{cfg.n_heads} d{cfg.d_model} "
+                        f"V{cfg.vocab} S{cfg.seq_len}, {c['data']}-shaped prompts batch "
+                        f"{c['items']}, PAHQ (E4M3 heads, BF16 MLP, FP32 source/unembed), "
+                        f"KL, ACDC iteration-1 scoring of every edge",
+            "items": c["items"], "parallelism": f"items sharded over {args.gpus} GPU(s)",
+            "low_precision": "e4m3 (reference-pinned; INT8 per-channel not implemented)",
+            "l2": "inputs >> L2 (activations per step ~GBs)"}
+
+
+# ------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="gpt2s", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--acdc", action="store_true", help="also time a full PAHQ-ACDC run")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    from paper_2510_23264_b200 import engine as eng
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    cfg, w, ds = make_inputs(args.config)
+    items = len(ds)
+    lo, hi = rank * items // world, (rank + 1) * items // world
+    shard = ds.subset(list(range(lo, hi)))
+    e = eng.Engine(w, device=local)
+    e.set_dataset(shard, eng.KL, lo, items)
+    if world > 1:
+        import torch
+        obj = [eng.Engine.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        e.init_comm(obj[0], rank, world)
+    mask = np.ones(e.n_edges, bool)
+    edges = eng.sweep_order(cfg, mask)
+    pol = eng.PrecisionPolicy.head_quantized()
+    passes_per_step = len(edges) * items
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        e.score_edges(mask, edges, pol, True, eng.LOSS)
+    barrier()
+    dev_ms = 0.0
+    launches = 0
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            scores = e.score_edges(mask, edges, pol, True, eng.LOSS)
+            st = e.stats()
+            dev_ms += st["ms_device"]
+            launches += st["kernel_launches"]
+        wall = time.perf_counter() - t0
+    barrier()
+    dev_s = max_over_ranks(dev_ms / 1e3)
+    wall = max_over_ranks(wall)
+    value = passes_per_step * args.steps / dev_s
+
+    # end to end through the C-ABI with host buffers: dataset tokens H2D
+    # (cqg_set_dataset) + mask/edge list H2D + per-edge scores D2H each step
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e.set_dataset(shard, eng.KL, lo, items)
+        e.score_edges(mask, edges, pol, True, eng.LOSS)
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    h2d = shard.clean.nbytes + shard.corrupt.nbytes + shard.answer.nbytes + \
+        shard.distractor.nbytes + mask.size + edges.size * 4
+    d2h = edges.size * 8
+
+    # one profiled step for the roofline of the dominant kernel
+    e.set_option("profile", 1)
+    e.score_edges(mask, edges, pol, True, eng.LOSS)
+    prof = e.profile()
+    e.set_option("profile", 0)
+    hbm, bf16, src = load_peaks()
+    name, p = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    if p["flops"] > 0:
+        ach = p["flops"] / (p["ms"] / 1e3) / 1e12
+        # exact-semantics SIMT GEMM: bounded by FP32 CUDA-core throughput;
+        # tensor-core GEMMs: by the measured bf16 (x2 for fp8) tensor peak
+        if name.startswith("gemm_tc_fp8"):
+            peak, unit, bound, psrc = 2 * bf16, "TFLOP/s", "tensor", f"2x {src} bf16"
+        elif name.startswith("gemm_tc"):
+            peak, unit, bound, psrc = bf16, "TFLOP/s", "tensor", src
+        else:
+            peak, unit, bound, psrc = 148 * 128 * 2 * 1.965e9 / 1e12, "TFLOP/s", "fp32-simt", \
+                "nominal FP32 CUDA-core peak"
+        traffic = None
+    else:
+        ach = p["bytes"] / (p["ms"] / 1e3) / 1e9
+        peak, unit, bound, psrc = hbm, "GB/s", "hbm", src
+        traffic = None
+    roofline = {"bound": bound, "kernel": name, "achieved": ach, "peak": peak, "unit": unit,
+                "frac": ach / peak, "traffic": traffic, "peak_source": psrc,
+                "kernel_share_of_step": p["ms"] / max(1e-9, sum(v["ms"] for v in prof.values())),
+                "per_kernel": {k: {"ms": v["ms"], "launches": v["launches"],
+                                   "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9,
+                                   "gbs": v["bytes"] / max(v["ms"], 1e-9) / 1e6}
+                               for k, v in prof.items()}}
+
+    acdc = None
+    if args.acdc and world == 1:
+        c = eng.method_prune_config(eng.PAHQ)
+        t0 = time.perf_counter()
+        r = e.run_acdc(c)
+        acdc = {"seconds": time.perf_counter() - t0, "steps": r.steps,
+                "kept_edges": int(r.final_mask.sum()), "tau": c.tau}
+
+    if rank == 0:
+        cb = None
+        if not args.no_cpu:
+            try:
+                cb = cpu_sample(cfg, w, ds, steps=1, warmup=0)
+            except Exception as ex:
+                cb = {"unavailable": f"{type(ex).__name__}: {ex}"}
+        out = {"metric": METRIC, "value": value, "unit": "passes/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "e4m3/bf16/fp32 (exact)",
+               "data": "synthetic (random-init weights per support.hpp, IOI-shaped prompts)",
+               "config": config_block(args), "clocks": clk.summary(),
+               "e2e": {"value": passes_per_step * args.steps / e2e_s, "unit": "passes/s",
+                       "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+               "gpu_launches": int(launches), "wall_s": wall, "roofline": roofline,
+               "cpu_baseline": cb, "passes_per_step": passes_per_step,
+               "acdc_end_to_end": acdc}
+        print(json.dumps(out))
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -108,13 +108,22 @@ int cqg_graph_edges(const cqg_config* cfg, int32_t* edge_src, int32_t* edge_dst)
 
 /* Timing/diagnostic counters of the last cqg_score_edges call. */
 typedef struct {
-  double ms_total, ms_baseline, ms_passes, ms_unembed;
+  double ms_total;  /* host wall time of the call */
+  double ms_device; /* CUDA-event time on the engine stream, first to last launch */
+  double ms_baseline, ms_passes;
   int64_t passes;          /* (edge, item) pairs evaluated on this rank */
   int64_t kernel_launches; /* kernels launched by the call */
   int64_t fallback_elems;  /* tensor-core outputs recomputed on the exact path */
   int64_t h2d_bytes, d2h_bytes;
 } cqg_stats;
 int cqg_last_stats(cqg_ctx* ctx, cqg_stats* out);
+
+/* Per-kernel-class totals of the last cqg_score_edges call: launches,
+ * algorithmic FLOPs / HBM bytes, and (with option "profile"=1) CUDA-event
+ * device time. Entry i < cqg_profile_count(). */
+int cqg_profile_count(cqg_ctx* ctx);
+int cqg_profile_entry(cqg_ctx* ctx, int i, char* name64, double* ms, double* flops, double* bytes,
+                      int64_t* launches);
 
 /* Engine knobs: 0 = exact SIMT GEMMs everywhere (debug), 1 = tensor cores
  * with exactness-certified fallback (default). */

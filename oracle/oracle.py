@@ -257,6 +257,18 @@ class RefModel:
                                                   int(per_edge), mode, out.ctypes.data_as(C.c_void_p)))
         return out
 
+    def time_delta_l(self, edges, policy: Policy, per_edge=True):
+        """(scores, ms_refresh, ms_score): delta_l over edges in an OpenMP
+        parallel-for (acdc.cpp:55-60), baseline refresh timed separately."""
+        e = np.ascontiguousarray(edges, np.int32)
+        out = np.empty(e.size, np.float64)
+        mr, ms = C.c_double(), C.c_double()
+        self.ref.check(self.lib.cqref_time_delta_l(self.h, e.ctypes.data_as(C.c_void_p), e.size,
+                                                   C.byref(policy), int(per_edge),
+                                                   out.ctypes.data_as(C.c_void_p), C.byref(mr),
+                                                   C.byref(ms)))
+        return out, mr.value, ms.value
+
     def run_acdc(self, prune: Prune) -> AcdcResult:
         E = self.n_edges
         cap = E * max(1, prune.max_steps)

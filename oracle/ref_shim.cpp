@@ -13,6 +13,8 @@
 #include <omp.h>
 
 #include <cstdint>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -125,8 +127,12 @@ struct Handle {
 
 std::unique_ptr<ImageBank> full_bank(const WeightSet& w) {
   std::vector<std::pair<Precision, LowMode>> needs = {
-      {Precision::P8, LowMode::E4m3}, {Precision::P8, LowMode::Rtn4},
-      {Precision::P16, LowMode::E4m3}, {Precision::P32, LowMode::E4m3}};
+      {Precision::P8, LowMode::E4m3}, {Precision::P16, LowMode::E4m3},
+      {Precision::P32, LowMode::E4m3}};
+  // The 4-bit grid image is only needed by Rtn4 policies; skipping it keeps
+  // the CPU-baseline setup at GPT-2 scale short (CQREF_NO_RTN4=1).
+  const char* no4 = std::getenv("CQREF_NO_RTN4");
+  if (!(no4 && *no4 == '1')) needs.push_back({Precision::P8, LowMode::Rtn4});
   return std::make_unique<ImageBank>(w, needs);
 }
 
@@ -412,6 +418,38 @@ int cqref_score_edges(void* hv, const uint8_t* mask, const int* edge_ids, int n,
     }
     for (const std::string& e : errs)
       if (!e.empty()) throw std::runtime_error(e);
+  });
+}
+
+// CPU baseline timing: refresh_baselines for the edges'
+// policies (untimed, reported in *ms_refresh), then DeltaLEngine::delta_l
+// over the edges in an OpenMP parallel-for exactly as acdc.cpp:55-60 (timed,
+// *ms_score). Full mask.
+int cqref_time_delta_l(void* hv, const int* edge_ids, int n, const cqref_policy* base,
+                       int per_edge_policy, double* out, double* ms_refresh, double* ms_score) {
+  return guarded([&] {
+    Handle* h = static_cast<Handle*>(hv);
+    h->g->reset_mask();
+    PrecisionPolicy bp = policy_from(*base);
+    std::vector<Edge> order;
+    for (int i = 0; i < n; ++i) order.push_back(h->g->all_edges().at(static_cast<size_t>(edge_ids[i])));
+    std::vector<PrecisionPolicy> policies(order.size());
+    std::map<std::string, size_t> seen;
+    auto t0 = std::chrono::steady_clock::now();
+    for (size_t i = 0; i < order.size(); ++i) {
+      policies[i] = per_edge_policy ? policy_for_edge(order[i], *h->g, bp) : bp;
+      if (!seen.count(policies[i].key())) {
+        h->eng->refresh_baselines(policies[i]);
+        seen.emplace(policies[i].key(), i);
+      }
+    }
+    auto t1 = std::chrono::steady_clock::now();
+#pragma omp parallel for schedule(dynamic)
+    for (int64_t i = 0; i < static_cast<int64_t>(order.size()); ++i)
+      out[i] = h->eng->delta_l(order[static_cast<size_t>(i)], policies[static_cast<size_t>(i)]);
+    auto t2 = std::chrono::steady_clock::now();
+    *ms_refresh = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    *ms_score = std::chrono::duration<double, std::milli>(t2 - t1).count();
   });
 }
 

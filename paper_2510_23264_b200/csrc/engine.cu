@@ -304,6 +304,51 @@ struct Engine {
 
   void launched(int n = 1) { stats.kernel_launches += n; }
 
+  // ---- per-kernel-class device timing (option "profile") ---------------------
+  struct KStat {
+    double ms = 0, flops = 0, bytes = 0;
+    int64_t launches = 0;
+  };
+  std::map<std::string, KStat> kprof;
+  struct Pending {
+    std::string name;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  std::vector<Pending> pending;
+  int64_t opt_profile = 0;
+  struct Prof {  // RAII region around one launch
+    Engine* e;
+    Pending p;
+    Prof(Engine* en, const char* name, double flops = 0, double bytes = 0) : e(en) {
+      e->launched();
+      auto& k = e->kprof[name];
+      k.launches++, k.flops += flops, k.bytes += bytes;
+      if (!e->opt_profile) return;
+      p.name = name, p.flops = flops, p.bytes = bytes;
+      cudaEventCreate(&p.a);
+      cudaEventCreate(&p.b);
+      cudaEventRecord(p.a, e->st);
+    }
+    ~Prof() {
+      if (!e->opt_profile) return;
+      cudaEventRecord(p.b, e->st);
+      e->pending.push_back(p);
+    }
+  };
+  void collect_profile() {
+    if (pending.empty()) return;
+    cudaStreamSynchronize(st);
+    for (auto& p : pending) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, p.a, p.b);
+      kprof[p.name].ms += ms;
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    pending.clear();
+  }
+
   // ---- weights -------------------------------------------------------------
   const float* W(int m, int prec, int mode) {
     if (prec == 2) return master[m]->as<float>();
@@ -349,36 +394,44 @@ struct Engine {
   // ---- launch helpers --------------------------------------------------------
   void fold(const std::vector<FoldOp>& ops, const std::vector<FoldProg>& progs, size_t elems) {
     if (progs.empty()) return;
+    // algorithmic bytes: every operand read once and every stored value written once
+    double words = 0;
+    for (const FoldOp& o : ops)
+      words += 1.0 + (o.a && o.a != CQG_REG_PREV ? 1.0 : 0.0) + (o.dst ? 1.0 : 0.0);
     reserve(up_bytes(ops.size(), sizeof(FoldOp)) + up_bytes(progs.size(), sizeof(FoldProg)));
+    Prof pf(this, "fold", 0, words * 4.0 * (double)elems);
     launch_fold(upload(ops), upload(progs), (int)progs.size(), (int64_t)elems, st);
-    launched();
   }
   void ln(const std::vector<LnJob>& jobs, int l_gamma, int l_beta, int prec) {
     if (jobs.empty()) return;
     int mx = 0;
-    for (auto& j : jobs) mx = std::max(mx, j.rows);
+    double rows = 0;
+    for (auto& j : jobs) mx = std::max(mx, j.rows), rows += j.rows;
     reserve(up_bytes(jobs.size(), sizeof(LnJob)));
+    Prof pf(this, "layernorm", 0, rows * g.D * 4.0 * 3.0);
     launch_layernorm(upload(jobs), (int)jobs.size(), mx, master[l_gamma]->as<float>(),
                      master[l_beta]->as<float>(), g.D, prec, st);
-    launched();
   }
-  void gemm(const std::vector<GemmJob>& jobs) {
+  void gemm(const std::vector<GemmJob>& jobs, const char* name = "gemm_exact") {
     if (jobs.empty()) return;
     std::vector<int> ts(jobs.size());
     int total = 0;
+    double flops = 0;
     for (size_t i = 0; i < jobs.size(); ++i) {
       ts[i] = total;
       total += gemm_exact_tiles(jobs[i].M, jobs[i].N);
+      flops += 2.0 * jobs[i].M * (double)jobs[i].N * jobs[i].K;
     }
     reserve(up_bytes(jobs.size(), sizeof(GemmJob)) + up_bytes(ts.size(), sizeof(int)));
+    Prof pf(this, name, flops, 0);
     launch_gemm_exact(upload(jobs), upload(ts), (int)jobs.size(), total, st);
-    launched();
   }
   void attn(const std::vector<AttnJob>& jobs, int nb) {
     if (jobs.empty()) return;
     reserve(up_bytes(jobs.size(), sizeof(AttnJob)));
+    const double S = g.S;
+    Prof pf(this, "attention", (double)jobs.size() * nb * 2.0 * g.dk * S * (S + 1), 0);
     launch_attention(upload(jobs), (int)jobs.size(), nb, g.S, g.dk, st);
-    launched();
   }
 
   void check_policy(const Policy& P) {
@@ -442,7 +495,7 @@ struct Engine {
       aj.push_back({qkv + (j * 3) * per, qkv + (j * 3 + 1) * per, qkv + (j * 3 + 2) * per,
                     z + j * per, dk, target ? 2 : p_low});
     }
-    gemm(gj);
+    gemm(gj, "gemm_qkv");
     attn(aj, nb);
     const float* wo = W(g.mat(7, l), P.wo_precision(l), P.mode);
     gj.clear();
@@ -455,7 +508,7 @@ struct Engine {
       o.prec = target ? 2 : p_low, o.epi = 0;
       gj.push_back(o);
     }
-    gemm(gj);
+    gemm(gj, "gemm_wo");
   }
 
   // MLP (model.cpp:720-739)
@@ -483,8 +536,8 @@ struct Engine {
       b.M = RB, b.N = D, b.K = 4 * D, b.lda = 4 * D, b.ldb = D, b.ldc = D, b.prec = p, b.epi = 0;
       g2.push_back(b);
     }
-    gemm(g1);
-    gemm(g2);
+    gemm(g1, "gemm_mlp_in");
+    gemm(g2, "gemm_mlp_out");
   }
 
   // unembed (model.cpp:741-753): all_rows=false computes only row S-1 of
@@ -507,7 +560,7 @@ struct Engine {
       a.M = rows, a.N = V, a.K = D, a.lda = D, a.ldb = V, a.ldc = V, a.prec = p, a.epi = 0;
       gj.push_back(a);
     }
-    gemm(gj);
+    gemm(gj, "gemm_unembed");
   }
 
   void run_embed(const Policy& P, const int* d_tok, float* out, int nb) {
@@ -829,13 +882,15 @@ struct Engine {
         for (int r = 0; r < rows; ++r) item_of[r] = r % nb;
         double* tmp = reinterpret_cast<double*>(scratch("p_kl", (size_t)rows * 2));
         reserve(up_bytes(item_of.size(), sizeof(int)));
-        if (metric == 0)
-          launch_kl(logits, R.logits.as<float>(), R.lse.as<double>(), upload(item_of), rows, V, tmp,
-                    d_nan, st);
-        else
-          launch_logitdiff(logits, R.logits.as<float>(), upload(item_of), d_ans.as<int>(),
-                           d_dis.as<int>(), rows, V, tmp, d_nan, st);
-        launched();
+        {
+          Prof pf(this, metric == 0 ? "kl" : "logitdiff", 0, (double)rows * V * 4.0 * 2.0);
+          if (metric == 0)
+            launch_kl(logits, R.logits.as<float>(), R.lse.as<double>(), upload(item_of), rows, V,
+                      tmp, d_nan, st);
+          else
+            launch_logitdiff(logits, R.logits.as<float>(), upload(item_of), d_ans.as<int>(),
+                             d_dis.as<int>(), rows, V, tmp, d_nan, st);
+        }
         for (size_t j = 0; j < unembed_edges.size(); ++j)
           CK(cudaMemcpyAsync(d_d + (size_t)unembed_edges[j] * nb, tmp + j * nb, sizeof(double) * nb,
                              cudaMemcpyDeviceToDevice, st));
@@ -895,6 +950,11 @@ struct Engine {
                    bool per_edge, int mode, double* out) {
     auto t0 = std::chrono::steady_clock::now();
     stats = cqg_stats{};
+    kprof.clear();
+    cudaEvent_t ev0, ev1;
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaEventRecord(ev0, st));
     if (B == 0) throw Error(1, "score_edges: no dataset (call cqg_set_dataset)");
     if (mode != 0 && mode != 1) throw Error(1, "score_mode must be 0 (loss) or 1 (act)");
     check_policy(base);
@@ -997,6 +1057,14 @@ struct Engine {
     for (int i = 0; i < n; ++i) out[i] = sums[i] / (double)item_total;
     stats.ms_baseline = ms_base;
     stats.ms_passes = ms_pass;
+    CK(cudaEventRecord(ev1, st));
+    CK(cudaEventSynchronize(ev1));
+    float dms = 0;
+    CK(cudaEventElapsedTime(&dms, ev0, ev1));
+    stats.ms_device = dms;
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    collect_profile();
     stats.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
 
@@ -1289,11 +1357,26 @@ int cqg_last_stats(cqg_ctx* ctx, cqg_stats* out) {
   });
 }
 
+int cqg_profile_count(cqg_ctx* ctx) { return ctx ? (int)ctx->e->kprof.size() : 0; }
+
+int cqg_profile_entry(cqg_ctx* ctx, int i, char* name64, double* ms, double* flops, double* bytes,
+                      int64_t* launches) {
+  return guarded([&] {
+    if (!ctx || i < 0 || i >= (int)ctx->e->kprof.size()) throw Error(1, "cqg_profile_entry: bad index");
+    auto it = ctx->e->kprof.begin();
+    std::advance(it, i);
+    std::snprintf(name64, 64, "%s", it->first.c_str());
+    *ms = it->second.ms, *flops = it->second.flops, *bytes = it->second.bytes;
+    *launches = it->second.launches;
+  });
+}
+
 int cqg_set_option(cqg_ctx* ctx, const char* key, int64_t value) {
   return guarded([&] {
     if (!ctx || !key) throw Error(1, "null argument");
     std::string k(key);
     if (k == "exact") ctx->e->opt_exact = value;
+    else if (k == "profile") ctx->e->opt_profile = value;
     else if (k == "mem_budget") ctx->e->opt_mem_budget = value;
     else throw Error(1, "cqg_set_option: unknown key " + k);
   });

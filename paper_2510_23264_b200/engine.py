@@ -47,8 +47,8 @@ class CqgConfig(C.Structure):
 
 
 class CqgStats(C.Structure):
-    _fields_ = [("ms_total", C.c_double), ("ms_baseline", C.c_double), ("ms_passes", C.c_double),
-                ("ms_unembed", C.c_double), ("passes", C.c_int64), ("kernel_launches", C.c_int64),
+    _fields_ = [("ms_total", C.c_double), ("ms_device", C.c_double), ("ms_baseline", C.c_double),
+                ("ms_passes", C.c_double), ("passes", C.c_int64), ("kernel_launches", C.c_int64),
                 ("fallback_elems", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
@@ -190,6 +190,8 @@ def load_library():
     lib.cqg_graph_edges.argtypes = [C.POINTER(CqgConfig), vp, vp]
     lib.cqg_last_stats.argtypes = [vp, C.POINTER(CqgStats)]
     lib.cqg_set_option.argtypes = [vp, C.c_char_p, C.c_int64]
+    lib.cqg_profile_count.argtypes = [vp]
+    lib.cqg_profile_entry.argtypes = [vp, C.c_int, C.c_char_p, vp, vp, vp, vp]
     lib.cqg_diag_e4m3_range.argtypes = [C.c_uint32, C.c_uint64, vp]
     lib.cqg_diag_bf16_range.argtypes = [C.c_uint32, C.c_uint64, vp]
     lib.cqg_diag_libm_range.argtypes = [C.c_int, C.c_uint32, C.c_uint64, vp]
@@ -354,6 +356,20 @@ class Engine:
         s = CqgStats()
         _check(self.lib.cqg_last_stats(self.h, C.byref(s)))
         return {k: getattr(s, k) for k, _ in CqgStats._fields_}
+
+    def profile(self) -> dict:
+        """Per-kernel-class totals of the last score call (cqg_profile_entry)."""
+        out = {}
+        n = self.lib.cqg_profile_count(self.h)
+        for i in range(n):
+            name = C.create_string_buffer(64)
+            ms, fl, by = C.c_double(), C.c_double(), C.c_double()
+            la = C.c_int64()
+            _check(self.lib.cqg_profile_entry(self.h, i, name, C.byref(ms), C.byref(fl),
+                                              C.byref(by), C.byref(la)))
+            out[name.value.decode()] = {"ms": ms.value, "flops": fl.value, "bytes": by.value,
+                                        "launches": la.value}
+        return out
 
     def set_option(self, key: str, value: int):
         _check(self.lib.cqg_set_option(self.h, key.encode(), int(value)))
