@@ -16,6 +16,13 @@ int cqg_diag_bf16_range(uint32_t lo, uint64_t count, uint16_t* out_host);
 /* which: 0 glibc-exact expf, 1 glibc-exact erff, 2 reference gelu
  * (kernels.cpp:226). */
 int cqg_diag_libm_range(int which, uint32_t lo, uint64_t count, float* out_host);
+/* One tensor-core GEMM C = round(A . B^T) (A: M x K, Bt: N x K, values on
+ * the elem grid: 0 E4M3, 1 BF16) through the production tcgen05 kernel +
+ * exactness fixup, and the same product through the exact sequential SIMT
+ * kernel. prec: output rounding (0 E4M3, 1 BF16, 2 none = raw accumulators);
+ * epi 1 = round-gelu-round. *n_fix = elements recomputed exactly. */
+int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const float* A,
+                     const float* Bt, float* out_tc, float* out_exact, uint32_t* n_fix);
 #ifdef __cplusplus
 }
 #endif

@@ -3,8 +3,10 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/cqg_diag.h"
+#include "gemm_tc.h"
 #include "kernels.h"
 
 namespace {
@@ -28,5 +30,91 @@ int cqg_diag_bf16_range(uint32_t lo, uint64_t count, uint16_t* out) {
 }
 int cqg_diag_libm_range(int which, uint32_t lo, uint64_t count, float* out) {
   return run(count, out, [&](float* d) { cqg::launch_libm_all(d, lo, count, which, 0); });
+}
+
+int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const float* A,
+                     const float* Bt, float* out_tc, float* out_exact, uint32_t* n_fix) {
+  using namespace cqg;
+  const int esz = elem == kTcBF16 ? 2 : 1;
+  float *dA, *dBt, *dB, *dC1, *dC2, *an, *bn;
+  uint8_t *pA, *pB;
+  uint32_t *fix, *cnt;
+  TcJob* dj;
+  int* dts;
+  GemmJob* dg;
+  size_t fcap = 1u << 20;
+  cudaMalloc(&dA, (size_t)M * K * 4);
+  cudaMalloc(&dBt, (size_t)N * K * 4);
+  cudaMalloc(&dB, (size_t)N * K * 4);
+  cudaMalloc(&dC1, (size_t)M * N * 4);
+  cudaMalloc(&dC2, (size_t)M * N * 4);
+  cudaMalloc(&an, (size_t)M * 4);
+  cudaMalloc(&bn, (size_t)N * 4);
+  cudaMalloc(&pA, (size_t)M * K * esz);
+  cudaMalloc(&pB, (size_t)N * K * esz);
+  cudaMalloc(&fix, fcap * 12);
+  cudaMalloc(&cnt, 16);
+  cudaMalloc(&dj, sizeof(TcJob));
+  cudaMalloc(&dts, sizeof(int));
+  cudaMalloc(&dg, sizeof(GemmJob));
+  cudaMemcpy(dA, A, (size_t)M * K * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dBt, Bt, (size_t)N * K * 4, cudaMemcpyHostToDevice);
+  cudaMemset(cnt, 0, 16);
+  {
+    // pack_t(in: K x N row-major) -> out[n][k]; feed transposed host copies so
+    // that pA is A (M x K) and pB is Bt (N x K), both K-major.
+    float* tmp;
+    cudaMalloc(&tmp, (size_t)(M > N ? M : N) * K * 4);
+    // tmp = A^T (K x M) in floats via pack-free transpose on host copy
+    std::vector<float> At((size_t)M * K);
+    for (int m = 0; m < M; ++m)
+      for (int k = 0; k < K; ++k) At[(size_t)k * M + m] = A[(size_t)m * K + k];
+    cudaMemcpy(tmp, At.data(), (size_t)M * K * 4, cudaMemcpyHostToDevice);
+    launch_pack_t(tmp, K, M, M, pA, K, elem, 0);
+    std::vector<float> Bk((size_t)N * K);
+    for (int n = 0; n < N; ++n)
+      for (int k = 0; k < K; ++k) Bk[(size_t)k * N + n] = Bt[(size_t)n * K + k];
+    cudaMemcpy(tmp, Bk.data(), (size_t)N * K * 4, cudaMemcpyHostToDevice);
+    launch_pack_t(tmp, K, N, N, pB, K, elem, 0);
+    cudaMemcpy(dB, Bk.data(), (size_t)N * K * 4, cudaMemcpyHostToDevice);  // K x N row-major
+    cudaDeviceSynchronize();
+    cudaFree(tmp);
+  }
+  launch_rownorm(pB, (int64_t)K * esz, elem, N, 0, K, bn, 0);
+  TcLaunch L{};
+  bool ok = tc_make_map(&L.tmA, pA, elem, M, K, (uint64_t)K * esz, kTcBM) &&
+            tc_make_map(&L.tmB, pB, elem, N, K, (uint64_t)K * esz, kTcBN);
+  int rc = 0;
+  if (!ok) rc = 2;
+  if (!rc) {
+    L.A = pA, L.B = pB, L.lda = (int64_t)K * esz, L.ldb = (int64_t)K * esz, L.elem = elem;
+    L.kappa = 8.0f;
+    launch_rownorm(pA, L.lda, elem, M, 0, K, an, 0);
+    L.a_norm = an;
+    TcJob j{};
+    j.M = M, j.N = N, j.K = K, j.out_f32 = dC1, j.ldo = N, j.b_norm = bn, j.prec = prec, j.epi = epi;
+    cudaMemcpy(dj, &j, sizeof j, cudaMemcpyHostToDevice);
+    L.n_jobs = 1;
+    L.total_tiles = ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
+    L.fix = fix, L.fix_count = cnt, L.fix_cap = (uint32_t)fcap;
+    launch_gemm_tc(L, dj, 0);
+    launch_gemm_fixup(L, dj, (uint32_t)fcap, 0);
+    // exact reference product on the decoded grid values
+    GemmJob gj{};
+    gj.A = dA, gj.B = dB, gj.C = dC2, gj.M = M, gj.N = N, gj.K = K, gj.lda = K, gj.ldb = N,
+    gj.ldc = N, gj.prec = prec, gj.epi = epi;
+    cudaMemcpy(dg, &gj, sizeof gj, cudaMemcpyHostToDevice);
+    int zero = 0;
+    cudaMemcpy(dts, &zero, sizeof zero, cudaMemcpyHostToDevice);
+    launch_gemm_exact(dg, dts, 1, gemm_exact_tiles(M, N), 0);
+    if (cudaDeviceSynchronize() != cudaSuccess) rc = 2;
+    cudaMemcpy(out_tc, dC1, (size_t)M * N * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(out_exact, dC2, (size_t)M * N * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(n_fix, cnt, 4, cudaMemcpyDeviceToHost);
+  }
+  for (void* p : {(void*)dA, (void*)dBt, (void*)dB, (void*)dC1, (void*)dC2, (void*)an, (void*)bn,
+                  (void*)pA, (void*)pB, (void*)fix, (void*)cnt, (void*)dj, (void*)dts, (void*)dg})
+    cudaFree(p);
+  return rc;
 }
 }

@@ -3,7 +3,12 @@
 // the reference (proj/src/patching.cpp, model.cpp, acdc.cpp).
 #include "engine.h"
 
+#include <dlfcn.h>
 #include <nccl.h>
+
+#include <tuple>
+
+#include "gemm_tc.h"
 
 #include <algorithm>
 #include <chrono>
@@ -25,10 +30,42 @@ static thread_local std::string g_err;
                       __FILE__ + ":" + std::to_string(__LINE__));                               \
   } while (0)
 
-#define NK(x)                                                                                   \
-  do {                                                                                          \
-    ncclResult_t r_ = (x);                                                                      \
-    if (r_ != ncclSuccess) throw Error(2, std::string("NCCL error: ") + ncclGetErrorString(r_)); \
+// NCCL is resolved at run time (dlopen of libnccl.so.2) instead of being
+// linked: a process that already loaded torch's bundled NCCL reuses that copy,
+// and loading libcqg.so never pins an NCCL version torch would then clash with.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+      api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+      api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+      api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+      api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    }
+  }
+  if (!api.AllReduce) throw Error(2, "NCCL (libnccl.so.2) not available");
+  return api;
+}
+
+#define NK(x)                                                                                  \
+  do {                                                                                         \
+    ncclResult_t r_ = (x);                                                                     \
+    if (r_ != ncclSuccess)                                                                     \
+      throw Error(2, std::string("NCCL error: ") + cqg::nccl().GetErrorString(r_));                 \
   } while (0)
 
 // ===========================================================================
@@ -247,7 +284,7 @@ struct Engine {
 
   Engine(const cqg_config& c) : g(c) {}
   ~Engine() {
-    if (comm) ncclCommDestroy(comm);
+    if (comm) nccl().CommDestroy(comm);
     if (h_stage) cudaFreeHost(h_stage);
     if (st) cudaStreamDestroy(st);
   }
@@ -442,13 +479,123 @@ struct Engine {
     if (P.tm >= 0 && (!g.mlp || P.tm >= g.L)) throw Error(1, "forward: target mlp out of range");
   }
 
+  // ---- tensor-core GEMMs ------------------------------------------------------
+  // Packed K-major weight images for the tensor cores (built once per layer
+  // from the bit-exact FP32 grid images) and their per-row L2 norms.
+  struct PackedB {
+    DeviceBuf buf, norm;
+    int rows = 0, cols = 0, elem = 0;
+  };
+  std::map<std::tuple<int, int, int>, std::unique_ptr<PackedB>> packed;
+  DeviceBuf fix_list, fix_cnt;
+  static constexpr uint32_t kFixCap = 1u << 22;
+
+  // which: 0 QKV [3D x D], 1 W_O [D x D] (per-head K slices), 2 W_in^T [4D x D],
+  // 3 W_out^T [D x 4D]
+  const PackedB& packedB(int which, int l, int elem, int prec, int mode) {
+    auto& p = packed[{which, l, elem}];
+    if (p) return *p;
+    p = std::make_unique<PackedB>();
+    const int D = g.D, esz = elem == kTcBF16 ? 2 : 1;
+    p->elem = elem;
+    if (which == 0) p->rows = 3 * D, p->cols = D;
+    else if (which == 1) p->rows = D, p->cols = D;
+    else if (which == 2) p->rows = 4 * D, p->cols = D;
+    else p->rows = D, p->cols = 4 * D;
+    p->buf.ensure((size_t)p->rows * p->cols * esz);
+    const int64_t ld = p->cols;
+    if (which == 0) {
+      for (int c = 0; c < 3; ++c)
+        launch_pack_t(W(g.mat(4 + c, l), prec, mode), D, D, D,
+                      p->buf.as<uint8_t>() + (size_t)c * D * D * esz, ld, elem, st);
+    } else if (which == 1) {
+      launch_pack_t(W(g.mat(7, l), prec, mode), D, D, D, p->buf.p, ld, elem, st);
+    } else if (which == 2) {
+      launch_pack_t(W(g.mat(10, l), prec, mode), D, 4 * D, 4 * D, p->buf.p, ld, elem, st);
+    } else {
+      launch_pack_t(W(g.mat(11, l), prec, mode), 4 * D, D, D, p->buf.p, ld, elem, st);
+    }
+    if (which == 1) {  // norms per head K-slice: [H][D]
+      p->norm.ensure((size_t)g.H * D * 4);
+      for (int h = 0; h < g.H; ++h)
+        launch_rownorm(p->buf.as<uint8_t>(), ld * esz, elem, D, h * g.dk, g.dk,
+                       p->norm.as<float>() + (size_t)h * D, st);
+    } else {
+      p->norm.ensure((size_t)p->rows * 4);
+      launch_rownorm(p->buf.as<uint8_t>(), ld * esz, elem, p->rows, 0, p->cols, p->norm.as<float>(), st);
+    }
+    launched(2);
+    return *p;
+  }
+
+  bool tc_dims_ok(int K, int elem) const { return (K * (elem == kTcBF16 ? 2 : 1)) % 32 == 0; }
+
+  void gemm_tc(int elem, const void* A, int64_t a_rows, int a_k, const PackedB& B,
+               std::vector<TcJob>& jobs, const char* name) {
+    if (jobs.empty()) return;
+    const int esz = elem == kTcBF16 ? 2 : 1;
+    TcLaunch L{};
+    if (!tc_make_map(&L.tmA, A, elem, (uint64_t)a_rows, (uint64_t)a_k, (uint64_t)a_k * esz, kTcBM))
+      throw Error(2, "cuTensorMapEncodeTiled failed for the A operand");
+    if (!tc_make_map(&L.tmB, B.buf.p, elem, (uint64_t)B.rows, (uint64_t)B.cols,
+                     (uint64_t)B.cols * esz, kTcBN))
+      throw Error(2, "cuTensorMapEncodeTiled failed for the B operand");
+    L.A = reinterpret_cast<const uint8_t*>(A);
+    L.B = B.buf.as<uint8_t>();
+    L.lda = (int64_t)a_k * esz;
+    L.ldb = (int64_t)B.cols * esz;
+    L.elem = elem;
+    L.kappa = 8.0f;
+    float* an = scratch("tc_anorm", (size_t)a_rows);
+    {
+      Prof pf(this, "rownorm", 0, (double)a_rows * a_k * esz);
+      launch_rownorm(L.A, L.lda, elem, (int)a_rows, 0, a_k, an, st);
+    }
+    L.a_norm = an;
+    int total = 0;
+    double flops = 0, bytes = 0;
+    for (TcJob& j : jobs) {
+      j.tile0 = total;
+      total += ((j.M + kTcBM - 1) / kTcBM) * ((j.N + kTcBN - 1) / kTcBN);
+      flops += 2.0 * j.M * (double)j.N * j.K;
+      bytes += (double)j.M * j.N * ((j.out_f32 ? 4 : 0) + (j.out_pack ? esz : 0));
+    }
+    L.n_jobs = (int)jobs.size();
+    L.total_tiles = total;
+    if (!fix_list.p) {
+      fix_list.ensure((size_t)kFixCap * 12);
+      fix_cnt.ensure(16);
+      CK(cudaMemsetAsync(fix_cnt.p, 0, 16, st));
+    }
+    L.fix = fix_list.as<uint32_t>();
+    L.fix_count = fix_cnt.as<uint32_t>();
+    L.fix_cap = kFixCap;
+    reserve(up_bytes(jobs.size(), sizeof(TcJob)));
+    const TcJob* dj = upload(jobs);
+    {
+      Prof pf(this, elem == kTcBF16 ? (std::string("gemm_tc_bf16_") + name).c_str()
+                                    : (std::string("gemm_tc_fp8_") + name).c_str(),
+              flops, bytes);
+      launch_gemm_tc(L, dj, st);
+    }
+    {
+      Prof pf(this, "gemm_fixup");
+      launch_gemm_fixup(L, dj, kFixCap, st);
+    }
+    launch_fix_account(L.fix_count, st);
+    launched();
+  }
+
   // ---- node computations ----------------------------------------------------
   // attention layer (model.cpp:622-718) for a list of (input, head, output)
   void run_heads(int l, const Policy& P, const std::vector<HeadIO>& jobs, int nb) {
     if (jobs.empty()) return;
-    const int RB = nb * g.S, D = g.D, dk = g.dk;
+    const int RB = nb * g.S, D = g.D, dk = g.dk, H = g.H;
     const size_t SEG = segf(nb);
     const int p_low = P.att;
+    // tensor cores for the E4M3 projections of non-target heads
+    const bool tc = !opt_exact && p_low == 0 && P.mode == 0 && tc_dims_ok(D, kTcE4M3) &&
+                    tc_dims_ok(dk, kTcE4M3);
     std::map<const float*, int> uidx;
     std::vector<const float*> uin;
     std::vector<int> u_of(jobs.size()), xln_of;
@@ -463,52 +610,116 @@ struct Engine {
       u_of[j] = it->second;
       if (P.th_l == l && P.th_h == jobs[j].head) need_xln[it->second] = 1;
     }
-    xln_of.assign(uin.size(), -1);
+    const size_t nu = uin.size();
+    xln_of.assign(nu, -1);
     int n_xln = 0;
-    for (size_t u = 0; u < uin.size(); ++u)
+    for (size_t u = 0; u < nu; ++u)
       if (need_xln[u]) xln_of[u] = n_xln++;
-    float* xq = scratch("h_xq", uin.size() * SEG);
+    float* xq = tc ? nullptr : scratch("h_xq", nu * SEG);
+    uint8_t* xq8 = tc ? reinterpret_cast<uint8_t*>(scratch("h_xq8", nu * SEG / 4 + 1)) : nullptr;
     float* xln = scratch("h_xln", std::max(n_xln, 1) * SEG);
     std::vector<LnJob> lj;
-    for (size_t u = 0; u < uin.size(); ++u)
-      lj.push_back({uin[u], xln_of[u] >= 0 ? xln + xln_of[u] * SEG : nullptr, xq + u * SEG, RB, D});
+    for (size_t u = 0; u < nu; ++u)
+      lj.push_back({uin[u], xln_of[u] >= 0 ? xln + xln_of[u] * SEG : nullptr,
+                    xq ? xq + u * SEG : nullptr, RB, D, xq8 ? xq8 + u * SEG : nullptr, 1});
     ln(lj, g.mat(2, l), g.mat(3, l), p_low);
 
-    const size_t per = (size_t)RB * dk;
-    float* qkv = scratch("h_qkv", jobs.size() * 3 * per);
-    float* z = scratch("h_z", jobs.size() * per);
+    // Q/K/V: per unique input a [RB][3D] block (q | k | v, head-major columns)
+    const size_t QKV = (size_t)RB * 3 * D;
+    float* qkv = scratch("h_qkv", nu * QKV);
     std::vector<GemmJob> gj;
+    std::vector<TcJob> tj;
+    const PackedB* bq = tc ? &packedB(0, l, kTcE4M3, p_low, P.mode) : nullptr;
+    for (size_t u = 0; u < nu; ++u) {
+      std::vector<int> hs;  // non-target heads reading input u
+      for (size_t j = 0; j < jobs.size(); ++j)
+        if (u_of[j] == (int)u && !(P.th_l == l && P.th_h == jobs[j].head)) hs.push_back(jobs[j].head);
+      std::sort(hs.begin(), hs.end());
+      hs.erase(std::unique(hs.begin(), hs.end()), hs.end());
+      float* blk = qkv + u * QKV;
+      if (tc && (int)hs.size() == H) {
+        TcJob t{};
+        t.a_row0 = (int)u * RB, t.b_row0 = 0, t.b_k0 = 0, t.M = RB, t.N = 3 * D, t.K = D;
+        t.out_f32 = blk, t.ldo = 3 * D, t.b_norm = bq->norm.as<float>(), t.prec = p_low;
+        tj.push_back(t);
+        continue;
+      }
+      for (int h : hs)
+        for (int c = 0; c < 3; ++c) {
+          if (tc) {
+            TcJob t{};
+            t.a_row0 = (int)u * RB, t.b_row0 = c * D + h * dk, t.b_k0 = 0, t.M = RB, t.N = dk, t.K = D;
+            t.out_f32 = blk + c * D + h * dk, t.ldo = 3 * D;
+            t.b_norm = bq->norm.as<float>() + c * D + h * dk, t.prec = p_low;
+            tj.push_back(t);
+          } else {
+            GemmJob q{};
+            q.A = xq + u * SEG, q.B = W(g.mat(4 + c, l), p_low, P.mode) + h * dk;
+            q.C = blk + c * D + h * dk;
+            q.M = RB, q.N = dk, q.K = D, q.lda = D, q.ldb = D, q.ldc = 3 * D, q.prec = p_low;
+            gj.push_back(q);
+          }
+        }
+    }
+    for (size_t j = 0; j < jobs.size(); ++j) {  // the elevated head: FP32 (model.cpp:665-675)
+      const int h = jobs[j].head;
+      if (!(P.th_l == l && P.th_h == h)) continue;
+      for (int c = 0; c < 3; ++c) {
+        GemmJob q{};
+        q.A = xln + xln_of[u_of[j]] * SEG, q.B = master[g.mat(4 + c, l)]->as<float>() + h * dk;
+        q.C = qkv + u_of[j] * QKV + c * D + h * dk;
+        q.M = RB, q.N = dk, q.K = D, q.lda = D, q.ldb = D, q.ldc = 3 * D, q.prec = 2;
+        gj.push_back(q);
+      }
+    }
+    if (tc) gemm_tc(kTcE4M3, xq8, (int64_t)nu * RB, D, *bq, tj, "qkv");
+    gemm(gj, "gemm_qkv");
+
+    // attention + z (FP32 for the exact W_O, E4M3 bytes for the tensor cores)
+    const int wo_prec = P.wo_precision(l);
+    const bool tc_wo = tc && wo_prec == 0;
+    const size_t per = (size_t)RB * dk;
+    float* z = tc_wo ? nullptr : scratch("h_z", jobs.size() * per);
+    uint8_t* z8 = tc_wo ? reinterpret_cast<uint8_t*>(scratch("h_z8", jobs.size() * per / 4 + 1)) : nullptr;
     std::vector<AttnJob> aj;
     for (size_t j = 0; j < jobs.size(); ++j) {
       const int h = jobs[j].head;
       const bool target = P.th_l == l && P.th_h == h;
-      for (int c = 0; c < 3; ++c) {
-        const int m = g.mat(4 + c, l);
-        GemmJob q{};
-        q.A = target ? xln + xln_of[u_of[j]] * SEG : xq + u_of[j] * SEG;
-        q.B = (target ? master[m]->as<float>() : W(m, p_low, P.mode)) + h * dk;
-        q.C = qkv + (j * 3 + c) * per;
-        q.M = RB, q.N = dk, q.K = D, q.lda = D, q.ldb = D, q.ldc = dk;
-        q.prec = target ? 2 : p_low, q.epi = 0;
-        gj.push_back(q);
-      }
-      aj.push_back({qkv + (j * 3) * per, qkv + (j * 3 + 1) * per, qkv + (j * 3 + 2) * per,
-                    z + j * per, dk, target ? 2 : p_low});
+      float* blk = qkv + u_of[j] * QKV;
+      AttnJob a{};
+      a.q = blk + h * dk, a.k = blk + D + h * dk, a.v = blk + 2 * D + h * dk, a.ld = 3 * D;
+      a.prec = target ? 2 : p_low, a.ldz = dk;
+      a.z = z ? z + j * per : nullptr;
+      a.z8 = z8 ? z8 + j * per : nullptr;
+      aj.push_back(a);
     }
-    gemm(gj, "gemm_qkv");
     attn(aj, nb);
-    const float* wo = W(g.mat(7, l), P.wo_precision(l), P.mode);
     gj.clear();
-    for (size_t j = 0; j < jobs.size(); ++j) {
-      const int h = jobs[j].head;
-      const bool target = P.th_l == l && P.th_h == h;
-      GemmJob o{};
-      o.A = z + j * per, o.B = wo + (size_t)h * dk * D, o.C = jobs[j].out;
-      o.M = RB, o.N = D, o.K = dk, o.lda = dk, o.ldb = D, o.ldc = D;
-      o.prec = target ? 2 : p_low, o.epi = 0;
-      gj.push_back(o);
+    tj.clear();
+    if (tc_wo) {
+      const PackedB& bo = packedB(1, l, kTcE4M3, wo_prec, P.mode);
+      for (size_t j = 0; j < jobs.size(); ++j) {
+        const int h = jobs[j].head;
+        TcJob t{};
+        t.a_row0 = (int)j * RB, t.b_row0 = 0, t.b_k0 = h * dk, t.M = RB, t.N = D, t.K = dk;
+        t.out_f32 = jobs[j].out, t.ldo = D, t.b_norm = bo.norm.as<float>() + (size_t)h * D;
+        t.prec = p_low;
+        tj.push_back(t);
+      }
+      gemm_tc(kTcE4M3, z8, (int64_t)jobs.size() * RB, dk, bo, tj, "wo");
+    } else {
+      const float* wo = W(g.mat(7, l), wo_prec, P.mode);
+      for (size_t j = 0; j < jobs.size(); ++j) {
+        const int h = jobs[j].head;
+        const bool target = P.th_l == l && P.th_h == h;
+        GemmJob o{};
+        o.A = z + j * per, o.B = wo + (size_t)h * dk * D, o.C = jobs[j].out;
+        o.M = RB, o.N = D, o.K = dk, o.lda = dk, o.ldb = D, o.ldc = D;
+        o.prec = target ? 2 : p_low, o.epi = 0;
+        gj.push_back(o);
+      }
+      gemm(gj, "gemm_wo");
     }
-    gemm(gj, "gemm_wo");
   }
 
   // MLP (model.cpp:720-739)
@@ -518,6 +729,35 @@ struct Engine {
     const size_t SEG = segf(nb);
     const int node = g.stage_nodes[2 + 2 * l][0];
     const int p = P.precision_of(g, node);
+    const int elem = p == 1 ? kTcBF16 : kTcE4M3;
+    const bool tc = !opt_exact && (p == 1 || (p == 0 && P.mode == 0)) && tc_dims_ok(D, elem) &&
+                    tc_dims_ok(4 * D, elem);
+    if (tc) {
+      const int esz = elem == kTcBF16 ? 2 : 1;
+      uint8_t* xqp = reinterpret_cast<uint8_t*>(scratch("m_xqp", jobs.size() * SEG * esz / 4 + 1));
+      uint8_t* hidp = reinterpret_cast<uint8_t*>(scratch("m_hidp", jobs.size() * SEG * esz + 1));
+      std::vector<LnJob> lj;
+      for (size_t j = 0; j < jobs.size(); ++j)
+        lj.push_back({jobs[j].in, nullptr, nullptr, RB, D, xqp + j * SEG * esz, elem == kTcBF16 ? 2 : 1});
+      ln(lj, g.mat(8, l), g.mat(9, l), p);
+      const PackedB& bi = packedB(2, l, elem, p, P.mode);
+      const PackedB& bo = packedB(3, l, elem, p, P.mode);
+      std::vector<TcJob> t1, t2;
+      for (size_t j = 0; j < jobs.size(); ++j) {
+        TcJob a{};
+        a.a_row0 = (int)j * RB, a.M = RB, a.N = 4 * D, a.K = D;
+        a.out_pack = hidp + j * SEG * 4 * esz, a.ldo = 4 * D, a.b_norm = bi.norm.as<float>();
+        a.prec = p, a.epi = 1;
+        t1.push_back(a);
+        TcJob b{};
+        b.a_row0 = (int)j * RB, b.M = RB, b.N = D, b.K = 4 * D;
+        b.out_f32 = jobs[j].out, b.ldo = D, b.b_norm = bo.norm.as<float>(), b.prec = p;
+        t2.push_back(b);
+      }
+      gemm_tc(elem, xqp, (int64_t)jobs.size() * RB, D, bi, t1, "mlp_in");
+      gemm_tc(elem, hidp, (int64_t)jobs.size() * RB, 4 * D, bo, t2, "mlp_out");
+      return;
+    }
     float* xq = scratch("m_xq", jobs.size() * SEG);
     float* hid = scratch("m_hid", jobs.size() * SEG * 4);
     std::vector<LnJob> lj;
@@ -1050,7 +1290,7 @@ struct Engine {
     if (world > 1) {
       DeviceBuf& ar = *pool_buf("allreduce", sizeof(double) * std::max(n, 1));
       CK(cudaMemcpyAsync(ar.p, sums.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
-      NK(ncclAllReduce(ar.p, ar.p, (size_t)n, ncclDouble, ncclSum, comm, st));
+      NK(nccl().AllReduce(ar.p, ar.p, (size_t)n, ncclDouble, ncclSum, comm, st));
       CK(cudaMemcpyAsync(sums.data(), ar.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
     }
@@ -1271,7 +1511,7 @@ int cqg_set_dataset(cqg_ctx* ctx, const int32_t* clean, const int32_t* corrupt, 
 int cqg_get_unique_id(void* out128) {
   return guarded([&] {
     ncclUniqueId id;
-    NK(ncclGetUniqueId(&id));
+    NK(cqg::nccl().GetUniqueId(&id));
     std::memcpy(out128, &id, sizeof id);
   });
 }
@@ -1286,7 +1526,7 @@ int cqg_init_comm(cqg_ctx* ctx, const void* unique_id, int rank, int world) {
     ncclUniqueId id;
     std::memcpy(&id, unique_id, sizeof id);
     CK(cudaSetDevice(E.device));
-    NK(ncclCommInitRank(&E.comm, world, id, rank));
+    NK(cqg::nccl().CommInitRank(&E.comm, world, id, rank));
   });
 }
 

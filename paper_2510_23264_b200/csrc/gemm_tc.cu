@@ -1,0 +1,407 @@
+// gemm_tc.cu — tcgen05 / TMA / TMEM GEMM for sm_100a (see gemm_tc.h).
+//
+// One CTA computes one 128 x 128 output tile:
+//   warp 0      TMA producer  (cp.async.bulk.tensor.2d, SWIZZLE_128B, mbarrier tx)
+//   warp 1      MMA issuer    (tcgen05.mma.cta_group::1, kind::f8f6f4 | kind::f16,
+//                              FP32 accumulator in TMEM; TMEM alloc/dealloc)
+//   warps 2..5  epilogue      (tcgen05.ld 32x32b -> round -> certify -> store)
+// A 4-stage smem ring (32 KB/stage) keeps the tensor pipe fed.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "gemm_tc.h"
+#include "numerics.cuh"
+
+namespace cqg {
+
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kBKBytes = 128;  // one SW128 atom row
+constexpr int kAStage = kTcBM * kBKBytes;  // 16 KB
+constexpr int kBStage = kTcBN * kBKBytes;  // 16 KB
+constexpr int kThreads = 192;
+constexpr size_t kSmemBytes = 1024 + (size_t)kStages * (kAStage + kBStage) + 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// K-major SWIZZLE_128B smem matrix descriptor (cute::UMMA::SmemDescriptor):
+// start>>4 [0,14), LBO>>4 [16,30) (=1, unused for swizzled K-major),
+// SBO>>4 [32,46) (=1024 B: 8 rows x 128 B), version 1 [46,48), layout 2 [61,64).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor (cute::UMMA::InstrDescriptor): c_format F32 [4,6),
+// a/b format [7,10)/[10,13) (E4M3=0 for f8f6f4, BF16=1 for f16), K-major A/B,
+// N>>3 [17,23), M>>4 [24,29).
+template <int ELEM>
+__device__ __forceinline__ uint32_t instr_desc() {
+  uint32_t d = 0;
+  d |= 1u << 4;
+  const uint32_t f = ELEM == kTcBF16 ? 1u : 0u;
+  d |= f << 7;
+  d |= f << 10;
+  d |= (uint32_t)(kTcBN >> 3) << 17;
+  d |= (uint32_t)(kTcBM >> 4) << 24;
+  return d;
+}
+
+template <int ELEM>
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                    uint32_t accum) {
+  if (ELEM == kTcBF16) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accum));
+  } else {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accum));
+  }
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float round_out(float x, int prec) {
+  return prec == 2 ? x : round_p(x, prec);
+}
+
+__device__ __forceinline__ int find_job(const TcJob* jobs, int n, int t) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (jobs[mid].tile0 <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void store_out(const TcJob& jb, int row, int col, float v) {
+  const int64_t o = (int64_t)row * jb.ldo + col;
+  if (jb.out_f32) jb.out_f32[o] = v;
+  if (jb.out_pack) {
+    if (jb.prec == 1) reinterpret_cast<uint16_t*>(jb.out_pack)[o] = enc_bf16(v);
+    else reinterpret_cast<uint8_t*>(jb.out_pack)[o] = enc_e4m3(v);
+  }
+}
+
+template <int ELEM>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ TcLaunch L, const TcJob* __restrict__ jobs) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kAStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
+  uint64_t* empty = full + kStages;
+  uint64_t* tmem_full = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ji = find_job(jobs, L.n_jobs, blockIdx.x);
+  const TcJob jb = jobs[ji];
+  const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
+  const int local = blockIdx.x - jb.tile0;
+  const int mt = local / tiles_n, nt = local % tiles_n;
+  constexpr int esz = ELEM == kTcBF16 ? 2 : 1;
+  constexpr int bke = kBKBytes / esz;  // elements per stage along K
+  const int kbytes = jb.K * esz;
+  const int nk = (kbytes + kBKBytes - 1) / kBKBytes;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTcBN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int arow = jb.a_row0 + mt * kTcBM;
+      const int brow = jb.b_row0 + nt * kTcBN;
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages;
+        if (kb >= kStages) mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
+        mbar_expect_tx(&full[s], kAStage + kBStage);
+        tma_load_2d(sA + s * kAStage, &L.tmA, &full[s], kb * bke, arow);
+        tma_load_2d(sB + s * kBStage, &L.tmB, &full[s], jb.b_k0 + kb * bke, brow);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = instr_desc<ELEM>();
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages;
+        mbar_wait(&full[s], (kb / kStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int nmma = min(4, (kbytes - kb * kBKBytes) / 32);
+        const uint32_t a0 = smem_u32(sA + s * kAStage), b0 = smem_u32(sB + s * kBStage);
+        for (int k = 0; k < nmma; ++k)
+          mma<ELEM>(tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
+                    (kb | k) != 0 ? 1u : 0u);
+        mma_commit(&empty[s]);
+      }
+      mma_commit(tmem_full);
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes [32*(w%4), +32)
+    const int q = warp & 3;
+    const int row = mt * kTcBM + q * 32 + lane;
+    const bool rvalid = row < jb.M;
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const float sk = sqrtf((float)jb.K);
+    const float na = rvalid && L.a_norm ? L.a_norm[jb.a_row0 + row] : 0.f;
+    const float ku = L.kappa * 5.9604644775390625e-08f * sk;
+    for (int c0 = 0; c0 < kTcBN; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
+      if (!rvalid) continue;
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        const int col = nt * kTcBN + c0 + j;
+        if (col >= jb.N) break;
+        const float acc = __uint_as_float(r[j]);
+        float v = round_out(acc, jb.prec);
+        bool amb = false;
+        if (jb.prec != 2) {
+          const float nb = jb.b_norm ? jb.b_norm[col] : 0.f;
+          const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
+          amb = !(round_out(acc - m, jb.prec) == round_out(acc + m, jb.prec)) || !(acc == acc);
+        }
+        if (jb.epi == 1) v = round_out(gelu_ref(v), jb.prec);
+        store_out(jb, row, col, v);
+        if (amb) {
+          const uint32_t i = atomicAdd(L.fix_count, 1u);
+          if (i < L.fix_cap) {
+            L.fix[3 * i] = (uint32_t)ji;
+            L.fix[3 * i + 1] = (uint32_t)row;
+            L.fix[3 * i + 2] = (uint32_t)col;
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcBN));
+  }
+}
+
+// Exact sequential recomputation of flagged elements (dot_col order).
+template <int ELEM>
+__global__ void gemm_fixup_kernel(const TcLaunch L, const TcJob* __restrict__ jobs) {
+  const uint32_t n = min(*L.fix_count, L.fix_cap);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const TcJob jb = jobs[L.fix[3 * i]];
+    const int row = (int)L.fix[3 * i + 1], col = (int)L.fix[3 * i + 2];
+    const uint8_t* a = L.A + (int64_t)(jb.a_row0 + row) * L.lda;
+    const uint8_t* b = L.B + (int64_t)(jb.b_row0 + col) * L.ldb + (int64_t)jb.b_k0 * (ELEM == kTcBF16 ? 2 : 1);
+    float acc = 0.f;
+    for (int k = 0; k < jb.K; ++k) {
+      float x, y;
+      if (ELEM == kTcBF16) {
+        x = dec_bf16(reinterpret_cast<const uint16_t*>(a)[k]);
+        y = dec_bf16(reinterpret_cast<const uint16_t*>(b)[k]);
+      } else {
+        x = dec_e4m3(a[k]);
+        y = dec_e4m3(b[k]);
+      }
+      acc = __fadd_rn(acc, __fmul_rn(x, y));
+    }
+    float v = round_out(acc, jb.prec);
+    if (jb.epi == 1) v = round_out(gelu_ref(v), jb.prec);
+    store_out(jb, row, col, v);
+  }
+}
+
+__global__ void rownorm_kernel(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K,
+                               float* out) {
+  const int warps = blockDim.x >> 5;
+  const int r = blockIdx.x * warps + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  float s = 0.f;
+  const uint8_t* p = A + (int64_t)r * lda;
+  for (int k = lane; k < K; k += 32) {
+    const float x = elem == kTcBF16 ? dec_bf16(reinterpret_cast<const uint16_t*>(p)[k0 + k])
+                                    : dec_e4m3(p[k0 + k]);
+    s = fmaf(x, x, s);
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[r] = sqrtf(s) * 1.0001f;  // tiny guard for the FP32 sum itself
+}
+
+__global__ void pack_t_kernel(const float* __restrict__ in, int K, int N, int ld_in, void* out,
+                              int64_t ld_out, int elem) {
+  __shared__ float t[32][33];
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int k = k0 + i, n = n0 + threadIdx.x;
+    t[i][threadIdx.x] = (k < K && n < N) ? in[(int64_t)k * ld_in + n] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int n = n0 + i, k = k0 + threadIdx.x;
+    if (n < N && k < K) {
+      const float v = t[threadIdx.x][i];
+      if (elem == kTcBF16) reinterpret_cast<uint16_t*>(out)[(int64_t)n * ld_out + k] = enc_bf16(v);
+      else reinterpret_cast<uint8_t*>(out)[(int64_t)n * ld_out + k] = enc_e4m3(v);
+    }
+  }
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                             CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+bool tc_make_map(CUtensorMap* map, const void* base, int elem, uint64_t rows, uint64_t cols_elems,
+                 uint64_t pitch_bytes, uint32_t box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  const int esz = elem == kTcBF16 ? 2 : 1;
+  cuuint64_t dims[2] = {cols_elems, rows};
+  cuuint64_t strides[1] = {pitch_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)(kBKBytes / esz), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, elem == kTcBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8,
+                  2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
+  if (L.total_tiles <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tc_kernel<kTcE4M3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemBytes);
+    cudaFuncSetAttribute(gemm_tc_kernel<kTcBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemBytes);
+    attr = true;
+  }
+  if (L.elem == kTcBF16)
+    gemm_tc_kernel<kTcBF16><<<L.total_tiles, kThreads, kSmemBytes, st>>>(L, d_jobs);
+  else
+    gemm_tc_kernel<kTcE4M3><<<L.total_tiles, kThreads, kSmemBytes, st>>>(L, d_jobs);
+}
+
+void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, uint32_t n_fix_max, cudaStream_t st) {
+  const int blocks = (int)std::min<uint32_t>(1024, (n_fix_max + 127) / 128 + 1);
+  if (L.elem == kTcBF16) gemm_fixup_kernel<kTcBF16><<<blocks, 128, 0, st>>>(L, d_jobs);
+  else gemm_fixup_kernel<kTcE4M3><<<blocks, 128, 0, st>>>(L, d_jobs);
+}
+
+__global__ void fix_account_kernel(uint32_t* cnt) {
+  // cnt[0]: this launch's flagged count; cnt[1]: running total; cnt[2]: max per launch
+  cnt[1] += cnt[0];
+  cnt[2] = max(cnt[2], cnt[0]);
+  cnt[0] = 0;
+}
+
+void launch_fix_account(uint32_t* cnt, cudaStream_t st) { fix_account_kernel<<<1, 1, 0, st>>>(cnt); }
+
+void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,
+                    cudaStream_t st) {
+  if (rows <= 0) return;
+  rownorm_kernel<<<(rows + 7) / 8, 256, 0, st>>>(A, lda, elem, rows, k0, K, out);
+}
+
+void launch_pack_t(const float* in, int K, int N, int ld_in, void* out, int64_t ld_out, int elem,
+                   cudaStream_t st) {
+  dim3 grid((N + 31) / 32, (K + 31) / 32), block(32, 8);
+  pack_t_kernel<<<grid, block, 0, st>>>(in, K, N, ld_in, out, ld_out, elem);
+}
+
+}  // namespace cqg

@@ -1,0 +1,72 @@
+// gemm_tc.h — tcgen05 tensor-core GEMMs for the low-precision projections
+// (E4M3 head Q/K/V and W_O, BF16 MLP) with an exactness-certified epilogue.
+//
+// C[m][n] = round_prec( sum_k A[m][k] * B[n][k] )      (A, B K-major)
+//
+// The reference accumulates each dot product sequentially in FP32
+// (kernels.cpp:44-52) and then rounds to E4M3/BF16. Products of two E4M3 or
+// two BF16 values are exact in FP32, so the tensor-core sum r_tc and the
+// reference's sequential sum r_ref differ only by accumulation rounding. The
+// epilogue rounds r_tc and flags every element whose rounding is not
+// certified: round(r_tc - m) != round(r_tc + m) for the error margin
+//   m = kappa * 2^-24 * sqrt(K) * max(|r_tc|, ||a_m|| ||b_n|| / sqrt(K)),
+// (a ~kappa-sigma bound on |r_tc - r_ref| for FP32 accumulation of K terms).
+// Flagged elements are recomputed by the exact sequential kernel
+// (fixup), so the stored result equals the reference's bit for bit.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cqg {
+
+enum TcElem : int { kTcE4M3 = 0, kTcBF16 = 1 };
+
+struct TcJob {
+  int a_row0;        // first A row (global row index in the A tensor)
+  int b_row0;        // first B row (= output column 0) in the B tensor
+  int b_k0;          // K offset inside B rows (W_O head slices)
+  int M, N, K;       // K in elements, multiple of 32 bytes
+  float* out_f32;    // [M][ldo] FP32 values (may be null)
+  void* out_pack;    // [M][ldo] packed E4M3/BF16 of the output (may be null)
+  int ldo;
+  int tile0;         // first tile index of this job
+  const float* b_norm;  // [N] ||B row n|| over [b_k0, b_k0+K)
+  int prec;          // output rounding: 0 E4M3, 1 BF16, 2 none
+  int epi;           // 1: round -> gelu -> round (MLP in, kernels.cpp:226)
+};
+
+struct TcLaunch {
+  CUtensorMap tmA, tmB;
+  const uint8_t* A;  // global base of A, row pitch lda bytes
+  const uint8_t* B;
+  int64_t lda, ldb;  // bytes
+  const float* a_norm;  // [rows of A] ||A row||
+  int elem;          // TcElem
+  int n_jobs, total_tiles;
+  uint32_t* fix;     // fix list: (job, row, col) triplets
+  uint32_t* fix_count;
+  uint32_t fix_cap;
+  float kappa;
+};
+
+// Builds 2D K-major tensor maps (SW128, box = 128 B x box_rows) for A/B.
+bool tc_make_map(CUtensorMap* map, const void* base, int elem, uint64_t rows, uint64_t cols_elems,
+                 uint64_t pitch_bytes, uint32_t box_rows);
+
+void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
+void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, uint32_t n_fix_max,
+                       cudaStream_t st);
+// cnt[1] += cnt[0]; cnt[2] = max(cnt[2], cnt[0]); cnt[0] = 0
+void launch_fix_account(uint32_t* cnt, cudaStream_t st);
+// ||row|| of a packed [rows][K] operand (elements starting at col k0)
+void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,
+                    cudaStream_t st);
+// transpose + pack: out[n][k] = enc(in[k][n]) for a row-major K x N FP32 image
+void launch_pack_t(const float* in, int K, int N, int ld_in, void* out, int64_t ld_out, int elem,
+                   cudaStream_t st);
+
+constexpr int kTcBM = 128;
+constexpr int kTcBN = 128;
+
+}  // namespace cqg

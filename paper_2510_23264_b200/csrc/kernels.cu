@@ -123,7 +123,12 @@ __global__ void __launch_bounds__(kLnRows) ln_kernel(const LnJob* __restrict__ j
     const float y = __fadd_rn(__fmul_rn(gamma[col], __fmul_rn(__fsub_rn(x, s_mean[rr]), s_inv[rr])),
                               beta[col]);
     if (j.xln) j.xln[row * D + col] = y;
-    if (j.xq) j.xq[row * D + col] = round_p(y, prec);
+    const float q = round_p(y, prec);
+    if (j.xq) j.xq[row * D + col] = q;
+    if (j.xqp) {
+      if (j.pack == 2) reinterpret_cast<uint16_t*>(j.xqp)[row * D + col] = enc_bf16(q);
+      else reinterpret_cast<uint8_t*>(j.xqp)[row * D + col] = enc_e4m3(q);
+    }
   }
 }
 
@@ -259,7 +264,9 @@ __global__ void attention_kernel(const AttnJob* __restrict__ jobs, int S, int dk
     for (int t = 0; t < dk; ++t) {
       float acc = 0.f;
       for (int jj = 0; jj <= i; ++jj) acc = __fadd_rn(acc, __fmul_rn(p[jj], v[jj * ldk + t]));
-      jb.z[(base + i) * jb.ld + t] = round_p(acc, jb.prec);
+      const float zr = round_p(acc, jb.prec);
+      if (jb.z) jb.z[(base + i) * jb.ldz + t] = zr;
+      if (jb.z8) jb.z8[(base + i) * jb.ldz + t] = enc_e4m3(zr);
     }
   }
 }

@@ -34,6 +34,8 @@ struct LnJob {
   float* xq;        // [rows][D] rounded at prec (may be null)
   int rows;
   int in_stride;
+  void* xqp;        // packed copy of xq for the tensor cores (may be null)
+  int pack;         // 1: E4M3 bytes, 2: BF16
 };
 void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float* gamma,
                       const float* beta, int D, int prec, cudaStream_t st);
@@ -58,8 +60,10 @@ struct AttnJob {
   const float* k;
   const float* v;
   float* z;
-  int ld;    // row stride of q/k/v/z (elements)
+  int ld;    // row stride of q/k/v (elements)
   int prec;  // rounding of z (model.cpp:688-689)
+  int ldz;   // row stride of z / z8
+  uint8_t* z8;  // packed E4M3 copy of z for the tensor-core W_O (may be null)
 };
 void launch_attention(const AttnJob* d_jobs, int n_jobs, int B, int S, int dk, cudaStream_t st);
 
