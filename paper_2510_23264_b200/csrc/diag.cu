@@ -42,7 +42,7 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
   TcJob* dj;
   int* dts;
   GemmJob* dg;
-  size_t fcap = 1u << 20;
+  size_t fcap = 1u << 16;
   cudaMalloc(&dA, (size_t)M * K * 4);
   cudaMalloc(&dBt, (size_t)N * K * 4);
   cudaMalloc(&dB, (size_t)N * K * 4);
@@ -52,7 +52,11 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
   cudaMalloc(&bn, (size_t)N * 4);
   cudaMalloc(&pA, (size_t)M * K * esz);
   cudaMalloc(&pB, (size_t)N * K * esz);
-  cudaMalloc(&fix, fcap * 12);
+  uint32_t *tmask, *tflag;
+  cudaMalloc(&fix, fcap * 4);
+  cudaMalloc(&tmask, fcap * kTcBM * (kTcBN / 32) * 4);
+  cudaMalloc(&tflag, fcap * 4);
+  cudaMemset(tflag, 0, fcap * 4);
   cudaMalloc(&cnt, 16);
   cudaMalloc(&dj, sizeof(TcJob));
   cudaMalloc(&dts, sizeof(int));
@@ -89,6 +93,10 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
   if (!rc) {
     L.A = pA, L.B = pB, L.lda = (int64_t)K * esz, L.ldb = (int64_t)K * esz, L.elem = elem;
     L.kappa = 8.0f;
+    uint16_t* lut;
+    cudaMalloc(&lut, 65536 * 2);
+    launch_gelu_lut(lut, 0);
+    L.gelu_lut = lut;
     launch_rownorm(pA, L.lda, elem, M, 0, K, an, 0);
     L.a_norm = an;
     TcJob j{};
@@ -97,8 +105,9 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
     L.n_jobs = 1;
     L.total_tiles = ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
     L.fix = fix, L.fix_count = cnt, L.fix_cap = (uint32_t)fcap;
+    L.tile_mask = tmask, L.tile_flag = tflag;
     launch_gemm_tc(L, dj, 0);
-    launch_gemm_fixup(L, dj, (uint32_t)fcap, 0);
+    launch_gemm_fixup(L, dj, 0);
     // exact reference product on the decoded grid values
     GemmJob gj{};
     gj.A = dA, gj.B = dB, gj.C = dC2, gj.M = M, gj.N = N, gj.K = K, gj.lda = K, gj.ldb = N,

@@ -487,8 +487,7 @@ struct Engine {
     int rows = 0, cols = 0, elem = 0;
   };
   std::map<std::tuple<int, int, int>, std::unique_ptr<PackedB>> packed;
-  DeviceBuf fix_list, fix_cnt;
-  static constexpr uint32_t kFixCap = 1u << 22;
+  DeviceBuf fix_list, fix_cnt, gelu_lut, tile_mask, tile_flag;
 
   // which: 0 QKV [3D x D], 1 W_O [D x D] (per-head K slices), 2 W_in^T [4D x D],
   // 3 W_out^T [D x 4D]
@@ -546,6 +545,12 @@ struct Engine {
     L.ldb = (int64_t)B.cols * esz;
     L.elem = elem;
     L.kappa = 8.0f;
+    if (!gelu_lut.p) {
+      gelu_lut.ensure(65536 * 2);
+      launch_gelu_lut(gelu_lut.as<uint16_t>(), st);
+      launched();
+    }
+    L.gelu_lut = gelu_lut.as<uint16_t>();
     float* an = scratch("tc_anorm", (size_t)a_rows);
     {
       Prof pf(this, "rownorm", 0, (double)a_rows * a_k * esz);
@@ -562,14 +567,19 @@ struct Engine {
     }
     L.n_jobs = (int)jobs.size();
     L.total_tiles = total;
-    if (!fix_list.p) {
-      fix_list.ensure((size_t)kFixCap * 12);
+    if (!fix_cnt.p) {
       fix_cnt.ensure(16);
       CK(cudaMemsetAsync(fix_cnt.p, 0, 16, st));
     }
+    fix_list.ensure((size_t)total * 4);
+    tile_mask.ensure((size_t)total * kTcBM * (kTcBN / 32) * 4);
+    tile_flag.ensure((size_t)total * 4);
+    CK(cudaMemsetAsync(tile_flag.p, 0, (size_t)total * 4, st));
     L.fix = fix_list.as<uint32_t>();
     L.fix_count = fix_cnt.as<uint32_t>();
-    L.fix_cap = kFixCap;
+    L.fix_cap = (uint32_t)total;
+    L.tile_mask = tile_mask.as<uint32_t>();
+    L.tile_flag = tile_flag.as<uint32_t>();
     reserve(up_bytes(jobs.size(), sizeof(TcJob)));
     const TcJob* dj = upload(jobs);
     {
@@ -580,7 +590,7 @@ struct Engine {
     }
     {
       Prof pf(this, "gemm_fixup");
-      launch_gemm_fixup(L, dj, kFixCap, st);
+      launch_gemm_fixup(L, dj, st);
     }
     launch_fix_account(L.fix_count, st);
     launched();

@@ -226,32 +226,54 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sk = sqrtf((float)jb.K);
     const float na = rvalid && L.a_norm ? L.a_norm[jb.a_row0 + row] : 0.f;
     const float ku = L.kappa * 5.9604644775390625e-08f * sk;
+    uint32_t flagged[kTcBN / 32];
     for (int c0 = 0; c0 < kTcBN; c0 += 32) {
       uint32_t r[32];
       tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
-      if (!rvalid) continue;
-#pragma unroll 4
-      for (int j = 0; j < 32; ++j) {
-        const int col = nt * kTcBN + c0 + j;
-        if (col >= jb.N) break;
-        const float acc = __uint_as_float(r[j]);
-        float v = round_out(acc, jb.prec);
-        bool amb = false;
-        if (jb.prec != 2) {
-          const float nb = jb.b_norm ? jb.b_norm[col] : 0.f;
-          const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
-          amb = !(round_out(acc - m, jb.prec) == round_out(acc + m, jb.prec)) || !(acc == acc);
-        }
-        if (jb.epi == 1) v = round_out(gelu_ref(v), jb.prec);
-        store_out(jb, row, col, v);
-        if (amb) {
-          const uint32_t i = atomicAdd(L.fix_count, 1u);
-          if (i < L.fix_cap) {
-            L.fix[3 * i] = (uint32_t)ji;
-            L.fix[3 * i + 1] = (uint32_t)row;
-            L.fix[3 * i + 2] = (uint32_t)col;
+      uint32_t fl = 0;
+      if (rvalid) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = nt * kTcBN + c0 + j;
+          if (col < jb.N) {
+            const float acc = __uint_as_float(r[j]);
+            float v = round_out(acc, jb.prec);
+            bool amb = !(acc == acc);
+            if (jb.prec != 2) {
+              const float nb = jb.b_norm ? jb.b_norm[col] : 0.f;
+              // E4M3 x E4M3 products are multiples of 2^-18; if every partial
+              // sum is below 2^6 (|s_k| <= ||a|| ||b||) all of them are exact
+              // in FP32, so the reference's sequential sum is the exact sum
+              // and so is the tensor-core sum: the rounding is certified.
+              const bool exact = ELEM == kTcE4M3 && na * nb < 63.99f;
+              if (!exact) {
+                const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
+                amb = amb || !(round_out(acc - m, jb.prec) == round_out(acc + m, jb.prec));
+              }
+            }
+            if (jb.epi == 1) {
+              if (jb.prec == 1 && L.gelu_lut) v = dec_bf16(L.gelu_lut[enc_bf16(v)]);
+              else v = round_out(gelu_ref(v), jb.prec);
+            }
+            store_out(jb, row, col, v);
+            if (amb) fl |= 1u << j;
           }
         }
+      }
+      flagged[c0 / 32] = fl;
+    }
+    {  // per-tile row masks (always written) + compact list of flagged tiles
+      uint32_t any = 0;
+      uint32_t* tm = L.tile_mask + ((size_t)blockIdx.x * kTcBM + q * 32 + lane) * (kTcBN / 32);
+      for (int w = 0; w < kTcBN / 32; ++w) {
+        const uint32_t f = rvalid ? flagged[w] : 0u;
+        tm[w] = f;
+        any |= f;
+      }
+      any = __any_sync(0xffffffffu, any != 0);
+      if (any && lane == 0 && atomicOr(&L.tile_flag[blockIdx.x], 1u) == 0u) {
+        const uint32_t i = atomicAdd(L.fix_count, 1u);
+        if (i < L.fix_cap) L.fix[i] = blockIdx.x;
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -263,31 +285,104 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Exact sequential recomputation of flagged elements (dot_col order).
+// Exact sequential recomputation of flagged elements (dot_col order,
+// kernels.cpp:44-52): one warp per (row, tile) record, the A row staged once
+// in shared memory, each lane walking one flagged column's B row.
+// One CTA per flagged tile, one thread per tile row: A and B K-chunks are
+// staged (decoded) in shared memory and each thread walks up to kFixGroup of
+// its flagged columns per pass with the reference's sequential FP32 chain.
+constexpr int kFixChunk = 32, kFixGroup = 8;
+
 template <int ELEM>
-__global__ void gemm_fixup_kernel(const TcLaunch L, const TcJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(kTcBM) gemm_fixup_kernel(const TcLaunch L,
+                                                            const TcJob* __restrict__ jobs) {
+  __shared__ float As[kTcBM][kFixChunk + 1];
+  __shared__ float Bs[kTcBN][kFixChunk + 1];
+  __shared__ int s_groups;
   const uint32_t n = min(*L.fix_count, L.fix_cap);
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const TcJob jb = jobs[L.fix[3 * i]];
-    const int row = (int)L.fix[3 * i + 1], col = (int)L.fix[3 * i + 2];
-    const uint8_t* a = L.A + (int64_t)(jb.a_row0 + row) * L.lda;
-    const uint8_t* b = L.B + (int64_t)(jb.b_row0 + col) * L.ldb + (int64_t)jb.b_k0 * (ELEM == kTcBF16 ? 2 : 1);
-    float acc = 0.f;
-    for (int k = 0; k < jb.K; ++k) {
-      float x, y;
-      if (ELEM == kTcBF16) {
-        x = dec_bf16(reinterpret_cast<const uint16_t*>(a)[k]);
-        y = dec_bf16(reinterpret_cast<const uint16_t*>(b)[k]);
-      } else {
-        x = dec_e4m3(a[k]);
-        y = dec_e4m3(b[k]);
-      }
-      acc = __fadd_rn(acc, __fmul_rn(x, y));
+  const int t = threadIdx.x;
+  for (uint32_t fi = blockIdx.x; fi < n; fi += gridDim.x) {
+    const int tile = (int)L.fix[fi];
+    const int ji = find_job(jobs, L.n_jobs, tile);
+    const TcJob jb = jobs[ji];
+    const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
+    const int mt = (tile - jb.tile0) / tiles_n, nt = (tile - jb.tile0) % tiles_n;
+    uint32_t mask[kTcBN / 32];
+    int nf = 0;
+    for (int w = 0; w < kTcBN / 32; ++w) {
+      mask[w] = L.tile_mask[((size_t)tile * kTcBM + t) * (kTcBN / 32) + w];
+      nf += __popc(mask[w]);
     }
-    float v = round_out(acc, jb.prec);
-    if (jb.epi == 1) v = round_out(gelu_ref(v), jb.prec);
-    store_out(jb, row, col, v);
+    if (t == 0) s_groups = 0;
+    __syncthreads();
+    atomicMax(&s_groups, (nf + kFixGroup - 1) / kFixGroup);
+    __syncthreads();
+    const int groups = s_groups;
+    const int row = mt * kTcBM + t;
+    for (int gi = 0; gi < groups; ++gi) {
+      int cols[kFixGroup];
+      int nc = 0;
+      {  // the gi-th group of this thread's flagged columns
+        int seen = 0;
+        for (int w = 0; w < kTcBN / 32; ++w) {
+          uint32_t m = mask[w];
+          while (m) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1;
+            if (seen >= gi * kFixGroup && nc < kFixGroup) cols[nc++] = w * 32 + bit;
+            ++seen;
+          }
+        }
+      }
+      float acc[kFixGroup];
+#pragma unroll
+      for (int j = 0; j < kFixGroup; ++j) acc[j] = 0.f;
+      for (int k0 = 0; k0 < jb.K; k0 += kFixChunk) {
+        __syncthreads();
+        for (int idx = t; idx < kTcBM * kFixChunk; idx += kTcBM) {
+          const int rr = idx / kFixChunk, kk = idx % kFixChunk, k = k0 + kk;
+          const int ar = mt * kTcBM + rr, bc = nt * kTcBN + rr;
+          float av = 0.f, bv = 0.f;
+          if (k < jb.K) {
+            if (ar < jb.M) {
+              const uint8_t* a = L.A + (int64_t)(jb.a_row0 + ar) * L.lda;
+              av = ELEM == kTcBF16 ? dec_bf16(reinterpret_cast<const uint16_t*>(a)[k]) : dec_e4m3(a[k]);
+            }
+            if (bc < jb.N) {
+              const uint8_t* b = L.B + (int64_t)(jb.b_row0 + bc) * L.ldb;
+              const int kb = jb.b_k0 + k;
+              bv = ELEM == kTcBF16 ? dec_bf16(reinterpret_cast<const uint16_t*>(b)[kb]) : dec_e4m3(b[kb]);
+            }
+          }
+          As[rr][kk] = av;
+          Bs[rr][kk] = bv;
+        }
+        __syncthreads();
+        const int kl = min(kFixChunk, jb.K - k0);
+        for (int kk = 0; kk < kl; ++kk) {
+          const float a = As[t][kk];
+#pragma unroll
+          for (int j = 0; j < kFixGroup; ++j)
+            if (j < nc) acc[j] = __fadd_rn(acc[j], __fmul_rn(a, Bs[cols[j]][kk]));
+        }
+      }
+      for (int j = 0; j < nc; ++j) {
+        const int col = nt * kTcBN + cols[j];
+        float v = round_out(acc[j], jb.prec);
+        if (jb.epi == 1) {
+          if (jb.prec == 1 && L.gelu_lut) v = dec_bf16(L.gelu_lut[enc_bf16(v)]);
+          else v = round_out(gelu_ref(v), jb.prec);
+        }
+        store_out(jb, row, col, v);
+      }
+    }
+    __syncthreads();
   }
+}
+
+__global__ void gelu_lut_kernel(uint16_t* lut) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 65536u) lut[i] = enc_bf16(round_bf16(gelu_ref(dec_bf16((uint16_t)i))));
 }
 
 __global__ void rownorm_kernel(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K,
@@ -377,11 +472,14 @@ void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
     gemm_tc_kernel<kTcE4M3><<<L.total_tiles, kThreads, kSmemBytes, st>>>(L, d_jobs);
 }
 
-void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, uint32_t n_fix_max, cudaStream_t st) {
-  const int blocks = (int)std::min<uint32_t>(1024, (n_fix_max + 127) / 128 + 1);
-  if (L.elem == kTcBF16) gemm_fixup_kernel<kTcBF16><<<blocks, 128, 0, st>>>(L, d_jobs);
-  else gemm_fixup_kernel<kTcE4M3><<<blocks, 128, 0, st>>>(L, d_jobs);
+void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
+  const int blocks = std::min(L.total_tiles, 148 * 8);
+  if (blocks <= 0) return;
+  if (L.elem == kTcBF16) gemm_fixup_kernel<kTcBF16><<<blocks, kTcBM, 0, st>>>(L, d_jobs);
+  else gemm_fixup_kernel<kTcE4M3><<<blocks, kTcBM, 0, st>>>(L, d_jobs);
 }
+
+void launch_gelu_lut(uint16_t* lut, cudaStream_t st) { gelu_lut_kernel<<<256, 256, 0, st>>>(lut); }
 
 __global__ void fix_account_kernel(uint32_t* cnt) {
   // cnt[0]: this launch's flagged count; cnt[1]: running total; cnt[2]: max per launch

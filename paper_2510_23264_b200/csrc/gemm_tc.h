@@ -44,10 +44,13 @@ struct TcLaunch {
   const float* a_norm;  // [rows of A] ||A row||
   int elem;          // TcElem
   int n_jobs, total_tiles;
-  uint32_t* fix;     // fix list: (job, row, col) triplets
-  uint32_t* fix_count;
-  uint32_t fix_cap;
+  uint32_t* fix;        // compact list of tiles holding flagged elements
+  uint32_t* fix_count;  // entries in fix (per launch)
+  uint32_t fix_cap;     // >= total_tiles
+  uint32_t* tile_mask;  // [total_tiles][kTcBM][kTcBN/32] flagged-column bits per row
+  uint32_t* tile_flag;  // [total_tiles], zeroed before the launch
   float kappa;
+  const uint16_t* gelu_lut;  // bf16 -> round_bf16(gelu(x)) for all 2^16 inputs
 };
 
 // Builds 2D K-major tensor maps (SW128, box = 128 B x box_rows) for A/B.
@@ -55,8 +58,9 @@ bool tc_make_map(CUtensorMap* map, const void* base, int elem, uint64_t rows, ui
                  uint64_t pitch_bytes, uint32_t box_rows);
 
 void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
-void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, uint32_t n_fix_max,
-                       cudaStream_t st);
+void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
+// lut[b] = enc_bf16(round_bf16(gelu_ref(dec_bf16(b)))) (glibc-exact erff)
+void launch_gelu_lut(uint16_t* lut, cudaStream_t st);
 // cnt[1] += cnt[0]; cnt[2] = max(cnt[2], cnt[0]); cnt[0] = 0
 void launch_fix_account(uint32_t* cnt, cudaStream_t st);
 // ||row|| of a packed [rows][K] operand (elements starting at col k0)
@@ -68,5 +72,6 @@ void launch_pack_t(const float* in, int K, int N, int ld_in, void* out, int64_t 
 
 constexpr int kTcBM = 128;
 constexpr int kTcBN = 128;
+constexpr int kFixRec = 3 + kTcBN / 32;
 
 }  // namespace cqg
