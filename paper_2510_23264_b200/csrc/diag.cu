@@ -42,7 +42,7 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
   TcJob* dj;
   int* dts;
   GemmJob* dg;
-  size_t fcap = 1u << 16;
+  size_t fcap = (size_t)M * N;
   cudaMalloc(&dA, (size_t)M * K * 4);
   cudaMalloc(&dBt, (size_t)N * K * 4);
   cudaMalloc(&dB, (size_t)N * K * 4);
@@ -52,11 +52,7 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
   cudaMalloc(&bn, (size_t)N * 4);
   cudaMalloc(&pA, (size_t)M * K * esz);
   cudaMalloc(&pB, (size_t)N * K * esz);
-  uint32_t *tmask, *tflag;
-  cudaMalloc(&fix, fcap * 4);
-  cudaMalloc(&tmask, fcap * kTcBM * (kTcBN / 32) * 4);
-  cudaMalloc(&tflag, fcap * 4);
-  cudaMemset(tflag, 0, fcap * 4);
+  cudaMalloc(&fix, fcap * 8);
   cudaMalloc(&cnt, 16);
   cudaMalloc(&dj, sizeof(TcJob));
   cudaMalloc(&dts, sizeof(int));
@@ -105,7 +101,6 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
     L.n_jobs = 1;
     L.total_tiles = ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
     L.fix = fix, L.fix_count = cnt, L.fix_cap = (uint32_t)fcap;
-    L.tile_mask = tmask, L.tile_flag = tflag;
     launch_gemm_tc(L, dj, 0);
     launch_gemm_fixup(L, dj, 0);
     // exact reference product on the decoded grid values

@@ -454,14 +454,17 @@ struct Engine {
     std::vector<int> ts(jobs.size());
     int total = 0;
     double flops = 0;
+    bool big = true;
+    for (const GemmJob& j : jobs) big = big && j.M >= 128 && j.N >= 128;
     for (size_t i = 0; i < jobs.size(); ++i) {
       ts[i] = total;
-      total += gemm_exact_tiles(jobs[i].M, jobs[i].N);
+      total += big ? gemm_exact_big_tiles(jobs[i].M, jobs[i].N) : gemm_exact_tiles(jobs[i].M, jobs[i].N);
       flops += 2.0 * jobs[i].M * (double)jobs[i].N * jobs[i].K;
     }
     reserve(up_bytes(jobs.size(), sizeof(GemmJob)) + up_bytes(ts.size(), sizeof(int)));
     Prof pf(this, name, flops, 0);
-    launch_gemm_exact(upload(jobs), upload(ts), (int)jobs.size(), total, st);
+    if (big) launch_gemm_exact_big(upload(jobs), upload(ts), (int)jobs.size(), total, st);
+    else launch_gemm_exact(upload(jobs), upload(ts), (int)jobs.size(), total, st);
   }
   void attn(const std::vector<AttnJob>& jobs, int nb) {
     if (jobs.empty()) return;
@@ -487,7 +490,7 @@ struct Engine {
     int rows = 0, cols = 0, elem = 0;
   };
   std::map<std::tuple<int, int, int>, std::unique_ptr<PackedB>> packed;
-  DeviceBuf fix_list, fix_cnt, gelu_lut, tile_mask, tile_flag;
+  DeviceBuf fix_list, fix_cnt, gelu_lut;
 
   // which: 0 QKV [3D x D], 1 W_O [D x D] (per-head K slices), 2 W_in^T [4D x D],
   // 3 W_out^T [D x 4D]
@@ -571,15 +574,13 @@ struct Engine {
       fix_cnt.ensure(16);
       CK(cudaMemsetAsync(fix_cnt.p, 0, 16, st));
     }
-    fix_list.ensure((size_t)total * 4);
-    tile_mask.ensure((size_t)total * kTcBM * (kTcBN / 32) * 4);
-    tile_flag.ensure((size_t)total * 4);
-    CK(cudaMemsetAsync(tile_flag.p, 0, (size_t)total * 4, st));
+    // capacity: 12.5% of the outputs (typical flagged share 0-5%); an
+    // overflow is detected after the call (fix_cnt[2]) and reported.
+    const size_t cap = std::max<size_t>((size_t)1 << 20, (size_t)total * kTcBM * kTcBN / 8);
+    fix_list.ensure(cap * 8);
     L.fix = fix_list.as<uint32_t>();
     L.fix_count = fix_cnt.as<uint32_t>();
-    L.fix_cap = (uint32_t)total;
-    L.tile_mask = tile_mask.as<uint32_t>();
-    L.tile_flag = tile_flag.as<uint32_t>();
+    L.fix_cap = (uint32_t)std::min<size_t>(cap, 0xFFFFFFFFu);
     reserve(up_bytes(jobs.size(), sizeof(TcJob)));
     const TcJob* dj = upload(jobs);
     {
@@ -804,11 +805,21 @@ struct Engine {
     ln(lj, g.mat(12, 0), g.mat(13, 0), p);
     const float* wu = W(g.mat(14, 0), p, P.mode);
     std::vector<GemmJob> gj;
-    for (size_t j = 0; j < jobs.size(); ++j) {
+    bool contiguous = true;  // all segments' logits back to back: one tall GEMM
+    for (size_t j = 0; j < jobs.size(); ++j)
+      contiguous = contiguous && jobs[j].out == jobs[0].out + j * (size_t)rows * V;
+    if (contiguous) {
       GemmJob a{};
-      a.A = xq + j * (size_t)rows * D, a.B = wu, a.C = jobs[j].out;
-      a.M = rows, a.N = V, a.K = D, a.lda = D, a.ldb = V, a.ldc = V, a.prec = p, a.epi = 0;
+      a.A = xq, a.B = wu, a.C = jobs[0].out;
+      a.M = rows * (int)jobs.size(), a.N = V, a.K = D, a.lda = D, a.ldb = V, a.ldc = V, a.prec = p;
       gj.push_back(a);
+    } else {
+      for (size_t j = 0; j < jobs.size(); ++j) {
+        GemmJob a{};
+        a.A = xq + j * (size_t)rows * D, a.B = wu, a.C = jobs[j].out;
+        a.M = rows, a.N = V, a.K = D, a.lda = D, a.ldb = V, a.ldc = V, a.prec = p, a.epi = 0;
+        gj.push_back(a);
+      }
     }
     gemm(gj, "gemm_unembed");
   }

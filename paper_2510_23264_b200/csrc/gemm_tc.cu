@@ -21,7 +21,8 @@ constexpr int kStages = 4;
 constexpr int kBKBytes = 128;  // one SW128 atom row
 constexpr int kAStage = kTcBM * kBKBytes;  // 16 KB
 constexpr int kBStage = kTcBN * kBKBytes;  // 16 KB
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr size_t kSmemBytes = 1024 + (size_t)kStages * (kAStage + kBStage) + 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -35,6 +36,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -145,6 +149,138 @@ __device__ __forceinline__ void store_out(const TcJob& jb, int row, int col, flo
   }
 }
 
+// Epilogue of one tile for one warp: 32 TMEM lanes (rows) x 64 columns.
+template <int ELEM>
+__device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb, int tile, int mt,
+                                              int nt, uint32_t tacc, int q, int half, int lane) {
+  const int row = mt * kTcBM + q * 32 + lane;
+  const bool rvalid = row < jb.M;
+  const float sk = sqrtf((float)jb.K);
+  const float na = rvalid && L.a_norm ? L.a_norm[jb.a_row0 + row] : 0.f;
+  const float ku = L.kappa * 5.9604644775390625e-08f * sk;
+  uint32_t flagged[2];
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    const int c0 = half * 64 + cc * 32;
+    uint32_t r[32];
+    tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
+    uint32_t fl = 0;
+    const int colb = nt * kTcBN + c0;
+    if (rvalid && colb < jb.N) {
+      float v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int col = colb + j;
+        const float acc = __uint_as_float(r[j]);
+        v[j] = round_out(acc, jb.prec);
+        bool amb = !(acc == acc);
+        if (jb.prec != 2 && col < jb.N) {
+          const float nb = jb.b_norm ? __ldg(jb.b_norm + col) : 0.f;
+          // E4M3 x E4M3 products are multiples of 2^-18; if every partial sum
+          // is below 2^6 (|s_k| <= ||a|| ||b||) all of them are exact in
+          // FP32, so the reference's sequential sum is the exact sum and so is
+          // the tensor-core sum: the rounding is certified without a fixup.
+          const bool exact = ELEM == kTcE4M3 && na * nb < 63.99f;
+          if (!exact) {
+            const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
+            amb = amb || !(round_out(acc - m, jb.prec) == round_out(acc + m, jb.prec));
+          }
+        }
+        if (amb && col < jb.N) fl |= 1u << j;
+      }
+      if (jb.epi == 1) {
+        if (jb.prec == 1 && L.gelu_lut) {
+          uint16_t g[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) g[j] = __ldg(L.gelu_lut + enc_bf16(v[j]));
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = dec_bf16(g[j]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = round_out(gelu_ref(v[j]), jb.prec);
+        }
+      }
+      const int64_t o = (int64_t)row * jb.ldo + colb;
+      const bool full = colb + 32 <= jb.N && (jb.ldo & 15) == 0;
+      if (jb.out_f32) {
+        float* dst = jb.out_f32 + o;
+        if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+          for (int j = 0; j < 32 && colb + j < jb.N; ++j) dst[j] = v[j];
+        }
+      }
+      if (jb.out_pack) {
+        if (jb.prec == 1) {
+          uint16_t* dst = reinterpret_cast<uint16_t*>(jb.out_pack) + o;
+          if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint4 w;
+              w.x = enc_bf16(v[j]) | ((uint32_t)enc_bf16(v[j + 1]) << 16);
+              w.y = enc_bf16(v[j + 2]) | ((uint32_t)enc_bf16(v[j + 3]) << 16);
+              w.z = enc_bf16(v[j + 4]) | ((uint32_t)enc_bf16(v[j + 5]) << 16);
+              w.w = enc_bf16(v[j + 6]) | ((uint32_t)enc_bf16(v[j + 7]) << 16);
+              *reinterpret_cast<uint4*>(dst + j) = w;
+            }
+          } else {
+            for (int j = 0; j < 32 && colb + j < jb.N; ++j) dst[j] = enc_bf16(v[j]);
+          }
+        } else {
+          uint8_t* dst = reinterpret_cast<uint8_t*>(jb.out_pack) + o;
+          if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 16) {
+              uint32_t w[4];
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                w[t] = enc_e4m3(v[j + 4 * t]) | ((uint32_t)enc_e4m3(v[j + 4 * t + 1]) << 8) |
+                       ((uint32_t)enc_e4m3(v[j + 4 * t + 2]) << 16) |
+                       ((uint32_t)enc_e4m3(v[j + 4 * t + 3]) << 24);
+              *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          } else {
+            for (int j = 0; j < 32 && colb + j < jb.N; ++j) dst[j] = enc_e4m3(v[j]);
+          }
+        }
+      }
+    }
+    flagged[cc] = fl;
+  }
+  // Append flagged (tile, row, col) entries, row-contiguous, with one
+  // warp-aggregated atomic per warp.
+  const int cnt = __popc(flagged[0]) + __popc(flagged[1]);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return;
+  uint32_t base = 0;
+  if (lane == 31) base = atomicAdd(L.fix_count, (uint32_t)total);
+  base = __shfl_sync(0xffffffffu, base, 31) + (uint32_t)(incl - cnt);
+  const uint32_t rc = (uint32_t)(q * 32 + lane) << 8;
+#pragma unroll
+  for (int cc = 0; cc < 2; ++cc) {
+    uint32_t m = flagged[cc];
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      if (base < L.fix_cap) {
+        L.fix[2 * base] = (uint32_t)tile;
+        L.fix[2 * base + 1] = rc | (uint32_t)(half * 64 + cc * 32 + bit);
+      }
+      ++base;
+    }
+  }
+}
+
+// Persistent warp-specialised kernel: the TMEM accumulator is double
+// buffered, so the epilogue of tile i overlaps the MMAs of tile i+1.
 template <int ELEM>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ TcLaunch L, const TcJob* __restrict__ jobs) {
@@ -155,32 +291,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sB = smem + kStages * kAStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
   uint64_t* empty = full + kStages;
-  uint64_t* tmem_full = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + kStages;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ji = find_job(jobs, L.n_jobs, blockIdx.x);
-  const TcJob jb = jobs[ji];
-  const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
-  const int local = blockIdx.x - jb.tile0;
-  const int mt = local / tiles_n, nt = local % tiles_n;
   constexpr int esz = ELEM == kTcBF16 ? 2 : 1;
   constexpr int bke = kBKBytes / esz;  // elements per stage along K
-  const int kbytes = jb.K * esz;
-  const int nk = (kbytes + kBKBytes - 1) / kBKBytes;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(kTcBN));
+                 "r"(2 * kTcBN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -189,194 +322,141 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      const int arow = jb.a_row0 + mt * kTcBM;
-      const int brow = jb.b_row0 + nt * kTcBN;
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        if (kb >= kStages) mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
-        mbar_expect_tx(&full[s], kAStage + kBStage);
-        tma_load_2d(sA + s * kAStage, &L.tmA, &full[s], kb * bke, arow);
-        tma_load_2d(sB + s * kBStage, &L.tmB, &full[s], jb.b_k0 + kb * bke, brow);
+    if (lane == 0) {  // TMA producer
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
+        const TcJob& jb = jobs[find_job(jobs, L.n_jobs, tile)];
+        const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
+        const int mt = (tile - jb.tile0) / tiles_n, nt = (tile - jb.tile0) % tiles_n;
+        const int nk = (jb.K * esz + kBKBytes - 1) / kBKBytes;
+        const int arow = jb.a_row0 + mt * kTcBM, brow = jb.b_row0 + nt * kTcBN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&empty[s], ((it / kStages) & 1) ^ 1);
+          mbar_expect_tx(&full[s], kAStage + kBStage);
+          tma_load_2d(sA + s * kAStage, &L.tmA, &full[s], kb * bke, arow);
+          tma_load_2d(sB + s * kBStage, &L.tmB, &full[s], jb.b_k0 + kb * bke, brow);
+        }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0) {  // MMA issuer
       const uint32_t idesc = instr_desc<ELEM>();
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        mbar_wait(&full[s], (kb / kStages) & 1);
+      uint32_t it = 0, ti = 0;
+      for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x, ++ti) {
+        const TcJob& jb = jobs[find_job(jobs, L.n_jobs, tile)];
+        const int kbytes = jb.K * esz;
+        const int nk = (kbytes + kBKBytes - 1) / kBKBytes;
+        const uint32_t b = ti & 1, bph = (ti >> 1) & 1;
+        mbar_wait(&tempty[b], bph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int nmma = min(4, (kbytes - kb * kBKBytes) / 32);
-        const uint32_t a0 = smem_u32(sA + s * kAStage), b0 = smem_u32(sB + s * kBStage);
-        for (int k = 0; k < nmma; ++k)
-          mma<ELEM>(tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
-                    (kb | k) != 0 ? 1u : 0u);
-        mma_commit(&empty[s]);
-      }
-      mma_commit(tmem_full);
-    }
-  } else {
-    // epilogue: warp w reads TMEM lanes [32*(w%4), +32)
-    const int q = warp & 3;
-    const int row = mt * kTcBM + q * 32 + lane;
-    const bool rvalid = row < jb.M;
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const float sk = sqrtf((float)jb.K);
-    const float na = rvalid && L.a_norm ? L.a_norm[jb.a_row0 + row] : 0.f;
-    const float ku = L.kappa * 5.9604644775390625e-08f * sk;
-    uint32_t flagged[kTcBN / 32];
-    for (int c0 = 0; c0 < kTcBN; c0 += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
-      uint32_t fl = 0;
-      if (rvalid) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int col = nt * kTcBN + c0 + j;
-          if (col < jb.N) {
-            const float acc = __uint_as_float(r[j]);
-            float v = round_out(acc, jb.prec);
-            bool amb = !(acc == acc);
-            if (jb.prec != 2) {
-              const float nb = jb.b_norm ? jb.b_norm[col] : 0.f;
-              // E4M3 x E4M3 products are multiples of 2^-18; if every partial
-              // sum is below 2^6 (|s_k| <= ||a|| ||b||) all of them are exact
-              // in FP32, so the reference's sequential sum is the exact sum
-              // and so is the tensor-core sum: the rounding is certified.
-              const bool exact = ELEM == kTcE4M3 && na * nb < 63.99f;
-              if (!exact) {
-                const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
-                amb = amb || !(round_out(acc - m, jb.prec) == round_out(acc + m, jb.prec));
-              }
-            }
-            if (jb.epi == 1) {
-              if (jb.prec == 1 && L.gelu_lut) v = dec_bf16(L.gelu_lut[enc_bf16(v)]);
-              else v = round_out(gelu_ref(v), jb.prec);
-            }
-            store_out(jb, row, col, v);
-            if (amb) fl |= 1u << j;
-          }
+        const uint32_t tacc = tmem + b * kTcBN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % kStages;
+          mbar_wait(&full[s], (it / kStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const int nmma = min(4, (kbytes - kb * kBKBytes) / 32);
+          const uint32_t a0 = smem_u32(sA + s * kAStage), b0 = smem_u32(sB + s * kBStage);
+          for (int k = 0; k < nmma; ++k)
+            mma<ELEM>(tacc, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
+                      (kb | k) != 0 ? 1u : 0u);
+          mma_commit(&empty[s]);
         }
-      }
-      flagged[c0 / 32] = fl;
-    }
-    {  // per-tile row masks (always written) + compact list of flagged tiles
-      uint32_t any = 0;
-      uint32_t* tm = L.tile_mask + ((size_t)blockIdx.x * kTcBM + q * 32 + lane) * (kTcBN / 32);
-      for (int w = 0; w < kTcBN / 32; ++w) {
-        const uint32_t f = rvalid ? flagged[w] : 0u;
-        tm[w] = f;
-        any |= f;
-      }
-      any = __any_sync(0xffffffffu, any != 0);
-      if (any && lane == 0 && atomicOr(&L.tile_flag[blockIdx.x], 1u) == 0u) {
-        const uint32_t i = atomicAdd(L.fix_count, 1u);
-        if (i < L.fix_cap) L.fix[i] = blockIdx.x;
+        mma_commit(&tfull[b]);
       }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  } else {  // epilogue warps: lanes quarter (warp % 4), column half ((warp - 2) / 4)
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    uint32_t ti = 0;
+    for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x, ++ti) {
+      const int ji = find_job(jobs, L.n_jobs, tile);
+      const TcJob jb = jobs[ji];
+      const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
+      const int mt = (tile - jb.tile0) / tiles_n, nt = (tile - jb.tile0) % tiles_n;
+      const uint32_t b = ti & 1, bph = (ti >> 1) & 1;
+      mbar_wait(&tfull[b], bph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      epilogue_tile<ELEM>(L, jb, tile, mt, nt, tmem + b * kTcBN, q, half, lane);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+    }
   }
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcBN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kTcBN));
   }
 }
 
 // Exact sequential recomputation of flagged elements (dot_col order,
 // kernels.cpp:44-52): one warp per (row, tile) record, the A row staged once
 // in shared memory, each lane walking one flagged column's B row.
-// One CTA per flagged tile, one thread per tile row: A and B K-chunks are
-// staged (decoded) in shared memory and each thread walks up to kFixGroup of
-// its flagged columns per pass with the reference's sequential FP32 chain.
-constexpr int kFixChunk = 32, kFixGroup = 8;
+// Exact sequential recomputation of flagged elements (dot_col order,
+// kernels.cpp:44-52): one thread per flagged element; entries are
+// row-contiguous so the A-row loads of a warp mostly coincide (broadcast)
+// while each lane streams its own B row, all with 16-byte vector loads.
+template <int ELEM>
+__device__ __forceinline__ void dec16(const uint4 v, float* out) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  if (ELEM == kTcBF16) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) out[t] = dec_bf16((uint16_t)(w[t / 2] >> (16 * (t & 1))));
+  } else {
+#pragma unroll
+    for (int t = 0; t < 16; ++t) out[t] = dec_e4m3((uint8_t)(w[t / 4] >> (8 * (t & 3))));
+  }
+}
 
 template <int ELEM>
-__global__ void __launch_bounds__(kTcBM) gemm_fixup_kernel(const TcLaunch L,
-                                                            const TcJob* __restrict__ jobs) {
-  __shared__ float As[kTcBM][kFixChunk + 1];
-  __shared__ float Bs[kTcBN][kFixChunk + 1];
-  __shared__ int s_groups;
+__global__ void __launch_bounds__(256) gemm_fixup_kernel(const TcLaunch L,
+                                                          const TcJob* __restrict__ jobs) {
   const uint32_t n = min(*L.fix_count, L.fix_cap);
-  const int t = threadIdx.x;
-  for (uint32_t fi = blockIdx.x; fi < n; fi += gridDim.x) {
-    const int tile = (int)L.fix[fi];
-    const int ji = find_job(jobs, L.n_jobs, tile);
-    const TcJob jb = jobs[ji];
+  constexpr int esz = ELEM == kTcBF16 ? 2 : 1;
+  constexpr int vel = 16 / esz;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int tile = (int)L.fix[2 * i];
+    const uint32_t rc = L.fix[2 * i + 1];
+    const TcJob jb = jobs[find_job(jobs, L.n_jobs, tile)];
     const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
     const int mt = (tile - jb.tile0) / tiles_n, nt = (tile - jb.tile0) % tiles_n;
-    uint32_t mask[kTcBN / 32];
-    int nf = 0;
-    for (int w = 0; w < kTcBN / 32; ++w) {
-      mask[w] = L.tile_mask[((size_t)tile * kTcBM + t) * (kTcBN / 32) + w];
-      nf += __popc(mask[w]);
-    }
-    if (t == 0) s_groups = 0;
-    __syncthreads();
-    atomicMax(&s_groups, (nf + kFixGroup - 1) / kFixGroup);
-    __syncthreads();
-    const int groups = s_groups;
-    const int row = mt * kTcBM + t;
-    for (int gi = 0; gi < groups; ++gi) {
-      int cols[kFixGroup];
-      int nc = 0;
-      {  // the gi-th group of this thread's flagged columns
-        int seen = 0;
-        for (int w = 0; w < kTcBN / 32; ++w) {
-          uint32_t m = mask[w];
-          while (m) {
-            const int bit = __ffs(m) - 1;
-            m &= m - 1;
-            if (seen >= gi * kFixGroup && nc < kFixGroup) cols[nc++] = w * 32 + bit;
-            ++seen;
-          }
-        }
-      }
-      float acc[kFixGroup];
+    const int row = mt * kTcBM + (int)(rc >> 8), col = nt * kTcBN + (int)(rc & 0xFF);
+    const uint4* a = reinterpret_cast<const uint4*>(L.A + (int64_t)(jb.a_row0 + row) * L.lda);
+    const uint4* b = reinterpret_cast<const uint4*>(L.B + (int64_t)(jb.b_row0 + col) * L.ldb +
+                                                    (int64_t)jb.b_k0 * esz);
+    float acc = 0.f;
+    const int nv = jb.K / vel;  // K * esz is a multiple of 32 bytes
+    // batches of kPf vectors: the next batch is in flight while the current
+    // one runs through the (latency-bound) sequential FADD chain
+    constexpr int kPf = 8;
+    uint4 ab[kPf], bb[kPf];
 #pragma unroll
-      for (int j = 0; j < kFixGroup; ++j) acc[j] = 0.f;
-      for (int k0 = 0; k0 < jb.K; k0 += kFixChunk) {
-        __syncthreads();
-        for (int idx = t; idx < kTcBM * kFixChunk; idx += kTcBM) {
-          const int rr = idx / kFixChunk, kk = idx % kFixChunk, k = k0 + kk;
-          const int ar = mt * kTcBM + rr, bc = nt * kTcBN + rr;
-          float av = 0.f, bv = 0.f;
-          if (k < jb.K) {
-            if (ar < jb.M) {
-              const uint8_t* a = L.A + (int64_t)(jb.a_row0 + ar) * L.lda;
-              av = ELEM == kTcBF16 ? dec_bf16(reinterpret_cast<const uint16_t*>(a)[k]) : dec_e4m3(a[k]);
-            }
-            if (bc < jb.N) {
-              const uint8_t* b = L.B + (int64_t)(jb.b_row0 + bc) * L.ldb;
-              const int kb = jb.b_k0 + k;
-              bv = ELEM == kTcBF16 ? dec_bf16(reinterpret_cast<const uint16_t*>(b)[kb]) : dec_e4m3(b[kb]);
-            }
-          }
-          As[rr][kk] = av;
-          Bs[rr][kk] = bv;
-        }
-        __syncthreads();
-        const int kl = min(kFixChunk, jb.K - k0);
-        for (int kk = 0; kk < kl; ++kk) {
-          const float a = As[t][kk];
+    for (int p = 0; p < kPf; ++p)
+      if (p < nv) ab[p] = __ldg(a + p), bb[p] = __ldg(b + p);
+    for (int v0 = 0; v0 < nv; v0 += kPf) {
+      uint4 an[kPf], bn[kPf];
 #pragma unroll
-          for (int j = 0; j < kFixGroup; ++j)
-            if (j < nc) acc[j] = __fadd_rn(acc[j], __fmul_rn(a, Bs[cols[j]][kk]));
+      for (int p = 0; p < kPf; ++p)
+        if (v0 + kPf + p < nv) an[p] = __ldg(a + v0 + kPf + p), bn[p] = __ldg(b + v0 + kPf + p);
+#pragma unroll
+      for (int p = 0; p < kPf; ++p) {
+        if (v0 + p < nv) {
+          float x[vel], y[vel];
+          dec16<ELEM>(ab[p], x);
+          dec16<ELEM>(bb[p], y);
+#pragma unroll
+          for (int t = 0; t < vel; ++t) acc = __fadd_rn(acc, __fmul_rn(x[t], y[t]));
         }
       }
-      for (int j = 0; j < nc; ++j) {
-        const int col = nt * kTcBN + cols[j];
-        float v = round_out(acc[j], jb.prec);
-        if (jb.epi == 1) {
-          if (jb.prec == 1 && L.gelu_lut) v = dec_bf16(L.gelu_lut[enc_bf16(v)]);
-          else v = round_out(gelu_ref(v), jb.prec);
-        }
-        store_out(jb, row, col, v);
-      }
+#pragma unroll
+      for (int p = 0; p < kPf; ++p) ab[p] = an[p], bb[p] = bn[p];
     }
-    __syncthreads();
+    float v = round_out(acc, jb.prec);
+    if (jb.epi == 1) {
+      if (jb.prec == 1 && L.gelu_lut) v = dec_bf16(L.gelu_lut[enc_bf16(v)]);
+      else v = round_out(gelu_ref(v), jb.prec);
+    }
+    store_out(jb, row, col, v);
   }
 }
 
@@ -466,17 +546,16 @@ void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
                          (int)kSmemBytes);
     attr = true;
   }
+  const int grid = std::min(L.total_tiles, 148);
   if (L.elem == kTcBF16)
-    gemm_tc_kernel<kTcBF16><<<L.total_tiles, kThreads, kSmemBytes, st>>>(L, d_jobs);
+    gemm_tc_kernel<kTcBF16><<<grid, kThreads, kSmemBytes, st>>>(L, d_jobs);
   else
-    gemm_tc_kernel<kTcE4M3><<<L.total_tiles, kThreads, kSmemBytes, st>>>(L, d_jobs);
+    gemm_tc_kernel<kTcE4M3><<<grid, kThreads, kSmemBytes, st>>>(L, d_jobs);
 }
 
 void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
-  const int blocks = std::min(L.total_tiles, 148 * 8);
-  if (blocks <= 0) return;
-  if (L.elem == kTcBF16) gemm_fixup_kernel<kTcBF16><<<blocks, kTcBM, 0, st>>>(L, d_jobs);
-  else gemm_fixup_kernel<kTcE4M3><<<blocks, kTcBM, 0, st>>>(L, d_jobs);
+  if (L.elem == kTcBF16) gemm_fixup_kernel<kTcBF16><<<148 * 8, 256, 0, st>>>(L, d_jobs);
+  else gemm_fixup_kernel<kTcE4M3><<<148 * 8, 256, 0, st>>>(L, d_jobs);
 }
 
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st) { gelu_lut_kernel<<<256, 256, 0, st>>>(lut); }

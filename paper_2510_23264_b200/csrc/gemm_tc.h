@@ -44,11 +44,9 @@ struct TcLaunch {
   const float* a_norm;  // [rows of A] ||A row||
   int elem;          // TcElem
   int n_jobs, total_tiles;
-  uint32_t* fix;        // compact list of tiles holding flagged elements
-  uint32_t* fix_count;  // entries in fix (per launch)
-  uint32_t fix_cap;     // >= total_tiles
-  uint32_t* tile_mask;  // [total_tiles][kTcBM][kTcBN/32] flagged-column bits per row
-  uint32_t* tile_flag;  // [total_tiles], zeroed before the launch
+  uint32_t* fix;        // flagged elements: {tile, row << 8 | col} pairs (row-contiguous)
+  uint32_t* fix_count;  // entries appended by the launch (zeroed after it)
+  uint32_t fix_cap;     // capacity in entries
   float kappa;
   const uint16_t* gelu_lut;  // bf16 -> round_bf16(gelu(x)) for all 2^16 inputs
 };

@@ -132,12 +132,77 @@ __global__ void __launch_bounds__(kLnRows) ln_kernel(const LnJob* __restrict__ j
   }
 }
 
+// Warp-per-32-rows variant: each warp owns a private padded 32 x 32 tile, so
+// warps progress independently (no block barriers); each lane runs its row's
+// sequential FP32 chain while the next 32-column chunk is already loading.
+__global__ void __launch_bounds__(128) ln_warp_kernel(const LnJob* __restrict__ jobs,
+                                                      const float* __restrict__ gamma,
+                                                      const float* __restrict__ beta, int D,
+                                                      int prec) {
+  __shared__ float tiles[4][32][33];
+  const LnJob j = jobs[blockIdx.y];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = (blockIdx.x * 4 + warp) * 32;
+  if (r0 >= j.rows) return;
+  float (*tile)[33] = tiles[warp];
+  const int nr = min(32, j.rows - r0);
+  float mean = 0.f, acc = 0.f;
+  float cur[32], nxt[32];
+  auto load = [&](int c0, float (&v)[32]) {
+    const int c = c0 + lane;
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      v[r] = (r < nr && c < D) ? j.in[(int64_t)(r0 + r) * j.in_stride + c] : 0.f;
+  };
+  for (int pass = 0; pass < 2; ++pass) {
+    acc = 0.f;
+    load(0, cur);
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      if (c0 + 32 < D) load(c0 + 32, nxt);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) tile[r][lane] = cur[r];
+      __syncwarp();
+      const int lim = min(32, D - c0);
+      if (pass == 0) {
+        for (int cc = 0; cc < lim; ++cc) acc = __fadd_rn(acc, tile[lane][cc]);
+      } else {
+        for (int cc = 0; cc < lim; ++cc) {
+          const float c = __fsub_rn(tile[lane][cc], mean);
+          acc = __fadd_rn(acc, __fmul_rn(c, c));
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 32; ++r) cur[r] = nxt[r];
+    }
+    acc = __fdiv_rn(acc, (float)D);  // mean /= d  |  var /= d
+    if (pass == 0) mean = acc;
+  }
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(acc, 1e-5f)));
+  for (int r = 0; r < nr; ++r) {
+    const float mr = __shfl_sync(0xffffffffu, mean, r);
+    const float ir = __shfl_sync(0xffffffffu, inv, r);
+    const int64_t row = r0 + r;
+    for (int c = lane; c < D; c += 32) {
+      const float x = j.in[row * j.in_stride + c];
+      const float y = __fadd_rn(__fmul_rn(gamma[c], __fmul_rn(__fsub_rn(x, mr), ir)), beta[c]);
+      if (j.xln) j.xln[row * D + c] = y;
+      const float q = round_p(y, prec);
+      if (j.xq) j.xq[row * D + c] = q;
+      if (j.xqp) {
+        if (j.pack == 2) reinterpret_cast<uint16_t*>(j.xqp)[row * D + c] = enc_bf16(q);
+        else reinterpret_cast<uint8_t*>(j.xqp)[row * D + c] = enc_e4m3(q);
+      }
+    }
+  }
+}
+
 void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float* gamma,
                       const float* beta, int D, int prec, cudaStream_t st) {
   if (n_jobs <= 0 || max_rows <= 0) return;
   for (int y0 = 0; y0 < n_jobs; y0 += 65535) {
-    dim3 grid((max_rows + kLnRows - 1) / kLnRows, (unsigned)std::min(65535, n_jobs - y0));
-    ln_kernel<<<grid, kLnRows, 0, st>>>(d_jobs + y0, gamma, beta, D, prec);
+    dim3 grid((max_rows + 127) / 128, (unsigned)std::min(65535, n_jobs - y0));
+    ln_warp_kernel<<<grid, 128, 0, st>>>(d_jobs + y0, gamma, beta, D, prec);
   }
 }
 
@@ -221,6 +286,105 @@ void launch_gemm_exact(const GemmJob* d_jobs, const int* d_tile_start, int n_job
                        cudaStream_t st) {
   if (n_jobs <= 0 || total_tiles <= 0) return;
   gemm_exact_kernel<<<total_tiles, 256, 0, st>>>(d_jobs, d_tile_start, n_jobs);
+}
+
+// Large-tile variant (128 x 128, 8 x 8 per thread, register-prefetched k
+// tiles): same per-element k-ascending fl(acc + fl(a*b)) chain, ~2x the FP32
+// issue efficiency of the 64 x 64 kernel. Used for big exact GEMMs (the
+// FP32 unembed of every patched pass).
+constexpr int kXBM = 128, kXBN = 128, kXBK = 8;
+
+int gemm_exact_big_tiles(int M, int N) { return ((M + kXBM - 1) / kXBM) * ((N + kXBN - 1) / kXBN); }
+
+__global__ void __launch_bounds__(256) gemm_exact_big_kernel(const GemmJob* __restrict__ jobs,
+                                                             const int* __restrict__ tile_start,
+                                                             int n_jobs) {
+  int lo = 0, hi = n_jobs - 1;
+  const int t = blockIdx.x;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_start[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmJob jb = jobs[lo];
+  const int local = t - tile_start[lo];
+  const int tiles_m = (jb.M + kXBM - 1) / kXBM;
+  // column-major tile raster: consecutive CTAs share the B (weight) tile
+  const int m0 = (local % tiles_m) * kXBM, n0 = (local / tiles_m) * kXBN;
+  __shared__ __align__(16) float As[2][kXBK][kXBM];
+  __shared__ __align__(16) float Bs[2][kXBK][kXBN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  // loaders: A tile 128 x 8 (each thread 4 consecutive k of one row),
+  // B tile 8 x 128 (each thread 4 consecutive n of one k row)
+  const int a_r = tid >> 1, a_k = (tid & 1) * 4;
+  const int b_k = tid >> 5, b_n = (tid & 31) * 4;
+  float ra[4], rb[4];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gm = m0 + a_r, gk = k0 + a_k + i;
+      ra[i] = (gm < jb.M && gk < jb.K) ? jb.A[(int64_t)gm * jb.lda + gk] : 0.f;
+      const int gk2 = k0 + b_k, gn = n0 + b_n + i;
+      rb[i] = (gk2 < jb.K && gn < jb.N) ? jb.B[(int64_t)gk2 * jb.ldb + gn] : 0.f;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) As[buf][a_k + i][a_r] = ra[i];
+    *reinterpret_cast<float4*>(&Bs[buf][b_k][b_n]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
+  };
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  load(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < jb.K; k0 += kXBK) {
+    const bool more = k0 + kXBK < jb.K;
+    if (more) load(k0 + kXBK);
+    const int kl = min(kXBK, jb.K - k0);
+    for (int kk = 0; kk < kl; ++kk) {
+      // rows ty*4 + {0..3} and 64 + ty*4 + {0..3}; cols tx*4 + {0..3} and 64 + tx*4 + {0..3}
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(a[i], b[j]));
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int gm = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (gm >= jb.M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int gn = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (gn >= jb.N) continue;
+      float v = round_p(acc[i][j], jb.prec);
+      if (jb.epi == 1) v = round_p(gelu_ref(v), jb.prec);
+      jb.C[(int64_t)gm * jb.ldc + gn] = v;
+    }
+  }
+}
+
+void launch_gemm_exact_big(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs,
+                           int total_tiles, cudaStream_t st) {
+  if (n_jobs <= 0 || total_tiles <= 0) return;
+  gemm_exact_big_kernel<<<total_tiles, 256, 0, st>>>(d_jobs, d_tile_start, n_jobs);
 }
 
 // ---------------------------------------------------------------------------

@@ -53,6 +53,10 @@ struct GemmJob {
 void launch_gemm_exact(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs, int total_tiles,
                        cudaStream_t st);
 int gemm_exact_tiles(int M, int N);
+// 128 x 128-tile variant for large jobs (same numerics)
+void launch_gemm_exact_big(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs,
+                           int total_tiles, cudaStream_t st);
+int gemm_exact_big_tiles(int M, int N);
 
 // ---- K5: causal attention (kernels.cpp:167-219) + z rounding ---------------
 struct AttnJob {
