@@ -99,6 +99,7 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
     j.M = M, j.N = N, j.K = K, j.out_f32 = dC1, j.ldo = N, j.b_norm = bn, j.prec = prec, j.epi = epi;
     cudaMemcpy(dj, &j, sizeof j, cudaMemcpyHostToDevice);
     L.n_jobs = 1;
+    L.prec = prec, L.epi = epi;
     L.total_tiles = ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
     L.fix = fix, L.fix_count = cnt, L.fix_cap = (uint32_t)fcap;
     launch_gemm_tc(L, dj, 0);

@@ -570,6 +570,10 @@ struct Engine {
     }
     L.n_jobs = (int)jobs.size();
     L.total_tiles = total;
+    L.prec = jobs[0].prec;
+    L.epi = jobs[0].epi;
+    for (const TcJob& j : jobs)
+      if (j.prec != L.prec || j.epi != L.epi) throw Error(2, "internal: mixed epilogues in one TC launch");
     if (!fix_cnt.p) {
       fix_cnt.ensure(16);
       CK(cudaMemsetAsync(fix_cnt.p, 0, 16, st));
@@ -590,10 +594,10 @@ struct Engine {
       launch_gemm_tc(L, dj, st);
     }
     {
-      Prof pf(this, "gemm_fixup");
+      Prof pf(this, (std::string("gemm_fixup_") + name).c_str());
       launch_gemm_fixup(L, dj, st);
     }
-    launch_fix_account(L.fix_count, st);
+    launch_fix_account(L.fix_count, L.fix_cap, st);
     launched();
   }
 
@@ -1316,6 +1320,15 @@ struct Engine {
       CK(cudaStreamSynchronize(st));
     }
     for (int i = 0; i < n; ++i) out[i] = sums[i] / (double)item_total;
+    if (fix_cnt.p) {  // elements recomputed by the exact fixup; overflow check
+      uint32_t c[4] = {0, 0, 0, 0};
+      CK(cudaMemcpy(c, fix_cnt.p, 16, cudaMemcpyDeviceToHost));
+      stats.fallback_elems = (int64_t)c[1];
+      CK(cudaMemsetAsync(fix_cnt.as<uint32_t>() + 1, 0, 12, st));
+      if (c[3])
+        throw Error(2, "tensor-core fixup list overflow (" + std::to_string(c[2]) +
+                           " flagged elements in one launch)");
+    }
     stats.ms_baseline = ms_base;
     stats.ms_passes = ms_pass;
     CK(cudaEventRecord(ev1, st));

@@ -23,7 +23,9 @@ constexpr int kAStage = kTcBM * kBKBytes;  // 16 KB
 constexpr int kBStage = kTcBN * kBKBytes;  // 16 KB
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr size_t kSmemBytes = 1024 + (size_t)kStages * (kAStage + kBStage) + 256;
+constexpr size_t kStageFloats = 32 * 33;  // per epilogue warp store staging
+constexpr size_t kSmemBytes =
+    1024 + (size_t)kStages * (kAStage + kBStage) + 256 + 8 * 32 * 33 * sizeof(float);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -150,9 +152,10 @@ __device__ __forceinline__ void store_out(const TcJob& jb, int row, int col, flo
 }
 
 // Epilogue of one tile for one warp: 32 TMEM lanes (rows) x 64 columns.
-template <int ELEM>
+template <int ELEM, int PREC, int EPI>
 __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb, int tile, int mt,
-                                              int nt, uint32_t tacc, int q, int half, int lane) {
+                                              int nt, uint32_t tacc, int q, int half, int lane,
+                                              float* stage) {
   const int row = mt * kTcBM + q * 32 + lane;
   const bool rvalid = row < jb.M;
   const float sk = sqrtf((float)jb.K);
@@ -166,16 +169,21 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
     tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
     uint32_t fl = 0;
     const int colb = nt * kTcBN + c0;
-    if (rvalid && colb < jb.N) {
-      float v[32];
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = 0.f;
+#define v_of(j) v[j]
+    // column norms: one coalesced load per lane, broadcast by shuffles
+    const float nb_l = (PREC != 2 && jb.b_norm && colb + lane < jb.N) ? __ldg(jb.b_norm + colb + lane) : 0.f;
+    if (colb < jb.N) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
+        const float nb = __shfl_sync(0xffffffffu, nb_l, j);
         const int col = colb + j;
         const float acc = __uint_as_float(r[j]);
-        v[j] = round_out(acc, jb.prec);
+        v[j] = round_out(acc, PREC);
         bool amb = !(acc == acc);
-        if (jb.prec != 2 && col < jb.N) {
-          const float nb = jb.b_norm ? __ldg(jb.b_norm + col) : 0.f;
+        if (PREC != 2) {
           // E4M3 x E4M3 products are multiples of 2^-18; if every partial sum
           // is below 2^6 (|s_k| <= ||a|| ||b||) all of them are exact in
           // FP32, so the reference's sequential sum is the exact sum and so is
@@ -183,13 +191,13 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
           const bool exact = ELEM == kTcE4M3 && na * nb < 63.99f;
           if (!exact) {
             const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
-            amb = amb || !(round_out(acc - m, jb.prec) == round_out(acc + m, jb.prec));
+            amb = amb || !(round_out(acc - m, PREC) == round_out(acc + m, PREC));
           }
         }
-        if (amb && col < jb.N) fl |= 1u << j;
+        if (amb && rvalid && col < jb.N) fl |= 1u << j;
       }
-      if (jb.epi == 1) {
-        if (jb.prec == 1 && L.gelu_lut) {
+      if (EPI == 1) {
+        if (PREC == 1) {
           uint16_t g[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) g[j] = __ldg(L.gelu_lut + enc_bf16(v[j]));
@@ -197,56 +205,63 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
           for (int j = 0; j < 32; ++j) v[j] = dec_bf16(g[j]);
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = round_out(gelu_ref(v[j]), jb.prec);
-        }
-      }
-      const int64_t o = (int64_t)row * jb.ldo + colb;
-      const bool full = colb + 32 <= jb.N && (jb.ldo & 15) == 0;
-      if (jb.out_f32) {
-        float* dst = jb.out_f32 + o;
-        if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        } else {
-          for (int j = 0; j < 32 && colb + j < jb.N; ++j) dst[j] = v[j];
-        }
-      }
-      if (jb.out_pack) {
-        if (jb.prec == 1) {
-          uint16_t* dst = reinterpret_cast<uint16_t*>(jb.out_pack) + o;
-          if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              uint4 w;
-              w.x = enc_bf16(v[j]) | ((uint32_t)enc_bf16(v[j + 1]) << 16);
-              w.y = enc_bf16(v[j + 2]) | ((uint32_t)enc_bf16(v[j + 3]) << 16);
-              w.z = enc_bf16(v[j + 4]) | ((uint32_t)enc_bf16(v[j + 5]) << 16);
-              w.w = enc_bf16(v[j + 6]) | ((uint32_t)enc_bf16(v[j + 7]) << 16);
-              *reinterpret_cast<uint4*>(dst + j) = w;
-            }
-          } else {
-            for (int j = 0; j < 32 && colb + j < jb.N; ++j) dst[j] = enc_bf16(v[j]);
-          }
-        } else {
-          uint8_t* dst = reinterpret_cast<uint8_t*>(jb.out_pack) + o;
-          if (full && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 16) {
-              uint32_t w[4];
-#pragma unroll
-              for (int t = 0; t < 4; ++t)
-                w[t] = enc_e4m3(v[j + 4 * t]) | ((uint32_t)enc_e4m3(v[j + 4 * t + 1]) << 8) |
-                       ((uint32_t)enc_e4m3(v[j + 4 * t + 2]) << 16) |
-                       ((uint32_t)enc_e4m3(v[j + 4 * t + 3]) << 24);
-              *reinterpret_cast<uint4*>(dst + j) = make_uint4(w[0], w[1], w[2], w[3]);
-            }
-          } else {
-            for (int j = 0; j < 32 && colb + j < jb.N; ++j) dst[j] = enc_e4m3(v[j]);
-          }
+          for (int j = 0; j < 32; ++j) v[j] = round_out(gelu_ref(v[j]), PREC);
         }
       }
     }
+    // Stores are staged through a warp-private smem tile and written row by
+    // row, so every store instruction covers one contiguous row segment.
+    const int row0 = mt * kTcBM + q * 32;
+    const int ncol = min(32, jb.N - colb);
+    if (ncol > 0) {
+      if (jb.out_f32) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = v_of(j);
+        __syncwarp();
+        for (int r = 0; r < 32 && row0 + r < jb.M; ++r)
+          if (lane < ncol) jb.out_f32[(int64_t)(row0 + r) * jb.ldo + colb + lane] = stage[r * 33 + lane];
+        __syncwarp();
+      }
+      if (jb.out_pack) {
+        uint32_t* sw = reinterpret_cast<uint32_t*>(stage);
+        if (PREC == 1) {  // 16 words of bf16 pairs per row
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            sw[lane * 17 + j] = enc_bf16(v_of(2 * j)) | ((uint32_t)enc_bf16(v_of(2 * j + 1)) << 16);
+          __syncwarp();
+          const bool w32 = ncol == 32 && (((reinterpret_cast<uintptr_t>(jb.out_pack) >> 1) + colb) & 1) == 0 &&
+                           (jb.ldo & 1) == 0;
+          for (int r = 0; r < 32 && row0 + r < jb.M; ++r) {
+            uint16_t* dst = reinterpret_cast<uint16_t*>(jb.out_pack) + (int64_t)(row0 + r) * jb.ldo + colb;
+            if (w32) {
+              if (lane < 16) reinterpret_cast<uint32_t*>(dst)[lane] = sw[r * 17 + lane];
+            } else if (lane < ncol) {
+              dst[lane] = (uint16_t)(sw[r * 17 + lane / 2] >> (16 * (lane & 1)));
+            }
+          }
+          __syncwarp();
+        } else {  // 8 words of E4M3 quads per row
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            sw[lane * 9 + j] = enc_e4m3(v_of(4 * j)) | ((uint32_t)enc_e4m3(v_of(4 * j + 1)) << 8) |
+                               ((uint32_t)enc_e4m3(v_of(4 * j + 2)) << 16) |
+                               ((uint32_t)enc_e4m3(v_of(4 * j + 3)) << 24);
+          __syncwarp();
+          const bool w32 = ncol == 32 && ((reinterpret_cast<uintptr_t>(jb.out_pack) + colb) & 3) == 0 &&
+                           (jb.ldo & 3) == 0;
+          for (int r = 0; r < 32 && row0 + r < jb.M; ++r) {
+            uint8_t* dst = reinterpret_cast<uint8_t*>(jb.out_pack) + (int64_t)(row0 + r) * jb.ldo + colb;
+            if (w32) {
+              if (lane < 8) reinterpret_cast<uint32_t*>(dst)[lane] = sw[r * 9 + lane];
+            } else if (lane < ncol) {
+              dst[lane] = (uint8_t)(sw[r * 9 + lane / 4] >> (8 * (lane & 3)));
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+#undef v_of
     flagged[cc] = fl;
   }
   // Append flagged (tile, row, col) entries, row-contiguous, with one
@@ -281,7 +296,7 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
 
 // Persistent warp-specialised kernel: the TMEM accumulator is double
 // buffered, so the epilogue of tile i overlaps the MMAs of tile i+1.
-template <int ELEM>
+template <int ELEM, int PREC, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ TcLaunch L, const TcJob* __restrict__ jobs) {
   extern __shared__ uint8_t smem_raw[];
@@ -294,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kStages;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* stage_all = reinterpret_cast<float*>(smem + kStages * (kAStage + kBStage) + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int esz = ELEM == kTcBF16 ? 2 : 1;
@@ -376,7 +392,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t b = ti & 1, bph = (ti >> 1) & 1;
       mbar_wait(&tfull[b], bph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      epilogue_tile<ELEM>(L, jb, tile, mt, nt, tmem + b * kTcBN, q, half, lane);
+      epilogue_tile<ELEM, PREC, EPI>(L, jb, tile, mt, nt, tmem + b * kTcBN, q, half, lane,
+                          stage_all + (size_t)(warp - 2) * kStageFloats);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
@@ -538,19 +555,24 @@ bool tc_make_map(CUtensorMap* map, const void* base, int elem, uint64_t rows, ui
 
 void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
   if (L.total_tiles <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_tc_kernel<kTcE4M3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSmemBytes);
-    cudaFuncSetAttribute(gemm_tc_kernel<kTcBF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSmemBytes);
-    attr = true;
-  }
   const int grid = std::min(L.total_tiles, 148);
-  if (L.elem == kTcBF16)
-    gemm_tc_kernel<kTcBF16><<<grid, kThreads, kSmemBytes, st>>>(L, d_jobs);
-  else
-    gemm_tc_kernel<kTcE4M3><<<grid, kThreads, kSmemBytes, st>>>(L, d_jobs);
+  // (element, output precision, GELU epilogue) specialisations keep each
+  // epilogue's code small (the generic one thrashed the instruction cache)
+  auto go = [&](auto kern) {
+    static bool attr = false;  // one static per instantiation of the lambda body
+    (void)attr;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    kern<<<grid, kThreads, kSmemBytes, st>>>(L, d_jobs);
+  };
+  if (L.elem == kTcBF16) {
+    if (L.prec == 1 && L.epi == 1) go(gemm_tc_kernel<kTcBF16, 1, 1>);
+    else if (L.prec == 1) go(gemm_tc_kernel<kTcBF16, 1, 0>);
+    else go(gemm_tc_kernel<kTcBF16, 2, 0>);
+  } else {
+    if (L.prec == 0 && L.epi == 1) go(gemm_tc_kernel<kTcE4M3, 0, 1>);
+    else if (L.prec == 0) go(gemm_tc_kernel<kTcE4M3, 0, 0>);
+    else go(gemm_tc_kernel<kTcE4M3, 2, 0>);
+  }
 }
 
 void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
@@ -560,14 +582,18 @@ void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) 
 
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st) { gelu_lut_kernel<<<256, 256, 0, st>>>(lut); }
 
-__global__ void fix_account_kernel(uint32_t* cnt) {
-  // cnt[0]: this launch's flagged count; cnt[1]: running total; cnt[2]: max per launch
+__global__ void fix_account_kernel(uint32_t* cnt, uint32_t cap) {
+  // cnt[0]: this launch's flagged count; cnt[1]: running total;
+  // cnt[2]: max per launch; cnt[3]: set if any launch exceeded its capacity
   cnt[1] += cnt[0];
   cnt[2] = max(cnt[2], cnt[0]);
+  if (cnt[0] > cap) cnt[3] = 1;
   cnt[0] = 0;
 }
 
-void launch_fix_account(uint32_t* cnt, cudaStream_t st) { fix_account_kernel<<<1, 1, 0, st>>>(cnt); }
+void launch_fix_account(uint32_t* cnt, uint32_t cap, cudaStream_t st) {
+  fix_account_kernel<<<1, 1, 0, st>>>(cnt, cap);
+}
 
 void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,
                     cudaStream_t st) {

@@ -43,6 +43,7 @@ struct TcLaunch {
   int64_t lda, ldb;  // bytes
   const float* a_norm;  // [rows of A] ||A row||
   int elem;          // TcElem
+  int prec, epi;     // launch-uniform output rounding / GELU epilogue (== every job's)
   int n_jobs, total_tiles;
   uint32_t* fix;        // flagged elements: {tile, row << 8 | col} pairs (row-contiguous)
   uint32_t* fix_count;  // entries appended by the launch (zeroed after it)
@@ -59,8 +60,8 @@ void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
 void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
 // lut[b] = enc_bf16(round_bf16(gelu_ref(dec_bf16(b)))) (glibc-exact erff)
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st);
-// cnt[1] += cnt[0]; cnt[2] = max(cnt[2], cnt[0]); cnt[0] = 0
-void launch_fix_account(uint32_t* cnt, cudaStream_t st);
+// cnt[1] += cnt[0]; cnt[2] = max(cnt[2], cnt[0]); cnt[3] |= cnt[0] > cap; cnt[0] = 0
+void launch_fix_account(uint32_t* cnt, uint32_t cap, cudaStream_t st);
 // ||row|| of a packed [rows][K] operand (elements starting at col k0)
 void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,
                     cudaStream_t st);

@@ -22,3 +22,4 @@ for it in range(2):
 prof = e.profile()
 for k, v in sorted(prof.items(), key=lambda kv: -kv[1]['ms']):
     print(f"  {k:12s} {v['ms']:10.1f} ms  launches {v['launches']:6d}  TFLOP/s {v['flops']/max(v['ms'],1e-9)/1e9:8.2f}  GB/s {v['bytes']/max(v['ms'],1e-9)/1e6:8.1f}")
+print("fallback elems", e.stats()["fallback_elems"], "passes", e.stats()["passes"])
