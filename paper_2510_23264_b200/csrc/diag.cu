@@ -38,11 +38,10 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
   const int esz = elem == kTcBF16 ? 2 : 1;
   float *dA, *dBt, *dB, *dC1, *dC2, *an, *bn;
   uint8_t *pA, *pB;
-  uint32_t *fix, *cnt;
+  uint32_t *fmask, *ftiles, *fmark, *cnt;
   TcJob* dj;
   int* dts;
   GemmJob* dg;
-  size_t fcap = (size_t)M * N;
   cudaMalloc(&dA, (size_t)M * K * 4);
   cudaMalloc(&dBt, (size_t)N * K * 4);
   cudaMalloc(&dB, (size_t)N * K * 4);
@@ -52,7 +51,11 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
   cudaMalloc(&bn, (size_t)N * 4);
   cudaMalloc(&pA, (size_t)M * K * esz);
   cudaMalloc(&pB, (size_t)N * K * esz);
-  cudaMalloc(&fix, fcap * 8);
+  const size_t ntile = (size_t)((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
+  cudaMalloc(&fmask, ntile * kFixWords * 4);
+  cudaMalloc(&ftiles, ntile * 4);
+  cudaMalloc(&fmark, ntile * 4);
+  cudaMemset(fmark, 0, ntile * 4);
   cudaMalloc(&cnt, 16);
   cudaMalloc(&dj, sizeof(TcJob));
   cudaMalloc(&dts, sizeof(int));
@@ -101,7 +104,7 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
     L.n_jobs = 1;
     L.prec = prec, L.epi = epi;
     L.total_tiles = ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
-    L.fix = fix, L.fix_count = cnt, L.fix_cap = (uint32_t)fcap;
+    L.fix_mask = fmask, L.fix_tiles = ftiles, L.tile_mark = fmark, L.fix_count = cnt;
     launch_gemm_tc(L, dj, 0);
     launch_gemm_fixup(L, dj, 0);
     // exact reference product on the decoded grid values
@@ -115,10 +118,12 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
     if (cudaDeviceSynchronize() != cudaSuccess) rc = 2;
     cudaMemcpy(out_tc, dC1, (size_t)M * N * 4, cudaMemcpyDeviceToHost);
     cudaMemcpy(out_exact, dC2, (size_t)M * N * 4, cudaMemcpyDeviceToHost);
-    cudaMemcpy(n_fix, cnt, 4, cudaMemcpyDeviceToHost);
+    uint64_t c[2] = {0, 0};
+    cudaMemcpy(c, cnt, 16, cudaMemcpyDeviceToHost);
+    *n_fix = (uint32_t)c[1];
   }
   for (void* p : {(void*)dA, (void*)dBt, (void*)dB, (void*)dC1, (void*)dC2, (void*)an, (void*)bn,
-                  (void*)pA, (void*)pB, (void*)fix, (void*)cnt, (void*)dj, (void*)dts, (void*)dg})
+                  (void*)pA, (void*)pB, (void*)fmask, (void*)ftiles, (void*)fmark, (void*)cnt, (void*)dj, (void*)dts, (void*)dg})
     cudaFree(p);
   return rc;
 }

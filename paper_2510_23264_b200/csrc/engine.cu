@@ -490,7 +490,7 @@ struct Engine {
     int rows = 0, cols = 0, elem = 0;
   };
   std::map<std::tuple<int, int, int>, std::unique_ptr<PackedB>> packed;
-  DeviceBuf fix_list, fix_cnt, gelu_lut;
+  DeviceBuf fix_mask, fix_tiles, tile_mark, fix_cnt, gelu_lut;
 
   // which: 0 QKV [3D x D], 1 W_O [D x D] (per-head K slices), 2 W_in^T [4D x D],
   // 3 W_out^T [D x 4D]
@@ -578,13 +578,15 @@ struct Engine {
       fix_cnt.ensure(16);
       CK(cudaMemsetAsync(fix_cnt.p, 0, 16, st));
     }
-    // capacity: 12.5% of the outputs (typical flagged share 0-5%); an
-    // overflow is detected after the call (fix_cnt[2]) and reported.
-    const size_t cap = std::max<size_t>((size_t)1 << 20, (size_t)total * kTcBM * kTcBN / 8);
-    fix_list.ensure(cap * 8);
-    L.fix = fix_list.as<uint32_t>();
+    fix_mask.ensure((size_t)total * kFixWords * 4);
+    fix_tiles.ensure((size_t)total * 4);
+    const size_t had = tile_mark.bytes;
+    tile_mark.ensure((size_t)total * 4);
+    if (tile_mark.bytes != had) CK(cudaMemsetAsync(tile_mark.p, 0, tile_mark.bytes, st));
+    L.fix_mask = fix_mask.as<uint32_t>();
+    L.fix_tiles = fix_tiles.as<uint32_t>();
+    L.tile_mark = tile_mark.as<uint32_t>();
     L.fix_count = fix_cnt.as<uint32_t>();
-    L.fix_cap = (uint32_t)std::min<size_t>(cap, 0xFFFFFFFFu);
     reserve(up_bytes(jobs.size(), sizeof(TcJob)));
     const TcJob* dj = upload(jobs);
     {
@@ -597,7 +599,7 @@ struct Engine {
       Prof pf(this, (std::string("gemm_fixup_") + name).c_str());
       launch_gemm_fixup(L, dj, st);
     }
-    launch_fix_account(L.fix_count, L.fix_cap, st);
+    launch_fix_account(L.fix_count, st);
     launched();
   }
 
@@ -1320,14 +1322,11 @@ struct Engine {
       CK(cudaStreamSynchronize(st));
     }
     for (int i = 0; i < n; ++i) out[i] = sums[i] / (double)item_total;
-    if (fix_cnt.p) {  // elements recomputed by the exact fixup; overflow check
-      uint32_t c[4] = {0, 0, 0, 0};
+    if (fix_cnt.p) {  // elements recomputed by the exact fixup
+      uint64_t c[2] = {0, 0};
       CK(cudaMemcpy(c, fix_cnt.p, 16, cudaMemcpyDeviceToHost));
       stats.fallback_elems = (int64_t)c[1];
-      CK(cudaMemsetAsync(fix_cnt.as<uint32_t>() + 1, 0, 12, st));
-      if (c[3])
-        throw Error(2, "tensor-core fixup list overflow (" + std::to_string(c[2]) +
-                           " flagged elements in one launch)");
+      CK(cudaMemsetAsync(fix_cnt.as<uint32_t>() + 2, 0, 8, st));
     }
     stats.ms_baseline = ms_base;
     stats.ms_passes = ms_pass;

@@ -264,33 +264,19 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
 #undef v_of
     flagged[cc] = fl;
   }
-  // Append flagged (tile, row, col) entries, row-contiguous, with one
-  // warp-aggregated atomic per warp.
+  // Record the flagged bits of this warp's 32 x 64 part; the first part of a
+  // tile to flag anything lists the tile for the fixup kernel.
   const int cnt = __popc(flagged[0]) + __popc(flagged[1]);
-  int incl = cnt;
+  if (!__any_sync(0xffffffffu, cnt != 0)) return;
+  *reinterpret_cast<uint2*>(L.fix_mask + (size_t)tile * kFixWords + (q * 32 + lane) * 4 + half * 2) =
+      make_uint2(flagged[0], flagged[1]);
+  int total = cnt;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  if (total == 0) return;
-  uint32_t base = 0;
-  if (lane == 31) base = atomicAdd(L.fix_count, (uint32_t)total);
-  base = __shfl_sync(0xffffffffu, base, 31) + (uint32_t)(incl - cnt);
-  const uint32_t rc = (uint32_t)(q * 32 + lane) << 8;
-#pragma unroll
-  for (int cc = 0; cc < 2; ++cc) {
-    uint32_t m = flagged[cc];
-    while (m) {
-      const int bit = __ffs(m) - 1;
-      m &= m - 1;
-      if (base < L.fix_cap) {
-        L.fix[2 * base] = (uint32_t)tile;
-        L.fix[2 * base + 1] = rc | (uint32_t)(half * 64 + cc * 32 + bit);
-      }
-      ++base;
-    }
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+  if (lane == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(L.fix_count + 2), (unsigned long long)total);
+    if (atomicOr(L.tile_mark + tile, 1u << (q + 4 * half)) == 0u)
+      L.fix_tiles[atomicAdd(L.fix_count, 1u)] = (uint32_t)tile;
   }
 }
 
@@ -406,74 +392,175 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Exact sequential recomputation of flagged elements (dot_col order,
-// kernels.cpp:44-52): one warp per (row, tile) record, the A row staged once
-// in shared memory, each lane walking one flagged column's B row.
-// Exact sequential recomputation of flagged elements (dot_col order,
-// kernels.cpp:44-52): one thread per flagged element; entries are
-// row-contiguous so the A-row loads of a warp mostly coincide (broadcast)
-// while each lane streams its own B row, all with 16-byte vector loads.
 template <int ELEM>
 __device__ __forceinline__ void dec16(const uint4 v, float* out) {
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
   if (ELEM == kTcBF16) {
 #pragma unroll
-    for (int t = 0; t < 8; ++t) out[t] = dec_bf16((uint16_t)(w[t / 2] >> (16 * (t & 1))));
+    for (int t = 0; t < 4; ++t) {
+      out[2 * t] = __uint_as_float(w[t] << 16);
+      out[2 * t + 1] = __uint_as_float(w[t] & 0xFFFF0000u);
+    }
   } else {
 #pragma unroll
     for (int t = 0; t < 16; ++t) out[t] = dec_e4m3((uint8_t)(w[t / 4] >> (8 * (t & 3))));
   }
 }
 
+constexpr int kFixThreads = 512;
+constexpr int kFixPer = 2;  // flagged elements per thread per round
+constexpr int kFixStages = 4;
+constexpr size_t kFixSmem = 1024 + (size_t)kFixStages * (kAStage + kBStage) + 256 +
+                            (size_t)kTcBM * kTcBN * sizeof(uint16_t) + 1024;
+
+// Exact sequential recomputation of the flagged elements (dot_col order,
+// kernels.cpp:44-52: every product rounded, then added, k ascending). One
+// CTA per listed tile: the tile's A rows and B rows stream through a TMA ring
+// (the GEMM's own SW128 tensor maps) once per round of up to
+// kFixThreads * kFixPer elements, and every thread runs the FP32 chains of its
+// elements out of shared memory. Elements are taken in row-major order, so
+// the lanes of a warp mostly share A rows (smem broadcast).
 template <int ELEM>
-__global__ void __launch_bounds__(256) gemm_fixup_kernel(const TcLaunch L,
-                                                          const TcJob* __restrict__ jobs) {
-  const uint32_t n = min(*L.fix_count, L.fix_cap);
+__global__ void __launch_bounds__(kFixThreads, 1)
+    gemm_fixup_kernel(const __grid_constant__ TcLaunch L, const TcJob* __restrict__ jobs) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kFixStages * kAStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kFixStages * kBStage);
+  uint64_t* empty = full + kFixStages;
+  int* wsum = reinterpret_cast<int*>(empty + kFixStages);  // [4] + total
+  uint16_t* list = reinterpret_cast<uint16_t*>(smem + kFixStages * (kAStage + kBStage) + 256);
   constexpr int esz = ELEM == kTcBF16 ? 2 : 1;
+  constexpr int bke = kBKBytes / esz;
   constexpr int vel = 16 / esz;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int tile = (int)L.fix[2 * i];
-    const uint32_t rc = L.fix[2 * i + 1];
+  constexpr int kWarps = kFixThreads / 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kFixStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t n_tiles = *L.fix_count;
+  uint32_t ld = 0, it = 0;  // TMA loads issued / chunks consumed (ring phases)
+  for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+    const int tile = (int)L.fix_tiles[ti];
+    // ---- flagged (row, col) list of the tile in row-major order
+    int cnt = 0;
+    uint32_t w[4] = {0, 0, 0, 0};
+    if (tid < kTcBM) {
+      const uint32_t parts = L.tile_mark[tile];
+      const uint4 m = *reinterpret_cast<const uint4*>(L.fix_mask + (size_t)tile * kFixWords + tid * 4);
+      const int q = tid >> 5;
+      w[0] = (parts >> q) & 1u ? m.x : 0u;
+      w[1] = (parts >> q) & 1u ? m.y : 0u;
+      w[2] = (parts >> (q + 4)) & 1u ? m.z : 0u;
+      w[3] = (parts >> (q + 4)) & 1u ? m.w : 0u;
+      cnt = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (tid < kTcBM && lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (tid < kTcBM) {
+      int pos = incl - cnt;
+      for (int p = 0; p < warp; ++p) pos += wsum[p];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t m = w[k];
+        while (m) {
+          const int bit = __ffs(m) - 1;
+          m &= m - 1;
+          list[pos++] = (uint16_t)((tid << 8) | (k * 32 + bit));
+        }
+      }
+    }
+    if (tid == 0) L.tile_mark[tile] = 0u;  // ready for the next launch
+    __syncthreads();
+    const int n = wsum[0] + wsum[1] + wsum[2] + wsum[3];
     const TcJob jb = jobs[find_job(jobs, L.n_jobs, tile)];
     const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
     const int mt = (tile - jb.tile0) / tiles_n, nt = (tile - jb.tile0) % tiles_n;
-    const int row = mt * kTcBM + (int)(rc >> 8), col = nt * kTcBN + (int)(rc & 0xFF);
-    const uint4* a = reinterpret_cast<const uint4*>(L.A + (int64_t)(jb.a_row0 + row) * L.lda);
-    const uint4* b = reinterpret_cast<const uint4*>(L.B + (int64_t)(jb.b_row0 + col) * L.ldb +
-                                                    (int64_t)jb.b_k0 * esz);
-    float acc = 0.f;
-    const int nv = jb.K / vel;  // K * esz is a multiple of 32 bytes
-    // batches of kPf vectors: the next batch is in flight while the current
-    // one runs through the (latency-bound) sequential FADD chain
-    constexpr int kPf = 8;
-    uint4 ab[kPf], bb[kPf];
+    const int arow = jb.a_row0 + mt * kTcBM, brow = jb.b_row0 + nt * kTcBN;
+    const int kbytes = jb.K * esz;
+    const int nk = (kbytes + kBKBytes - 1) / kBKBytes;
+    for (int e0 = 0; e0 < n; e0 += kFixThreads * kFixPer) {
+      // ---- prologue: fill the ring
+      if (tid == 0) {
+        for (int kb = 0; kb < min(kFixStages, nk); ++kb, ++ld) {
+          const int s = ld % kFixStages;
+          mbar_wait(&empty[s], ((ld / kFixStages) & 1) ^ 1);
+          mbar_expect_tx(&full[s], kAStage + kBStage);
+          tma_load_2d(sA + s * kAStage, &L.tmA, &full[s], kb * bke, arow);
+          tma_load_2d(sB + s * kBStage, &L.tmB, &full[s], jb.b_k0 + kb * bke, brow);
+        }
+      }
+      int er[kFixPer], ec[kFixPer];
+      float acc[kFixPer];
 #pragma unroll
-    for (int p = 0; p < kPf; ++p)
-      if (p < nv) ab[p] = __ldg(a + p), bb[p] = __ldg(b + p);
-    for (int v0 = 0; v0 < nv; v0 += kPf) {
-      uint4 an[kPf], bn[kPf];
+      for (int j = 0; j < kFixPer; ++j) {
+        const int e = e0 + j * kFixThreads + tid;
+        const uint32_t rc = e < n ? list[e] : 0u;
+        er[j] = e < n ? (int)(rc >> 8) : -1;
+        ec[j] = (int)(rc & 0xFF);
+        acc[j] = 0.f;
+      }
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % kFixStages;
+        mbar_wait(&full[s], (it / kFixStages) & 1);
+        const uint8_t* a0 = sA + s * kAStage;
+        const uint8_t* b0 = sB + s * kBStage;
+        const int nu = min(8, (kbytes - kb * kBKBytes) / 16);
 #pragma unroll
-      for (int p = 0; p < kPf; ++p)
-        if (v0 + kPf + p < nv) an[p] = __ldg(a + v0 + kPf + p), bn[p] = __ldg(b + v0 + kPf + p);
+        for (int j = 0; j < kFixPer; ++j) {
+          if (er[j] < 0) continue;
+          const uint8_t* ar = a0 + er[j] * kBKBytes;
+          const uint8_t* br = b0 + ec[j] * kBKBytes;
+          const int ra = er[j] & 7, rb = ec[j] & 7;
+          float sacc = acc[j];
+#pragma unroll 2
+          for (int u = 0; u < nu; ++u) {
+            const uint4 av = *reinterpret_cast<const uint4*>(ar + ((u ^ ra) << 4));
+            const uint4 bv = *reinterpret_cast<const uint4*>(br + ((u ^ rb) << 4));
+            float x[vel], y[vel];
+            dec16<ELEM>(av, x);
+            dec16<ELEM>(bv, y);
 #pragma unroll
-      for (int p = 0; p < kPf; ++p) {
-        if (v0 + p < nv) {
-          float x[vel], y[vel];
-          dec16<ELEM>(ab[p], x);
-          dec16<ELEM>(bb[p], y);
-#pragma unroll
-          for (int t = 0; t < vel; ++t) acc = __fadd_rn(acc, __fmul_rn(x[t], y[t]));
+            for (int t = 0; t < vel; ++t) sacc = __fadd_rn(sacc, __fmul_rn(x[t], y[t]));
+          }
+          acc[j] = sacc;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (tid == 0 && kb + kFixStages < nk) {
+          const int ss = ld % kFixStages;
+          mbar_wait(&empty[ss], ((ld / kFixStages) & 1) ^ 1);
+          mbar_expect_tx(&full[ss], kAStage + kBStage);
+          tma_load_2d(sA + ss * kAStage, &L.tmA, &full[ss], (kb + kFixStages) * bke, arow);
+          tma_load_2d(sB + ss * kBStage, &L.tmB, &full[ss], jb.b_k0 + (kb + kFixStages) * bke, brow);
+          ++ld;
         }
       }
 #pragma unroll
-      for (int p = 0; p < kPf; ++p) ab[p] = an[p], bb[p] = bn[p];
+      for (int j = 0; j < kFixPer; ++j) {
+        if (er[j] < 0) continue;
+        float v = round_out(acc[j], jb.prec);
+        if (jb.epi == 1) {
+          if (jb.prec == 1 && L.gelu_lut) v = dec_bf16(L.gelu_lut[enc_bf16(v)]);
+          else v = round_out(gelu_ref(v), jb.prec);
+        }
+        store_out(jb, mt * kTcBM + er[j], nt * kTcBN + ec[j], v);
+      }
     }
-    float v = round_out(acc, jb.prec);
-    if (jb.epi == 1) {
-      if (jb.prec == 1 && L.gelu_lut) v = dec_bf16(L.gelu_lut[enc_bf16(v)]);
-      else v = round_out(gelu_ref(v), jb.prec);
-    }
-    store_out(jb, row, col, v);
+    __syncthreads();  // list reuse
   }
 }
 
@@ -576,23 +663,22 @@ void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
 }
 
 void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
-  if (L.elem == kTcBF16) gemm_fixup_kernel<kTcBF16><<<148 * 8, 256, 0, st>>>(L, d_jobs);
-  else gemm_fixup_kernel<kTcE4M3><<<148 * 8, 256, 0, st>>>(L, d_jobs);
+  if (L.total_tiles <= 0) return;
+  const int grid = std::min(L.total_tiles, 148);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFixSmem);
+    kern<<<grid, kFixThreads, kFixSmem, st>>>(L, d_jobs);
+  };
+  if (L.elem == kTcBF16) go(gemm_fixup_kernel<kTcBF16>);
+  else go(gemm_fixup_kernel<kTcE4M3>);
 }
 
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st) { gelu_lut_kernel<<<256, 256, 0, st>>>(lut); }
 
-__global__ void fix_account_kernel(uint32_t* cnt, uint32_t cap) {
-  // cnt[0]: this launch's flagged count; cnt[1]: running total;
-  // cnt[2]: max per launch; cnt[3]: set if any launch exceeded its capacity
-  cnt[1] += cnt[0];
-  cnt[2] = max(cnt[2], cnt[0]);
-  if (cnt[0] > cap) cnt[3] = 1;
-  cnt[0] = 0;
-}
+__global__ void fix_account_kernel(uint32_t* cnt) { cnt[0] = 0; }
 
-void launch_fix_account(uint32_t* cnt, uint32_t cap, cudaStream_t st) {
-  fix_account_kernel<<<1, 1, 0, st>>>(cnt, cap);
+void launch_fix_account(uint32_t* cnt, cudaStream_t st) {
+  fix_account_kernel<<<1, 1, 0, st>>>(cnt);
 }
 
 void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,

@@ -45,9 +45,12 @@ struct TcLaunch {
   int elem;          // TcElem
   int prec, epi;     // launch-uniform output rounding / GELU epilogue (== every job's)
   int n_jobs, total_tiles;
-  uint32_t* fix;        // flagged elements: {tile, row << 8 | col} pairs (row-contiguous)
-  uint32_t* fix_count;  // entries appended by the launch (zeroed after it)
-  uint32_t fix_cap;     // capacity in entries
+  uint32_t* fix_mask;   // [total_tiles][kFixWords] flagged bits, row r at r*4 (words = 32 cols);
+                        // valid for the 32 x 64 parts whose bit is set in tile_mark
+  uint32_t* fix_tiles;  // [total_tiles] tiles with flagged elements
+  uint32_t* tile_mark;  // [total_tiles] flagged-part bits (q + 4*half); zero between launches
+  uint32_t* fix_count;  // [0] tiles listed by this launch (zeroed after it),
+                        // [2..3] u64 running total of flagged elements
   float kappa;
   const uint16_t* gelu_lut;  // bf16 -> round_bf16(gelu(x)) for all 2^16 inputs
 };
@@ -60,8 +63,8 @@ void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
 void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
 // lut[b] = enc_bf16(round_bf16(gelu_ref(dec_bf16(b)))) (glibc-exact erff)
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st);
-// cnt[1] += cnt[0]; cnt[2] = max(cnt[2], cnt[0]); cnt[3] |= cnt[0] > cap; cnt[0] = 0
-void launch_fix_account(uint32_t* cnt, uint32_t cap, cudaStream_t st);
+// cnt[0] = 0 (the listed-tile count, after the fixup has consumed it)
+void launch_fix_account(uint32_t* cnt, cudaStream_t st);
 // ||row|| of a packed [rows][K] operand (elements starting at col k0)
 void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,
                     cudaStream_t st);
@@ -71,6 +74,6 @@ void launch_pack_t(const float* in, int K, int N, int ld_in, void* out, int64_t 
 
 constexpr int kTcBM = 128;
 constexpr int kTcBN = 128;
-constexpr int kFixRec = 3 + kTcBN / 32;
+constexpr int kFixWords = kTcBM * kTcBN / 32;
 
 }  // namespace cqg
