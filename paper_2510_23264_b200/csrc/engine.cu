@@ -587,6 +587,11 @@ struct Engine {
     L.fix_tiles = fix_tiles.as<uint32_t>();
     L.tile_mark = tile_mark.as<uint32_t>();
     L.fix_count = fix_cnt.as<uint32_t>();
+    uint64_t fixed0 = 0;
+    if (opt_profile) {  // flagged-element count (appended by the GEMM epilogue) -> fixup flops
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpy(&fixed0, fix_cnt.as<uint8_t>() + 8, 8, cudaMemcpyDeviceToHost));
+    }
     reserve(up_bytes(jobs.size(), sizeof(TcJob)));
     const TcJob* dj = upload(jobs);
     {
@@ -595,9 +600,16 @@ struct Engine {
               flops, bytes);
       launch_gemm_tc(L, dj, st);
     }
+    const std::string fname = std::string("gemm_fixup_") + name;
     {
-      Prof pf(this, (std::string("gemm_fixup_") + name).c_str());
+      Prof pf(this, fname.c_str());
       launch_gemm_fixup(L, dj, st);
+    }
+    if (opt_profile) {
+      uint64_t fixed1 = 0;
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpy(&fixed1, fix_cnt.as<uint8_t>() + 8, 8, cudaMemcpyDeviceToHost));
+      kprof[fname].flops += 2.0 * jobs[0].K * (double)(fixed1 - fixed0);
     }
     launch_fix_account(L.fix_count, st);
     launched();
