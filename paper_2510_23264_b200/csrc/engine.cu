@@ -466,6 +466,14 @@ struct Engine {
     if (big) launch_gemm_exact_big(upload(jobs), upload(ts), (int)jobs.size(), total, st);
     else launch_gemm_exact(upload(jobs), upload(ts), (int)jobs.size(), total, st);
   }
+  // Rtn4 activation groups (one per item), in place
+  static bool rtn4(int prec, const Policy& P) { return prec == 0 && P.mode == 1; }
+  void rtn_act(const std::vector<RtnJob>& jobs, int nb) {
+    if (jobs.empty()) return;
+    reserve(up_bytes(jobs.size(), sizeof(RtnJob)));
+    Prof pf(this, "rtn4_act");
+    launch_rtn_act(upload(jobs), (int)jobs.size(), nb, 4, st);
+  }
   void attn(const std::vector<AttnJob>& jobs, int nb) {
     if (jobs.empty()) return;
     reserve(up_bytes(jobs.size(), sizeof(AttnJob)));
@@ -475,8 +483,6 @@ struct Engine {
   }
 
   void check_policy(const Policy& P) {
-    if (P.mode == 1 && (P.att == 0 || P.mlp == 0 || P.emb == 0 || P.unemb == 0))
-      throw Error(1, "low_mode Rtn4 activations are not supported on the GPU path yet");
     if (P.th_l >= g.L || P.th_h >= g.H || (P.th_l >= 0 && P.th_h < 0))
       throw Error(1, "forward: target head out of range");
     if (P.tm >= 0 && (!g.mlp || P.tm >= g.L)) throw Error(1, "forward: target mlp out of range");
@@ -651,7 +657,13 @@ struct Engine {
     for (size_t u = 0; u < nu; ++u)
       lj.push_back({uin[u], xln_of[u] >= 0 ? xln + xln_of[u] * SEG : nullptr,
                     xq ? xq + u * SEG : nullptr, RB, D, xq8 ? xq8 + u * SEG : nullptr, 1});
-    ln(lj, g.mat(2, l), g.mat(3, l), p_low);
+    const bool r4 = rtn4(p_low, P);  // (tc is off for Rtn4)
+    ln(lj, g.mat(2, l), g.mat(3, l), r4 ? 2 : p_low);
+    std::vector<RtnJob> rq;
+    if (r4)
+      for (size_t u = 0; u < nu; ++u) rq.push_back({xq + u * SEG, (int64_t)g.S * D, g.S, D, D, 0});
+    rtn_act(rq, nb);
+    rq.clear();
 
     // Q/K/V: per unique input a [RB][3D] block (q | k | v, head-major columns)
     const size_t QKV = (size_t)RB * 3 * D;
@@ -685,8 +697,9 @@ struct Engine {
             GemmJob q{};
             q.A = xq + u * SEG, q.B = W(g.mat(4 + c, l), p_low, P.mode) + h * dk;
             q.C = blk + c * D + h * dk;
-            q.M = RB, q.N = dk, q.K = D, q.lda = D, q.ldb = D, q.ldc = 3 * D, q.prec = p_low;
+            q.M = RB, q.N = dk, q.K = D, q.lda = D, q.ldb = D, q.ldc = 3 * D, q.prec = r4 ? 2 : p_low;
             gj.push_back(q);
+            if (r4) rq.push_back({q.C, (int64_t)g.S * 3 * D, g.S, dk, 3 * D, 0});
           }
         }
     }
@@ -703,6 +716,8 @@ struct Engine {
     }
     if (tc) gemm_tc(kTcE4M3, xq8, (int64_t)nu * RB, D, *bq, tj, "qkv");
     gemm(gj, "gemm_qkv");
+    rtn_act(rq, nb);
+    rq.clear();
 
     // attention + z (FP32 for the exact W_O, E4M3 bytes for the tensor cores)
     const int wo_prec = P.wo_precision(l);
@@ -717,12 +732,15 @@ struct Engine {
       float* blk = qkv + u_of[j] * QKV;
       AttnJob a{};
       a.q = blk + h * dk, a.k = blk + D + h * dk, a.v = blk + 2 * D + h * dk, a.ld = 3 * D;
-      a.prec = target ? 2 : p_low, a.ldz = dk;
+      a.prec = (target || r4) ? 2 : p_low, a.ldz = dk;
       a.z = z ? z + j * per : nullptr;
+      if (r4 && !target) rq.push_back({a.z, (int64_t)g.S * dk, g.S, dk, dk, 0});
       a.z8 = z8 ? z8 + j * per : nullptr;
       aj.push_back(a);
     }
     attn(aj, nb);
+    rtn_act(rq, nb);
+    rq.clear();
     gj.clear();
     tj.clear();
     if (tc_wo) {
@@ -744,10 +762,12 @@ struct Engine {
         GemmJob o{};
         o.A = z + j * per, o.B = wo + (size_t)h * dk * D, o.C = jobs[j].out;
         o.M = RB, o.N = D, o.K = dk, o.lda = dk, o.ldb = D, o.ldc = D;
-        o.prec = target ? 2 : p_low, o.epi = 0;
+        o.prec = (target || r4) ? 2 : p_low, o.epi = 0;
         gj.push_back(o);
+        if (r4 && !target) rq.push_back({o.C, (int64_t)g.S * D, g.S, D, D, 0});
       }
       gemm(gj, "gemm_wo");
+      rtn_act(rq, nb);
     }
   }
 
@@ -791,22 +811,36 @@ struct Engine {
     float* hid = scratch("m_hid", jobs.size() * SEG * 4);
     std::vector<LnJob> lj;
     for (size_t j = 0; j < jobs.size(); ++j) lj.push_back({jobs[j].in, nullptr, xq + j * SEG, RB, D});
-    ln(lj, g.mat(8, l), g.mat(9, l), p);
+    const bool r4 = rtn4(p, P);
+    ln(lj, g.mat(8, l), g.mat(9, l), r4 ? 2 : p);
+    std::vector<RtnJob> r0, r1, r2, r3;
+    for (size_t j = 0; j < jobs.size() && r4; ++j) {
+      const int64_t S = g.S;
+      r0.push_back({xq + j * SEG, S * D, g.S, D, D, 0});
+      r1.push_back({hid + j * SEG * 4, S * 4 * D, g.S, 4 * D, 4 * D, 0});
+      r2.push_back({hid + j * SEG * 4, S * 4 * D, g.S, 4 * D, 4 * D, 1});
+      r3.push_back({jobs[j].out, S * D, g.S, D, D, 0});
+    }
+    rtn_act(r0, nb);
     const float* win = W(g.mat(10, l), p, P.mode);
     const float* wout = W(g.mat(11, l), p, P.mode);
     std::vector<GemmJob> g1, g2;
     for (size_t j = 0; j < jobs.size(); ++j) {
       GemmJob a{};
       a.A = xq + j * SEG, a.B = win, a.C = hid + j * SEG * 4;
-      a.M = RB, a.N = 4 * D, a.K = D, a.lda = D, a.ldb = 4 * D, a.ldc = 4 * D, a.prec = p, a.epi = 1;
+      a.M = RB, a.N = 4 * D, a.K = D, a.lda = D, a.ldb = 4 * D, a.ldc = 4 * D;
+      a.prec = r4 ? 2 : p, a.epi = r4 ? 0 : 1;
       g1.push_back(a);
       GemmJob b{};
       b.A = hid + j * SEG * 4, b.B = wout, b.C = jobs[j].out;
-      b.M = RB, b.N = D, b.K = 4 * D, b.lda = 4 * D, b.ldb = D, b.ldc = D, b.prec = p, b.epi = 0;
+      b.M = RB, b.N = D, b.K = 4 * D, b.lda = 4 * D, b.ldb = D, b.ldc = D, b.prec = r4 ? 2 : p, b.epi = 0;
       g2.push_back(b);
     }
     gemm(g1, "gemm_mlp_in");
+    rtn_act(r1, nb);  // round -> GELU -> round (model.cpp:727-731)
+    rtn_act(r2, nb);
     gemm(g2, "gemm_mlp_out");
+    rtn_act(r3, nb);
   }
 
   // unembed (model.cpp:741-753): all_rows=false computes only row S-1 of
@@ -815,6 +849,23 @@ struct Engine {
     if (jobs.empty()) return;
     const int rows = all_rows ? nb * g.S : nb, D = g.D, V = g.V;
     const int p = P.unemb;
+    if (rtn4(p, P)) {  // group = all S rows of an item: every row is needed
+      for (const SegIO& jb : jobs) {
+        float* xq = scratch("u_xq", (size_t)nb * g.S * D);
+        float* lg = all_rows ? jb.out : scratch("u_lg", (size_t)nb * g.S * V);
+        ln({{jb.in, nullptr, xq, nb * g.S, D}}, g.mat(12, 0), g.mat(13, 0), 2);
+        rtn_act({{xq, (int64_t)g.S * D, g.S, D, D, 0}}, nb);
+        GemmJob a{};
+        a.A = xq, a.B = W(g.mat(14, 0), p, P.mode), a.C = lg;
+        a.M = nb * g.S, a.N = V, a.K = D, a.lda = D, a.ldb = V, a.ldc = V, a.prec = 2;
+        gemm({a}, "gemm_unembed");
+        rtn_act({{lg, (int64_t)g.S * V, g.S, V, V, 0}}, nb);
+        if (!all_rows)
+          CK(cudaMemcpy2DAsync(jb.out, (size_t)V * 4, lg + (size_t)(g.S - 1) * V, (size_t)g.S * V * 4,
+                               (size_t)V * 4, nb, cudaMemcpyDeviceToDevice, st));
+      }
+      return;
+    }
     float* xq = scratch("u_xq", jobs.size() * (size_t)rows * D);
     std::vector<LnJob> lj;
     for (size_t j = 0; j < jobs.size(); ++j)
@@ -843,9 +894,11 @@ struct Engine {
   }
 
   void run_embed(const Policy& P, const int* d_tok, float* out, int nb) {
+    const bool r4 = rtn4(P.emb, P);
     launch_embed(d_tok, W(g.mat(0, 0), P.emb, P.mode), W(g.mat(1, 0), P.emb, P.mode), out, nb, g.S,
-                 g.D, P.emb, st);
+                 g.D, r4 ? 2 : P.emb, st);
     launched();
+    if (r4) rtn_act({{out, (int64_t)g.S * g.D, g.S, g.D, g.D, 0}}, nb);
   }
 
   // ---- a full (or suffix) forward over a trie: the baseline runs ----------

@@ -672,6 +672,33 @@ void launch_rtn_groups(const float* in, float* out, int n_groups, int64_t group_
     rtn_groups_kernel<<<n_groups, 256, 0, st>>>(in, out, group_off, rows, cols, ld, bits);
 }
 
+__global__ void rtn_act_kernel(const RtnJob* __restrict__ jobs, int bits) {
+  __shared__ double sh[32];
+  const RtnJob jb = jobs[blockIdx.y];
+  float* base = jb.p + (int64_t)blockIdx.x * jb.group_off;
+  const int64_t n = (int64_t)jb.rows * jb.cols;
+  double mx = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t off = (i / jb.cols) * jb.ld + (i % jb.cols);
+    float x = base[off];
+    if (jb.gelu) base[off] = x = gelu_ref(x);
+    const double a = fabs((double)x);
+    mx = (a > mx) ? a : mx;
+  }
+  mx = block_reduce(mx, MaxOp(), sh, (double)-INFINITY);
+  const double delta = (mx == 0.0) ? 0.0 : __ddiv_rn(mx, ldexp(1.0, bits - 1));
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t off = (i / jb.cols) * jb.ld + (i % jb.cols);
+    base[off] = rtn_apply(base[off], delta);
+  }
+}
+
+void launch_rtn_act(const RtnJob* d_jobs, int n_jobs, int n_groups, int bits, cudaStream_t st) {
+  for (int y0 = 0; y0 < n_jobs; y0 += 65535)
+    if (n_groups > 0)
+      rtn_act_kernel<<<dim3(n_groups, std::min(65535, n_jobs - y0)), 256, 0, st>>>(d_jobs + y0, bits);
+}
+
 // ---------------------------------------------------------------------------
 // exhaustive scalar checks (tests)
 // ---------------------------------------------------------------------------

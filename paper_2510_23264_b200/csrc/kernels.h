@@ -104,6 +104,18 @@ void launch_pack_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st
 void launch_rtn_groups(const float* in, float* out, int n_groups, int64_t group_off, int rows,
                        int cols, int ld, int bits, cudaStream_t st);
 
+// ---- Rtn4 activations (quantize_span P8/Rtn4, kernels.cpp:236-251) ---------
+// In place: each of n_groups groups (one per item) is a rows x cols block
+// with row stride ld, groups group_off apart; the whole group shares one
+// delta = max|x| / 2^(bits-1) (quantize_rtn, numerics.cpp:105-120).
+// gelu = 1 applies gelu_ref first (the MLP's round -> GELU -> round chain).
+struct RtnJob {
+  float* p;
+  int64_t group_off;
+  int rows, cols, ld, gelu;
+};
+void launch_rtn_act(const RtnJob* d_jobs, int n_jobs, int n_groups, int bits, cudaStream_t st);
+
 // ---- tests: exhaustive scalar checks on the device --------------------------
 void launch_e4m3_all(uint8_t* out, uint32_t lo, uint64_t count, cudaStream_t st);
 void launch_bf16_all(uint16_t* out, uint32_t lo, uint64_t count, cudaStream_t st);

@@ -16,7 +16,7 @@ import os
 import numpy as np
 import pytest
 
-from oracle.oracle import KL, LOGITDIFF, Policy, Port
+from oracle.oracle import KL, LOGITDIFF, P8, RTN4, Policy, Port
 from paper_2510_23264_b200 import engine as eng
 from paper_2510_23264_b200 import formats
 from helpers import GOLDEN, SMALL, TINY, TOY, bits, make, random_mask
@@ -121,6 +121,9 @@ def test_forward_bitexact(cfg):
             Policy.make(th=(L - 1, H - 1)), Policy.make(att=1), Policy.make(th=(0, 1))]
     if cfg.has_mlp:
         pols.append(Policy.make(tm=L - 1))
+    # Rtn4 activations (quantize_span P8/Rtn4, kernels.cpp:236-251): one delta per tensor
+    pols += [Policy.all_low(RTN4), Policy.make(mode=RTN4, th=(L - 1, 0)),
+             Policy.make(att=P8, mlp=P8, mode=RTN4, tm=0 if cfg.has_mlp else None)]
     SD = cfg.seq_len * cfg.d_model
     rng = np.random.RandomState(0)
     for i, pol in enumerate(pols):
@@ -171,6 +174,25 @@ def test_small_scores_match_oracle(per_edge, metric, mode):
                              metric=metric, mode=mode, mask=mask)
         got = e.score_edges(mask, edges, eng.PrecisionPolicy.head_quantized(), per_edge, mode)
         assert close(got, want), (seed, np.max(np.abs(got - want)))
+    e.close()
+
+
+@pytest.mark.parametrize("cfg", [SMALL, TOY])
+def test_rtn4_scores_match_oracle(cfg):
+    """PAHQ at 4 bits (ablation_policy(4) = head_quantized(P8, Rtn4), eval.cpp:1045)
+    and all-low Rtn4 (every activation tensor quantized with its own delta)."""
+    w, ds = make(cfg, 6, 3, 8)
+    p = Port(cfg, w.mats)
+    e = eng.Engine(w)
+    for metric in (KL, LOGITDIFF):
+        e.set_dataset(ds, metric)
+        for pol, per_edge, seed in ((Policy.head_quantized(mode=RTN4), True, None),
+                                    (Policy.all_low(RTN4), False, 13)):
+            mask = np.ones(p.n_edges, bool) if seed is None else random_mask(p.n_edges, seed, 0.6)
+            edges = np.nonzero(mask)[0]
+            want = p.score_edges(ds, edges, pol, per_edge=per_edge, metric=metric, mask=mask)
+            got = e.score_edges(mask, edges, gpol(pol), per_edge, 0)
+            assert close(got, want), (metric, per_edge, np.max(np.abs(got - want)))
     e.close()
 
 

@@ -191,7 +191,8 @@ def test_port_forward_equals_reference(ref, cfg, tmp_path):
     L, H = cfg.n_layers, cfg.n_heads
     pols = [Policy.all_fp32(), Policy.head_quantized(), Policy.all_low(),
             Policy.make(th=(L - 1, H - 1)), Policy.head_quantized(mode=1),
-            Policy.make(att=1), Policy.make(mode=1, th=(0, 0))]
+            Policy.make(att=1), Policy.make(mode=1, th=(0, 0)), Policy.all_low(1),
+            Policy.make(att=0, mlp=0, mode=1, tm=0 if cfg.has_mlp else None)]
     if cfg.has_mlp:
         pols.append(Policy.make(tm=0))
     for i, pol in enumerate(pols):
