@@ -623,9 +623,16 @@ struct Engine {
 
   // ---- node computations ----------------------------------------------------
   // attention layer (model.cpp:622-718) for a list of (input, head, output)
-  void run_heads(int l, const Policy& P, const std::vector<HeadIO>& jobs, int nb) {
+  // last_only: only row S-1 of each item is consumed downstream (the final
+  // layer under a loss metric): K/V still use every row, but the queries,
+  // attention, z and W_O run for the last row only and write that row of out.
+  void run_heads(int l, const Policy& P, const std::vector<HeadIO>& jobs, int nb,
+                 bool last_only = false) {
     if (jobs.empty()) return;
     const int RB = nb * g.S, D = g.D, dk = g.dk, H = g.H;
+    const int ZR = last_only ? nb : RB;  // z / W_O rows per job
+    const size_t o_off = last_only ? (size_t)(g.S - 1) * D : 0;
+    const int o_ld = last_only ? g.S * D : D;
     const size_t SEG = segf(nb);
     const int p_low = P.att;
     // tensor cores for the E4M3 projections of non-target heads
@@ -722,7 +729,7 @@ struct Engine {
     // attention + z (FP32 for the exact W_O, E4M3 bytes for the tensor cores)
     const int wo_prec = P.wo_precision(l);
     const bool tc_wo = tc && wo_prec == 0;
-    const size_t per = (size_t)RB * dk;
+    const size_t per = (size_t)ZR * dk;
     float* z = tc_wo ? nullptr : scratch("h_z", jobs.size() * per);
     uint8_t* z8 = tc_wo ? reinterpret_cast<uint8_t*>(scratch("h_z8", jobs.size() * per / 4 + 1)) : nullptr;
     std::vector<AttnJob> aj;
@@ -732,7 +739,7 @@ struct Engine {
       float* blk = qkv + u_of[j] * QKV;
       AttnJob a{};
       a.q = blk + h * dk, a.k = blk + D + h * dk, a.v = blk + 2 * D + h * dk, a.ld = 3 * D;
-      a.prec = (target || r4) ? 2 : p_low, a.ldz = dk;
+      a.prec = (target || r4) ? 2 : p_low, a.ldz = dk, a.q0 = last_only ? g.S - 1 : 0;
       a.z = z ? z + j * per : nullptr;
       if (r4 && !target) rq.push_back({a.z, (int64_t)g.S * dk, g.S, dk, dk, 0});
       a.z8 = z8 ? z8 + j * per : nullptr;
@@ -748,20 +755,20 @@ struct Engine {
       for (size_t j = 0; j < jobs.size(); ++j) {
         const int h = jobs[j].head;
         TcJob t{};
-        t.a_row0 = (int)j * RB, t.b_row0 = 0, t.b_k0 = h * dk, t.M = RB, t.N = D, t.K = dk;
-        t.out_f32 = jobs[j].out, t.ldo = D, t.b_norm = bo.norm.as<float>() + (size_t)h * D;
+        t.a_row0 = (int)j * ZR, t.b_row0 = 0, t.b_k0 = h * dk, t.M = ZR, t.N = D, t.K = dk;
+        t.out_f32 = jobs[j].out + o_off, t.ldo = o_ld, t.b_norm = bo.norm.as<float>() + (size_t)h * D;
         t.prec = p_low;
         tj.push_back(t);
       }
-      gemm_tc(kTcE4M3, z8, (int64_t)jobs.size() * RB, dk, bo, tj, "wo");
+      gemm_tc(kTcE4M3, z8, (int64_t)jobs.size() * ZR, dk, bo, tj, "wo");
     } else {
       const float* wo = W(g.mat(7, l), wo_prec, P.mode);
       for (size_t j = 0; j < jobs.size(); ++j) {
         const int h = jobs[j].head;
         const bool target = P.th_l == l && P.th_h == h;
         GemmJob o{};
-        o.A = z + j * per, o.B = wo + (size_t)h * dk * D, o.C = jobs[j].out;
-        o.M = RB, o.N = D, o.K = dk, o.lda = dk, o.ldb = D, o.ldc = D;
+        o.A = z + j * per, o.B = wo + (size_t)h * dk * D, o.C = jobs[j].out + o_off;
+        o.M = ZR, o.N = D, o.K = dk, o.lda = dk, o.ldb = D, o.ldc = o_ld;
         o.prec = (target || r4) ? 2 : p_low, o.epi = 0;
         gj.push_back(o);
         if (r4 && !target) rq.push_back({o.C, (int64_t)g.S * D, g.S, D, D, 0});
@@ -772,9 +779,12 @@ struct Engine {
   }
 
   // MLP (model.cpp:720-739)
-  void run_mlp(int l, const Policy& P, const std::vector<SegIO>& jobs, int nb) {
+  void run_mlp(int l, const Policy& P, const std::vector<SegIO>& jobs, int nb,
+               bool last_only = false) {
     if (jobs.empty()) return;
-    const int RB = nb * g.S, D = g.D;
+    const int RB = last_only ? nb : nb * g.S, D = g.D;
+    const size_t i_off = last_only ? (size_t)(g.S - 1) * D : 0;
+    const int i_ld = last_only ? g.S * D : D;
     const size_t SEG = segf(nb);
     const int node = g.stage_nodes[2 + 2 * l][0];
     const int p = P.precision_of(g, node);
@@ -787,7 +797,8 @@ struct Engine {
       uint8_t* hidp = reinterpret_cast<uint8_t*>(scratch("m_hidp", jobs.size() * SEG * esz + 1));
       std::vector<LnJob> lj;
       for (size_t j = 0; j < jobs.size(); ++j)
-        lj.push_back({jobs[j].in, nullptr, nullptr, RB, D, xqp + j * SEG * esz, elem == kTcBF16 ? 2 : 1});
+        lj.push_back({jobs[j].in + i_off, nullptr, nullptr, RB, i_ld, xqp + j * RB * D * esz,
+                      elem == kTcBF16 ? 2 : 1});
       ln(lj, g.mat(8, l), g.mat(9, l), p);
       const PackedB& bi = packedB(2, l, elem, p, P.mode);
       const PackedB& bo = packedB(3, l, elem, p, P.mode);
@@ -795,12 +806,12 @@ struct Engine {
       for (size_t j = 0; j < jobs.size(); ++j) {
         TcJob a{};
         a.a_row0 = (int)j * RB, a.M = RB, a.N = 4 * D, a.K = D;
-        a.out_pack = hidp + j * SEG * 4 * esz, a.ldo = 4 * D, a.b_norm = bi.norm.as<float>();
+        a.out_pack = hidp + j * RB * 4 * D * esz, a.ldo = 4 * D, a.b_norm = bi.norm.as<float>();
         a.prec = p, a.epi = 1;
         t1.push_back(a);
         TcJob b{};
         b.a_row0 = (int)j * RB, b.M = RB, b.N = D, b.K = 4 * D;
-        b.out_f32 = jobs[j].out, b.ldo = D, b.b_norm = bo.norm.as<float>(), b.prec = p;
+        b.out_f32 = jobs[j].out + i_off, b.ldo = i_ld, b.b_norm = bo.norm.as<float>(), b.prec = p;
         t2.push_back(b);
       }
       gemm_tc(elem, xqp, (int64_t)jobs.size() * RB, D, bi, t1, "mlp_in");
@@ -810,7 +821,7 @@ struct Engine {
     float* xq = scratch("m_xq", jobs.size() * SEG);
     float* hid = scratch("m_hid", jobs.size() * SEG * 4);
     std::vector<LnJob> lj;
-    for (size_t j = 0; j < jobs.size(); ++j) lj.push_back({jobs[j].in, nullptr, xq + j * SEG, RB, D});
+    for (size_t j = 0; j < jobs.size(); ++j) lj.push_back({jobs[j].in + i_off, nullptr, xq + j * SEG, RB, i_ld});
     const bool r4 = rtn4(p, P);
     ln(lj, g.mat(8, l), g.mat(9, l), r4 ? 2 : p);
     std::vector<RtnJob> r0, r1, r2, r3;
@@ -832,8 +843,8 @@ struct Engine {
       a.prec = r4 ? 2 : p, a.epi = r4 ? 0 : 1;
       g1.push_back(a);
       GemmJob b{};
-      b.A = hid + j * SEG * 4, b.B = wout, b.C = jobs[j].out;
-      b.M = RB, b.N = D, b.K = 4 * D, b.lda = 4 * D, b.ldb = D, b.ldc = D, b.prec = r4 ? 2 : p, b.epi = 0;
+      b.A = hid + j * SEG * 4, b.B = wout, b.C = jobs[j].out + i_off;
+      b.M = RB, b.N = D, b.K = 4 * D, b.lda = 4 * D, b.ldb = D, b.ldc = i_ld, b.prec = r4 ? 2 : p, b.epi = 0;
       g2.push_back(b);
     }
     gemm(g1, "gemm_mlp_in");
@@ -915,8 +926,15 @@ struct Engine {
     return T.rec_in[w] == 0 ? zeros(R.seg) : R.t(T.rec_in[w]);
   }
 
+  // loss metrics read only the last position of the logits: the final
+  // layer's attention outputs and MLP are then needed at row S-1 only
+  // (not under Rtn4, whose per-tensor delta spans every row).
+  bool last_rows(int l, const Policy& P, bool loss_only) const {
+    return loss_only && l == g.L - 1 && P.mode == 0;
+  }
+
   void forward_run(Run& R, const Trie& T, const Policy& P, const int* d_tok, int sigma0,
-                   bool all_rows, int* d_nan) {
+                   bool all_rows, int* d_nan, bool loss_only = false) {
     for (int s = sigma0; s < g.n_stages; ++s) {
       const auto& nodes = g.stage_nodes[s];
       if (nodes.empty()) continue;  // MLP stages of attention-only models
@@ -926,9 +944,10 @@ struct Engine {
       } else if (k == kHead) {
         std::vector<HeadIO> hj;
         for (int w : nodes) hj.push_back({input_of(T, R, w), g.head[w], R.o(w)});
-        run_heads(g.layer[nodes[0]], P, hj, R.nb);
+        run_heads(g.layer[nodes[0]], P, hj, R.nb, last_rows(g.layer[nodes[0]], P, loss_only));
       } else if (k == kMlp) {
-        run_mlp(g.layer[nodes[0]], P, {{input_of(T, R, nodes[0]), R.o(nodes[0])}}, R.nb);
+        run_mlp(g.layer[nodes[0]], P, {{input_of(T, R, nodes[0]), R.o(nodes[0])}}, R.nb,
+                last_rows(g.layer[nodes[0]], P, loss_only));
       } else {
         run_unembed(P, {{input_of(T, R, g.unembed), R.logits.as<float>()}}, R.nb, all_rows);
         if (!all_rows) {
@@ -1141,8 +1160,8 @@ struct Engine {
           }
         }
       }
-      if (k == kHead) run_heads(g.layer[nodes[0]], P, hj, nb);
-      else if (k == kMlp) run_mlp(g.layer[nodes[0]], P, mj, nb);
+      if (k == kHead) run_heads(g.layer[nodes[0]], P, hj, nb, last_rows(g.layer[nodes[0]], P, loss));
+      else if (k == kMlp) run_mlp(g.layer[nodes[0]], P, mj, nb, last_rows(g.layer[nodes[0]], P, loss));
       else if (k == kUnembed && !mj.empty()) {
         const bool all_rows = !loss;
         const size_t rows = all_rows ? (size_t)nb * g.S : (size_t)nb;
@@ -1319,7 +1338,7 @@ struct Engine {
       for (int i = 0; i < n; ++i) need_all_rows |= g.edst[edge_ids[i]] == g.unembed;
     prepare_run(base_run, T, B, need_all_rows);
     auto tb = std::chrono::steady_clock::now();
-    forward_run(base_run, T, base, tokens(base_tok), 0, need_all_rows, d_nan);
+    forward_run(base_run, T, base, tokens(base_tok), 0, need_all_rows, d_nan, loss);
     double ms_base = 0, ms_pass = 0;
     std::vector<double> sums(n, 0.0);
     std::vector<double> hd;
@@ -1330,9 +1349,9 @@ struct Engine {
       check_policy(P);
       if (per_edge && !(P == base)) {
         tb = std::chrono::steady_clock::now();
-        forward_run(base_run, T, P, tokens(base_tok), g.stage[src], need_all_rows, d_nan);
+        forward_run(base_run, T, P, tokens(base_tok), g.stage[src], need_all_rows, d_nan, loss);
       } else if (per_edge && src >= 0 && g.kind[src] == kEmbed) {
-        forward_run(base_run, T, P, tokens(base_tok), 0, need_all_rows, d_nan);
+        forward_run(base_run, T, P, tokens(base_tok), 0, need_all_rows, d_nan, loss);
       }
       CK(cudaStreamSynchronize(st));
       auto tp = std::chrono::steady_clock::now();

@@ -135,64 +135,103 @@ __global__ void __launch_bounds__(kLnRows) ln_kernel(const LnJob* __restrict__ j
 // Warp-per-32-rows variant: each warp owns a private padded 32 x 32 tile, so
 // warps progress independently (no block barriers); each lane runs its row's
 // sequential FP32 chain while the next 32-column chunk is already loading.
-__global__ void __launch_bounds__(128) ln_warp_kernel(const LnJob* __restrict__ jobs,
-                                                      const float* __restrict__ gamma,
-                                                      const float* __restrict__ beta, int D,
-                                                      int prec) {
-  __shared__ float tiles[4][32][33];
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// One warp per 32 rows, lane = row for the two sequential reductions
+// (mean = sum/D, var = sum((x-mean)^2)/D in column order, kernels.cpp:127-163).
+// The row block streams through a cp.async ring of 32 x 32 chunks, so many
+// chunks are in flight per warp; pass 3 normalises a chunk per lane-row and
+// writes it back row by row (coalesced).
+constexpr int kLnStages = 4;
+constexpr int kLnWarps = 4;
+constexpr int kLnTile = 32 * 33;
+
+__global__ void __launch_bounds__(32 * kLnWarps) ln_warp_kernel(const LnJob* __restrict__ jobs,
+                                                              const float* __restrict__ gamma,
+                                                              const float* __restrict__ beta,
+                                                              int D, int prec) {
+  extern __shared__ float ln_sm[];
   const LnJob j = jobs[blockIdx.y];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r0 = (blockIdx.x * 4 + warp) * 32;
+  const int r0 = (blockIdx.x * kLnWarps + warp) * 32;
   if (r0 >= j.rows) return;
-  float (*tile)[33] = tiles[warp];
+  float* ring = ln_sm + (size_t)warp * kLnStages * kLnTile;
   const int nr = min(32, j.rows - r0);
-  float mean = 0.f, acc = 0.f;
-  float cur[32], nxt[32];
-  auto load = [&](int c0, float (&v)[32]) {
-    const int c = c0 + lane;
-#pragma unroll
-    for (int r = 0; r < 32; ++r)
-      v[r] = (r < nr && c < D) ? j.in[(int64_t)(r0 + r) * j.in_stride + c] : 0.f;
+  const int nc = (D + 31) / 32;
+  // source of element (row r, col c0 + lane), clamped into the valid block
+  const int cl = lane;
+  auto issue = [&](int ch) {
+    float* t = ring + (ch % kLnStages) * kLnTile;
+    const int c = min(ch * 32 + cl, D - 1);
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {
+      const int rr = min(r, nr - 1);
+      cp_async4(t + r * 33 + cl, j.in + (int64_t)(r0 + rr) * j.in_stride + c);
+    }
   };
-  for (int pass = 0; pass < 2; ++pass) {
+  float mean = 0.f, acc = 0.f, inv = 0.f;
+  for (int pass = 0; pass < 3; ++pass) {
     acc = 0.f;
-    load(0, cur);
-    for (int c0 = 0; c0 < D; c0 += 32) {
-      if (c0 + 32 < D) load(c0 + 32, nxt);
 #pragma unroll
-      for (int r = 0; r < 32; ++r) tile[r][lane] = cur[r];
+    for (int p = 0; p < kLnStages - 1; ++p) {
+      if (p < nc) issue(p);
+      cp_async_commit();
+    }
+    float g_l = 0.f, b_l = 0.f;
+    for (int ch = 0; ch < nc; ++ch) {
+      if (ch + kLnStages - 1 < nc) issue(ch + kLnStages - 1);
+      cp_async_commit();
+      cp_async_wait<kLnStages - 1>();
       __syncwarp();
+      float* t = ring + (ch % kLnStages) * kLnTile;
+      const int c0 = ch * 32;
       const int lim = min(32, D - c0);
       if (pass == 0) {
-        for (int cc = 0; cc < lim; ++cc) acc = __fadd_rn(acc, tile[lane][cc]);
-      } else {
+        for (int cc = 0; cc < lim; ++cc) acc = __fadd_rn(acc, t[lane * 33 + cc]);
+      } else if (pass == 1) {
         for (int cc = 0; cc < lim; ++cc) {
-          const float c = __fsub_rn(tile[lane][cc], mean);
+          const float c = __fsub_rn(t[lane * 33 + cc], mean);
           acc = __fadd_rn(acc, __fmul_rn(c, c));
         }
+      } else {
+        if (c0 + lane < D) g_l = gamma[c0 + lane], b_l = beta[c0 + lane];
+        // y in place (row = lane), then row-wise coalesced stores
+        for (int cc = 0; cc < 32; ++cc) {
+          const float gc = __shfl_sync(0xffffffffu, g_l, cc), bc = __shfl_sync(0xffffffffu, b_l, cc);
+          const float x = t[lane * 33 + cc];
+          t[lane * 33 + cc] = __fadd_rn(__fmul_rn(gc, __fmul_rn(__fsub_rn(x, mean), inv)), bc);
+        }
+        __syncwarp();
+        if (lane < lim) {
+          for (int r = 0; r < nr; ++r) {
+            const int64_t o = (int64_t)(r0 + r) * D + c0 + lane;
+            const float y = t[r * 33 + lane];
+            if (j.xln) j.xln[o] = y;
+            const float q = round_p(y, prec);
+            if (j.xq) j.xq[o] = q;
+            if (j.xqp) {
+              if (j.pack == 2) reinterpret_cast<uint16_t*>(j.xqp)[o] = enc_bf16(q);
+              else reinterpret_cast<uint8_t*>(j.xqp)[o] = enc_e4m3(q);
+            }
+          }
+        }
       }
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < 32; ++r) cur[r] = nxt[r];
+      __syncwarp();  // the stage is refilled by the next iteration's issue
     }
-    acc = __fdiv_rn(acc, (float)D);  // mean /= d  |  var /= d
-    if (pass == 0) mean = acc;
-  }
-  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(acc, 1e-5f)));
-  for (int r = 0; r < nr; ++r) {
-    const float mr = __shfl_sync(0xffffffffu, mean, r);
-    const float ir = __shfl_sync(0xffffffffu, inv, r);
-    const int64_t row = r0 + r;
-    for (int c = lane; c < D; c += 32) {
-      const float x = j.in[row * j.in_stride + c];
-      const float y = __fadd_rn(__fmul_rn(gamma[c], __fmul_rn(__fsub_rn(x, mr), ir)), beta[c]);
-      if (j.xln) j.xln[row * D + c] = y;
-      const float q = round_p(y, prec);
-      if (j.xq) j.xq[row * D + c] = q;
-      if (j.xqp) {
-        if (j.pack == 2) reinterpret_cast<uint16_t*>(j.xqp)[row * D + c] = enc_bf16(q);
-        else reinterpret_cast<uint8_t*>(j.xqp)[row * D + c] = enc_e4m3(q);
-      }
+    cp_async_wait<0>();
+    if (pass < 2) {
+      acc = __fdiv_rn(acc, (float)D);  // mean /= d  |  var /= d
+      if (pass == 0) mean = acc;
+      else inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(acc, 1e-5f)));
     }
   }
 }
@@ -200,9 +239,15 @@ __global__ void __launch_bounds__(128) ln_warp_kernel(const LnJob* __restrict__ 
 void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float* gamma,
                       const float* beta, int D, int prec, cudaStream_t st) {
   if (n_jobs <= 0 || max_rows <= 0) return;
+  const size_t smem = sizeof(float) * kLnWarps * kLnStages * kLnTile;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ln_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
   for (int y0 = 0; y0 < n_jobs; y0 += 65535) {
-    dim3 grid((max_rows + 127) / 128, (unsigned)std::min(65535, n_jobs - y0));
-    ln_warp_kernel<<<grid, 128, 0, st>>>(d_jobs + y0, gamma, beta, D, prec);
+    dim3 grid((max_rows + 32 * kLnWarps - 1) / (32 * kLnWarps), (unsigned)std::min(65535, n_jobs - y0));
+    ln_warp_kernel<<<grid, 32 * kLnWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
   }
 }
 
@@ -388,9 +433,93 @@ void launch_gemm_exact_big(const GemmJob* d_jobs, const int* d_tile_start, int n
 }
 
 // ---------------------------------------------------------------------------
-// K5: causal attention, one CTA per (item, head job), one thread per query
-// row; reference order (kernels.cpp:167-190) with glibc-exact expf.
-// ---------------------------------------------------------------------------
+// K5: causal attention (kernels.cpp:167-219), one warp per (item, head job).
+// Exact reference order: score = (sum_t q_t k_t sequentially) * (1/sqrt(dk));
+// max; p = expf(s - max); den = sequential sum; p /= den; z_t = sequential
+// sum over j of p_j v_jt; z rounded at prec. Query rows q0..S-1 only (q0 =
+// S-1 when only the last position is consumed); z rows are compact:
+// item * (S - q0) + (i - q0).
+template <int NT>  // dk = 32 * NT
+__global__ void __launch_bounds__(128) attention_warp_kernel(const AttnJob* __restrict__ jobs,
+                                                             int n_inst, int B, int S) {
+  constexpr int dk = 32 * NT, ldk = dk + 1;
+  extern __shared__ float sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (w >= n_inst) return;
+  const int lds = S + 1;
+  float* q = sm + (size_t)warp * (3 * S * ldk + S * lds);
+  float* k = q + S * ldk;
+  float* v = k + S * ldk;
+  float* pr = v + S * ldk;
+  const AttnJob& jb = jobs[w / B];
+  const int item = w % B;
+  const int q0 = jb.q0;
+  const int64_t base = (int64_t)item * S;
+  // every load in flight at once (cp.async: no register staging, no
+  // generic-pointer aliasing between the global loads and the smem stores)
+  for (int r = 0; r < S; ++r) {
+    const int64_t g = (base + r) * jb.ld;
+#pragma unroll
+    for (int c = 0; c < NT; ++c) {
+      const int t = lane + 32 * c;
+      if (r >= q0) cp_async4(q + r * ldk + t, jb.q + g + t);
+      cp_async4(k + r * ldk + t, jb.k + g + t);
+      cp_async4(v + r * ldk + t, jb.v + g + t);
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+  const float scale = __fdiv_rn(1.0f, __fsqrt_rn((float)dk));
+  // scores for the causal pairs (i, j <= i), i >= q0
+  const int p0 = q0 * (q0 + 1) / 2, np = S * (S + 1) / 2 - p0;
+  for (int pi = lane; pi < np; pi += 32) {
+    const int pp = p0 + pi;
+    int i = (int)((sqrtf(8.f * pp + 1.f) - 1.f) * 0.5f);
+    while (i * (i + 1) / 2 > pp) --i;
+    while ((i + 1) * (i + 2) / 2 <= pp) ++i;
+    const int j = pp - i * (i + 1) / 2;
+    const float* qi = q + i * ldk;
+    const float* kj = k + j * ldk;
+    float acc = 0.f;
+#pragma unroll 16
+    for (int t = 0; t < dk; ++t) acc = __fadd_rn(acc, __fmul_rn(qi[t], kj[t]));
+    pr[i * lds + j] = __fmul_rn(acc, scale);
+  }
+  __syncwarp();
+  for (int i = q0 + lane; i < S; i += 32) {
+    float* p = pr + i * lds;
+    float mx = -INFINITY;
+    for (int j = 0; j <= i; ++j) mx = (mx < p[j]) ? p[j] : mx;
+    float den = 0.f;
+    for (int j = 0; j <= i; ++j) {
+      p[j] = glibc_expf(__fsub_rn(p[j], mx));
+      den = __fadd_rn(den, p[j]);
+    }
+    for (int j = 0; j <= i; ++j) p[j] = __fdiv_rn(p[j], den);
+  }
+  __syncwarp();
+  for (int i = q0; i < S; ++i) {
+    const float* p = pr + i * lds;
+    float acc[NT];
+#pragma unroll
+    for (int c = 0; c < NT; ++c) acc[c] = 0.f;
+    for (int j = 0; j <= i; ++j) {
+      const float pj = p[j];
+#pragma unroll
+      for (int c = 0; c < NT; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(pj, v[j * ldk + lane + 32 * c]));
+    }
+    const int64_t zr = (int64_t)item * (S - q0) + (i - q0);
+#pragma unroll
+    for (int c = 0; c < NT; ++c) {
+      const float zv = round_p(acc[c], jb.prec);
+      if (jb.z) jb.z[zr * jb.ldz + lane + 32 * c] = zv;
+      if (jb.z8) jb.z8[zr * jb.ldz + lane + 32 * c] = enc_e4m3(zv);
+    }
+  }
+}
+
+// generic dk: one CTA per (item, head job), one thread per query row
 __global__ void attention_kernel(const AttnJob* __restrict__ jobs, int S, int dk) {
   extern __shared__ float sm[];
   const AttnJob jb = jobs[blockIdx.y];
@@ -410,7 +539,7 @@ __global__ void attention_kernel(const AttnJob* __restrict__ jobs, int S, int dk
   }
   __syncthreads();
   const float scale = __fdiv_rn(1.0f, __fsqrt_rn((float)dk));
-  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+  for (int i = jb.q0 + threadIdx.x; i < S; i += blockDim.x) {
     float* p = pr + i * lds;
     float mx = -INFINITY;
     for (int jj = 0; jj <= i; ++jj) {
@@ -425,19 +554,35 @@ __global__ void attention_kernel(const AttnJob* __restrict__ jobs, int S, int dk
       den = __fadd_rn(den, p[jj]);
     }
     for (int jj = 0; jj <= i; ++jj) p[jj] = __fdiv_rn(p[jj], den);
+    const int64_t zr = (int64_t)item * (S - jb.q0) + (i - jb.q0);
     for (int t = 0; t < dk; ++t) {
       float acc = 0.f;
       for (int jj = 0; jj <= i; ++jj) acc = __fadd_rn(acc, __fmul_rn(p[jj], v[jj * ldk + t]));
-      const float zr = round_p(acc, jb.prec);
-      if (jb.z) jb.z[(base + i) * jb.ldz + t] = zr;
-      if (jb.z8) jb.z8[(base + i) * jb.ldz + t] = enc_e4m3(zr);
+      const float zr_v = round_p(acc, jb.prec);
+      if (jb.z) jb.z[zr * jb.ldz + t] = zr_v;
+      if (jb.z8) jb.z8[zr * jb.ldz + t] = enc_e4m3(zr_v);
     }
   }
 }
 
 void launch_attention(const AttnJob* d_jobs, int n_jobs, int B, int S, int dk, cudaStream_t st) {
   if (n_jobs <= 0) return;
-  const size_t smem = sizeof(float) * (size_t)(3 * S * (dk + 1) + S * (S + 1));
+  const size_t per_warp = sizeof(float) * (size_t)(3 * S * (dk + 1) + S * (S + 1));
+  if (dk % 32 == 0 && dk <= 128 && per_warp <= 200 * 1024) {
+    const int wpc = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / per_warp));
+    const int64_t n_inst = (int64_t)n_jobs * B;
+    const unsigned grid = (unsigned)((n_inst + wpc - 1) / wpc);
+    const size_t smem = per_warp * wpc;
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      kern<<<grid, 32 * wpc, smem, st>>>(d_jobs, (int)n_inst, B, S);
+    };
+    if (dk == 32) go(attention_warp_kernel<1>);
+    else if (dk == 64) go(attention_warp_kernel<2>);
+    else go(attention_warp_kernel<4>);
+    return;
+  }
+  const size_t smem = per_warp;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -68,6 +68,8 @@ struct AttnJob {
   int prec;  // rounding of z (model.cpp:688-689)
   int ldz;   // row stride of z / z8
   uint8_t* z8;  // packed E4M3 copy of z for the tensor-core W_O (may be null)
+  int q0;       // first query row computed (S-1: last position only); z rows
+                // are compact: item * (S - q0) + (i - q0)
 };
 void launch_attention(const AttnJob* d_jobs, int n_jobs, int B, int S, int dk, cudaStream_t st);
 
