@@ -159,7 +159,7 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
   const int row = mt * kTcBM + q * 32 + lane;
   const bool rvalid = row < jb.M;
   const float sk = sqrtf((float)jb.K);
-  const float na = rvalid && L.a_norm ? L.a_norm[jb.a_row0 + row] : 0.f;
+  const float na = rvalid && L.a_norm ? fabsf(L.a_norm[jb.a_row0 + row]) : 0.f;
   const float ku = L.kappa * 5.9604644775390625e-08f * sk;
   uint32_t flagged[2];
 #pragma unroll
@@ -174,7 +174,7 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
     for (int j = 0; j < 32; ++j) v[j] = 0.f;
 #define v_of(j) v[j]
     // column norms: one coalesced load per lane, broadcast by shuffles
-    const float nb_l = (PREC != 2 && jb.b_norm && colb + lane < jb.N) ? __ldg(jb.b_norm + colb + lane) : 0.f;
+    const float nb_l = (PREC != 2 && jb.b_norm && colb + lane < jb.N) ? fabsf(__ldg(jb.b_norm + colb + lane)) : 0.f;
     if (colb < jb.N) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -408,18 +408,144 @@ __device__ __forceinline__ void dec16(const uint4 v, float* out) {
 }
 
 constexpr int kFixThreads = 512;
-constexpr int kFixPer = 2;  // flagged elements per thread per round
+constexpr int kFixCols = 4;   // flagged columns of one row per work item
+constexpr int kFixPer = 2;    // work items per thread per round
 constexpr int kFixStages = 4;
+constexpr int kFixMaxItems = kTcBM * kTcBN / kFixCols + kTcBM;
 constexpr size_t kFixSmem = 1024 + (size_t)kFixStages * (kAStage + kBStage) + 256 +
-                            (size_t)kTcBM * kTcBN * sizeof(uint16_t) + 1024;
+                            (size_t)kFixMaxItems * sizeof(uint64_t) + 1024;
+
+// A row's norm carries a sign bit when the row holds a value whose products
+// might not be exact in FP32 (rownorm_kernel); otherwise fl(s + fl(a*b)) ==
+// fma(a, b, s) bit for bit, because the product is exact.
+__device__ __forceinline__ bool fma_safe(float norm) { return (__float_as_uint(norm) >> 31) == 0; }
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+// k then k+1 (low half first) of two packed BF16 pairs: fma.rn.f32.bf16 is
+// one rounding of the exact a*b + s (FHFMA.BF16 on sm_100a, no unpacking)
+__device__ __forceinline__ float fma_bf16x2(uint32_t a, uint32_t b, float s) {
+  asm("{\n.reg .b16 al, ah, bl, bh;\nmov.b32 {al, ah}, %1;\nmov.b32 {bl, bh}, %2;\n"
+      "fma.rn.f32.bf16 %0, al, bl, %0;\nfma.rn.f32.bf16 %0, ah, bh, %0;\n}"
+      : "+f"(s)
+      : "r"(a), "r"(b));
+  return s;
+}
+
+// Chains of one work item over 16-byte K units [u0, u0 + NU) of one chunk
+// (SW128 layout: unit u of row r lives at (u ^ (r & 7)) << 4 within the row).
+// All shared loads of the group are issued first (they are volatile, so the
+// compiler keeps their order), then the CPI chains consume them.
+template <int ELEM, bool FMA, int CPI, int NU>
+__device__ __forceinline__ void fix_units(uint32_t a_row, uint32_t ra16, const uint32_t (&b_row)[kFixCols],
+                                          const uint32_t (&rb16)[kFixCols], int u0,
+                                          float (&acc)[kFixCols]) {
+  uint4 av[NU], bv[CPI][NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) av[u] = lds128(a_row | (((uint32_t)(u0 + u) << 4) ^ ra16));
+#pragma unroll
+  for (int c = 0; c < CPI; ++c)
+#pragma unroll
+    for (int u = 0; u < NU; ++u) bv[c][u] = lds128(b_row[c] | (((uint32_t)(u0 + u) << 4) ^ rb16[c]));
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    if (ELEM == kTcBF16 && FMA) {
+#pragma unroll
+      for (int c = 0; c < CPI; ++c) {
+        float s = acc[c];
+        s = fma_bf16x2(av[u].x, bv[c][u].x, s);
+        s = fma_bf16x2(av[u].y, bv[c][u].y, s);
+        s = fma_bf16x2(av[u].z, bv[c][u].z, s);
+        s = fma_bf16x2(av[u].w, bv[c][u].w, s);
+        acc[c] = s;
+      }
+    } else {
+      constexpr int vel = ELEM == kTcBF16 ? 8 : 16;
+      float x[vel];
+      dec16<ELEM>(av[u], x);
+#pragma unroll
+      for (int c = 0; c < CPI; ++c) {
+        float y[vel];
+        dec16<ELEM>(bv[c][u], y);
+        float s = acc[c];
+#pragma unroll
+        for (int t = 0; t < vel; ++t) s = FMA ? __fmaf_rn(x[t], y[t], s) : __fadd_rn(s, __fmul_rn(x[t], y[t]));
+        acc[c] = s;
+      }
+    }
+  }
+}
+
+template <int ELEM, bool FMA, int CPI>
+__device__ __forceinline__ void fix_chunk(uint32_t a_row, uint32_t ra16, uint32_t b_stage,
+                                          const int (&col)[kFixCols], int nu, float (&acc)[kFixCols]) {
+  uint32_t b_row[kFixCols], rb16[kFixCols];
+#pragma unroll
+  for (int c = 0; c < CPI; ++c) b_row[c] = b_stage + col[c] * kBKBytes, rb16[c] = (col[c] & 7) << 4;
+  if (nu == 8) {
+    fix_units<ELEM, FMA, CPI, 4>(a_row, ra16, b_row, rb16, 0, acc);
+    fix_units<ELEM, FMA, CPI, 4>(a_row, ra16, b_row, rb16, 4, acc);
+  } else {
+    for (int u = 0; u < nu; ++u) fix_units<ELEM, FMA, CPI, 1>(a_row, ra16, b_row, rb16, u, acc);
+  }
+}
+
+struct FixItem {
+  int row;  // -1: none
+  int nc;
+  bool fma;
+  int col[kFixCols];
+  float acc[kFixCols];
+};
+
+// One round of the TMA ring over the tile's K extent for this thread's items.
+template <int ELEM, int CPI>
+__device__ __forceinline__ void fix_round(const TcLaunch& L, FixItem (&w)[kFixPer], uint8_t* sA,
+                                          uint8_t* sB, uint64_t* full, uint64_t* empty, int nk,
+                                          int kbytes, int arow, int brow, int bk0, uint32_t& ld,
+                                          uint32_t& it) {
+  constexpr int esz = ELEM == kTcBF16 ? 2 : 1;
+  constexpr int bke = kBKBytes / esz;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int kb = 0; kb < nk; ++kb, ++it) {
+    const int s = it % kFixStages;
+    mbar_wait(&full[s], (it / kFixStages) & 1);
+    const uint32_t a0 = smem_u32(sA + s * kAStage), b0 = smem_u32(sB + s * kBStage);
+    const int nu = min(8, (kbytes - kb * kBKBytes) / 16);
+#pragma unroll
+    for (int j = 0; j < kFixPer; ++j) {
+      if (w[j].row < 0) continue;
+      const uint32_t ar = a0 + w[j].row * kBKBytes, ra16 = (w[j].row & 7) << 4;
+      if (w[j].fma) fix_chunk<ELEM, true, CPI>(ar, ra16, b0, w[j].col, nu, w[j].acc);
+      else fix_chunk<ELEM, false, CPI>(ar, ra16, b0, w[j].col, nu, w[j].acc);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (tid == 0 && kb + kFixStages < nk) {
+      const int ss = ld % kFixStages;
+      mbar_wait(&empty[ss], ((ld / kFixStages) & 1) ^ 1);
+      mbar_expect_tx(&full[ss], kAStage + kBStage);
+      tma_load_2d(sA + ss * kAStage, &L.tmA, &full[ss], (kb + kFixStages) * bke, arow);
+      tma_load_2d(sB + ss * kBStage, &L.tmB, &full[ss], bk0 + (kb + kFixStages) * bke, brow);
+      ++ld;
+    }
+  }
+}
 
 // Exact sequential recomputation of the flagged elements (dot_col order,
 // kernels.cpp:44-52: every product rounded, then added, k ascending). One
 // CTA per listed tile: the tile's A rows and B rows stream through a TMA ring
-// (the GEMM's own SW128 tensor maps) once per round of up to
-// kFixThreads * kFixPer elements, and every thread runs the FP32 chains of its
-// elements out of shared memory. Elements are taken in row-major order, so
-// the lanes of a warp mostly share A rows (smem broadcast).
+// (the GEMM's own SW128 tensor maps) once per round, and every thread runs
+// the FP32 chains of its work items out of shared memory. A work item is up
+// to kFixCols flagged columns of one row (the A unit is loaded once for all).
+// Where every product is exact in FP32 the chain uses FMA (identical
+// result), for BF16 straight from the packed pairs (FHFMA.BF16).
 template <int ELEM>
 __global__ void __launch_bounds__(kFixThreads, 1)
     gemm_fixup_kernel(const __grid_constant__ TcLaunch L, const TcJob* __restrict__ jobs) {
@@ -430,11 +556,10 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   uint8_t* sB = smem + kFixStages * kAStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + kFixStages * kBStage);
   uint64_t* empty = full + kFixStages;
-  int* wsum = reinterpret_cast<int*>(empty + kFixStages);  // [4] + total
-  uint16_t* list = reinterpret_cast<uint16_t*>(smem + kFixStages * (kAStage + kBStage) + 256);
+  int* wsum = reinterpret_cast<int*>(empty + kFixStages);  // [8]
+  uint64_t* items = reinterpret_cast<uint64_t*>(smem + kFixStages * (kAStage + kBStage) + 256);
   constexpr int esz = ELEM == kTcBF16 ? 2 : 1;
   constexpr int bke = kBKBytes / esz;
-  constexpr int vel = 16 / esz;
   constexpr int kWarps = kFixThreads / 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -449,19 +574,30 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   uint32_t ld = 0, it = 0;  // TMA loads issued / chunks consumed (ring phases)
   for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
     const int tile = (int)L.fix_tiles[ti];
-    // ---- flagged (row, col) list of the tile in row-major order
-    int cnt = 0;
-    uint32_t w[4] = {0, 0, 0, 0};
+    // ---- work items: row | ncol << 8 | col_c << (16 + 12 c). Columns per item
+    // adapt to the tile's flagged count: one per item while the CTA has idle
+    // threads (parallelism), up to kFixCols when there is work to spare.
+    int pc = 0;
+    uint32_t wm[4] = {0, 0, 0, 0};
     if (tid < kTcBM) {
       const uint32_t parts = L.tile_mark[tile];
       const uint4 m = *reinterpret_cast<const uint4*>(L.fix_mask + (size_t)tile * kFixWords + tid * 4);
       const int q = tid >> 5;
-      w[0] = (parts >> q) & 1u ? m.x : 0u;
-      w[1] = (parts >> q) & 1u ? m.y : 0u;
-      w[2] = (parts >> (q + 4)) & 1u ? m.z : 0u;
-      w[3] = (parts >> (q + 4)) & 1u ? m.w : 0u;
-      cnt = __popc(w[0]) + __popc(w[1]) + __popc(w[2]) + __popc(w[3]);
+      wm[0] = (parts >> q) & 1u ? m.x : 0u;
+      wm[1] = (parts >> q) & 1u ? m.y : 0u;
+      wm[2] = (parts >> (q + 4)) & 1u ? m.z : 0u;
+      wm[3] = (parts >> (q + 4)) & 1u ? m.w : 0u;
+      pc = __popc(wm[0]) + __popc(wm[1]) + __popc(wm[2]) + __popc(wm[3]);
     }
+    int tot = pc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (tid < kTcBM && lane == 0) wsum[4 + warp] = tot;
+    __syncthreads();
+    const int n_el = wsum[4] + wsum[5] + wsum[6] + wsum[7];
+    const int need = (n_el + kFixThreads * kFixPer - 1) / (kFixThreads * kFixPer);
+    const int cpi = need <= 1 ? 1 : (need == 2 ? 2 : kFixCols);
+    const int cnt = (pc + cpi - 1) / cpi;
     int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -473,15 +609,22 @@ __global__ void __launch_bounds__(kFixThreads, 1)
     if (tid < kTcBM) {
       int pos = incl - cnt;
       for (int p = 0; p < warp; ++p) pos += wsum[p];
+      uint64_t item = 0;
+      int nc = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        uint32_t m = w[k];
+        uint32_t m = wm[k];
         while (m) {
           const int bit = __ffs(m) - 1;
           m &= m - 1;
-          list[pos++] = (uint16_t)((tid << 8) | (k * 32 + bit));
+          item |= (uint64_t)(k * 32 + bit) << (16 + 12 * nc);
+          if (++nc == cpi) {
+            items[pos++] = item | (uint64_t)tid | ((uint64_t)nc << 8);
+            item = 0, nc = 0;
+          }
         }
       }
+      if (nc) items[pos++] = item | (uint64_t)tid | ((uint64_t)nc << 8);
     }
     if (tid == 0) L.tile_mark[tile] = 0u;  // ready for the next launch
     __syncthreads();
@@ -493,8 +636,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)
     const int kbytes = jb.K * esz;
     const int nk = (kbytes + kBKBytes - 1) / kBKBytes;
     for (int e0 = 0; e0 < n; e0 += kFixThreads * kFixPer) {
-      // ---- prologue: fill the ring
-      if (tid == 0) {
+      if (tid == 0) {  // prologue: fill the ring
         for (int kb = 0; kb < min(kFixStages, nk); ++kb, ++ld) {
           const int s = ld % kFixStages;
           mbar_wait(&empty[s], ((ld / kFixStages) & 1) ^ 1);
@@ -503,64 +645,42 @@ __global__ void __launch_bounds__(kFixThreads, 1)
           tma_load_2d(sB + s * kBStage, &L.tmB, &full[s], jb.b_k0 + kb * bke, brow);
         }
       }
-      int er[kFixPer], ec[kFixPer];
-      float acc[kFixPer];
+      FixItem w[kFixPer];
 #pragma unroll
       for (int j = 0; j < kFixPer; ++j) {
         const int e = e0 + j * kFixThreads + tid;
-        const uint32_t rc = e < n ? list[e] : 0u;
-        er[j] = e < n ? (int)(rc >> 8) : -1;
-        ec[j] = (int)(rc & 0xFF);
-        acc[j] = 0.f;
-      }
-      for (int kb = 0; kb < nk; ++kb, ++it) {
-        const int s = it % kFixStages;
-        mbar_wait(&full[s], (it / kFixStages) & 1);
-        const uint8_t* a0 = sA + s * kAStage;
-        const uint8_t* b0 = sB + s * kBStage;
-        const int nu = min(8, (kbytes - kb * kBKBytes) / 16);
+        const uint64_t item = e < n ? items[e] : 0ull;
+        w[j].row = e < n ? (int)(item & 0xFF) : -1;
+        w[j].nc = (int)((item >> 8) & 0xFF);
+        bool ok = e < n && (ELEM == kTcE4M3 || fma_safe(L.a_norm[jb.a_row0 + mt * kTcBM + w[j].row]));
 #pragma unroll
-        for (int j = 0; j < kFixPer; ++j) {
-          if (er[j] < 0) continue;
-          const uint8_t* ar = a0 + er[j] * kBKBytes;
-          const uint8_t* br = b0 + ec[j] * kBKBytes;
-          const int ra = er[j] & 7, rb = ec[j] & 7;
-          float sacc = acc[j];
-#pragma unroll 2
-          for (int u = 0; u < nu; ++u) {
-            const uint4 av = *reinterpret_cast<const uint4*>(ar + ((u ^ ra) << 4));
-            const uint4 bv = *reinterpret_cast<const uint4*>(br + ((u ^ rb) << 4));
-            float x[vel], y[vel];
-            dec16<ELEM>(av, x);
-            dec16<ELEM>(bv, y);
-#pragma unroll
-            for (int t = 0; t < vel; ++t) sacc = __fadd_rn(sacc, __fmul_rn(x[t], y[t]));
-          }
-          acc[j] = sacc;
+        for (int c = 0; c < kFixCols; ++c) {
+          // missing columns of a short item repeat its first (results unused)
+          w[j].col[c] = c < w[j].nc ? (int)((item >> (16 + 12 * c)) & 0xFFF) : (int)((item >> 16) & 0xFFF);
+          w[j].acc[c] = 0.f;
+          if (ELEM == kTcBF16 && c < w[j].nc) ok = ok && fma_safe(jb.b_norm[nt * kTcBN + w[j].col[c]]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (tid == 0 && kb + kFixStages < nk) {
-          const int ss = ld % kFixStages;
-          mbar_wait(&empty[ss], ((ld / kFixStages) & 1) ^ 1);
-          mbar_expect_tx(&full[ss], kAStage + kBStage);
-          tma_load_2d(sA + ss * kAStage, &L.tmA, &full[ss], (kb + kFixStages) * bke, arow);
-          tma_load_2d(sB + ss * kBStage, &L.tmB, &full[ss], jb.b_k0 + (kb + kFixStages) * bke, brow);
-          ++ld;
-        }
+        w[j].fma = ok;
       }
+      if (cpi == 1) fix_round<ELEM, 1>(L, w, sA, sB, full, empty, nk, kbytes, arow, brow, jb.b_k0, ld, it);
+      else if (cpi == 2) fix_round<ELEM, 2>(L, w, sA, sB, full, empty, nk, kbytes, arow, brow, jb.b_k0, ld, it);
+      else fix_round<ELEM, kFixCols>(L, w, sA, sB, full, empty, nk, kbytes, arow, brow, jb.b_k0, ld, it);
 #pragma unroll
       for (int j = 0; j < kFixPer; ++j) {
-        if (er[j] < 0) continue;
-        float v = round_out(acc[j], jb.prec);
-        if (jb.epi == 1) {
-          if (jb.prec == 1 && L.gelu_lut) v = dec_bf16(L.gelu_lut[enc_bf16(v)]);
-          else v = round_out(gelu_ref(v), jb.prec);
+        if (w[j].row < 0) continue;
+#pragma unroll
+        for (int c = 0; c < kFixCols; ++c) {
+          if (c >= w[j].nc) continue;
+          float v = round_out(w[j].acc[c], jb.prec);
+          if (jb.epi == 1) {
+            if (jb.prec == 1 && L.gelu_lut) v = dec_bf16(L.gelu_lut[enc_bf16(v)]);
+            else v = round_out(gelu_ref(v), jb.prec);
+          }
+          store_out(jb, mt * kTcBM + w[j].row, nt * kTcBN + w[j].col[c], v);
         }
-        store_out(jb, mt * kTcBM + er[j], nt * kTcBN + ec[j], v);
       }
     }
-    __syncthreads();  // list reuse
+    __syncthreads();  // item list reuse
   }
 }
 
@@ -576,14 +696,20 @@ __global__ void rownorm_kernel(const uint8_t* A, int64_t lda, int elem, int rows
   if (r >= rows) return;
   const int lane = threadIdx.x & 31;
   float s = 0.f;
+  bool bad = false;  // a value whose products with the other operand may be inexact in FP32
   const uint8_t* p = A + (int64_t)r * lda;
   for (int k = lane; k < K; k += 32) {
     const float x = elem == kTcBF16 ? dec_bf16(reinterpret_cast<const uint16_t*>(p)[k0 + k])
                                     : dec_e4m3(p[k0 + k]);
     s = fmaf(x, x, s);
+    // BF16 x BF16: 16 significant bits; exact iff |a|,|b| in [2^-67, 2^64) (or 0)
+    const float ax = fabsf(x);
+    bad = bad || !(ax == 0.f || (ax >= 6.7762635780344027e-21f && ax < 1.8446744073709552e19f));
   }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) out[r] = sqrtf(s) * 1.0001f;  // tiny guard for the FP32 sum itself
+  bad = __any_sync(0xffffffffu, bad);
+  // tiny guard for the FP32 sum itself; the sign bit marks "not FMA-safe"
+  if (lane == 0) out[r] = (bad && elem == kTcBF16) ? -(sqrtf(s) * 1.0001f) : sqrtf(s) * 1.0001f;
 }
 
 __global__ void pack_t_kernel(const float* __restrict__ in, int K, int N, int ld_in, void* out,

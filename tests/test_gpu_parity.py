@@ -139,6 +139,47 @@ def test_forward_bitexact(cfg):
     e.close()
 
 
+# --- tensor-core GEMM with the exactness certificate + fixup -----------------------
+def _tc_gemm(elem, prec, epi, A, Bt):
+    lib = eng.load_library()
+    lib.cqg_diag_gemm_tc.argtypes = [C.c_int] * 6 + [C.c_void_p] * 5
+    M, K = A.shape
+    N = Bt.shape[0]
+    out, ex = np.empty((M, N), np.float32), np.empty((M, N), np.float32)
+    nf = np.zeros(1, np.uint32)
+    v = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    assert lib.cqg_diag_gemm_tc(elem, prec, epi, M, N, K, v(A), v(Bt), v(out), v(ex), v(nf)) == 0
+    return out, ex, int(nf[0])
+
+
+def _bf16_grid(x):
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+@pytest.mark.parametrize("K", [768, 3072])
+def test_tc_gemm_bitexact_incl_non_fma_rows(K):
+    """BF16 x BF16 on tcgen05 + certified fixup equals the sequential FP32 dot
+    (kernels.cpp:44-52) bit for bit, also for rows holding values whose products
+    are not exact in FP32 (|x| < 2^-67: the fixup then keeps fmul + fadd)."""
+    rng = np.random.RandomState(K)
+    M, N = 256, 256
+    A = _bf16_grid(rng.randn(M, K).astype(np.float32))
+    A[::7, ::5] = _bf16_grid(np.float32(3e-23) * rng.randn(len(range(0, M, 7)), len(range(0, K, 5))))
+    Bt = _bf16_grid((rng.rand(N, K).astype(np.float32) - 0.5) * 0.0288)
+    Bt[::11, ::3] = _bf16_grid(np.float32(2e-22) * rng.randn(len(range(0, N, 11)), len(range(0, K, 3))))
+    seq = np.zeros((M, N), np.float32)
+    for k in range(K):
+        seq = (seq + (A[:, k:k + 1] * Bt[:, k][None, :]).astype(np.float32)).astype(np.float32)
+    for epi in (0, 1):
+        out, ex, nf = _tc_gemm(1, 1, epi, A, Bt)
+        assert np.array_equal(bits(out), bits(ex)), epi
+        assert nf > 0
+        if epi == 0:
+            assert np.array_equal(bits(out), bits(_bf16_grid(seq)))
+
+
 # --- scores (patching.cpp:227-264) ------------------------------------------------
 def test_tiny_scores_match_reference_golden():
     w, ds = make(TINY, 101, 3, 7)
