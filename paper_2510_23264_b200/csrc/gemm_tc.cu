@@ -23,9 +23,9 @@ constexpr int kAStage = kTcBM * kBKBytes;  // 16 KB
 constexpr int kBStage = kTcBN * kBKBytes;  // 16 KB
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr size_t kStageFloats = 32 * 33;  // per epilogue warp store staging
+constexpr size_t kStageFloats = 32 * 36;  // per epilogue warp store staging
 constexpr size_t kSmemBytes =
-    1024 + (size_t)kStages * (kAStage + kBStage) + 256 + 8 * 32 * 33 * sizeof(float);
+    1024 + (size_t)kStages * (kAStage + kBStage) + 256 + kEpiWarps * kStageFloats * sizeof(float);
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -151,6 +151,27 @@ __device__ __forceinline__ void store_out(const TcJob& jb, int row, int col, flo
   }
 }
 
+// E4M3 round trip of two values with the paired hardware conversions
+// (F2FP.SATFINITE.E4M3 / F2FP.F16.E4M3 unpack); NaN -> 0x7F as enc_e4m3.
+__device__ __forceinline__ float2 round_e4m3x2(float a, float b) {
+  const __nv_fp8x2_storage_t p = __nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+  float2 f = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2(p, __NV_E4M3)));
+  const float qnan = dec_e4m3(0x7F);
+  if (a != a) f.x = qnan;
+  if (b != b) f.y = qnan;
+  return f;
+}
+
+template <int PREC>
+__device__ __forceinline__ void round_pair(float& a, float& b) {
+  if (PREC == 0) {
+    const float2 f = round_e4m3x2(a, b);
+    a = f.x, b = f.y;
+  } else if (PREC == 1) {
+    a = round_bf16(a), b = round_bf16(b);
+  }
+}
+
 // Epilogue of one tile for one warp: 32 TMEM lanes (rows) x 64 columns.
 template <int ELEM, int PREC, int EPI>
 __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb, int tile, int mt,
@@ -161,6 +182,8 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
   const float sk = sqrtf((float)jb.K);
   const float na = rvalid && L.a_norm ? fabsf(L.a_norm[jb.a_row0 + row]) : 0.f;
   const float ku = L.kappa * 5.9604644775390625e-08f * sk;
+  const int row0 = mt * kTcBM + q * 32;
+  const int nrow = min(32, jb.M - row0);
   uint32_t flagged[2];
 #pragma unroll
   for (int cc = 0; cc < 2; ++cc) {
@@ -169,99 +192,132 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
     tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
     uint32_t fl = 0;
     const int colb = nt * kTcBN + c0;
+    const int ncol = min(32, jb.N - colb);
     float v[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = 0.f;
-#define v_of(j) v[j]
-    // column norms: one coalesced load per lane, broadcast by shuffles
-    const float nb_l = (PREC != 2 && jb.b_norm && colb + lane < jb.N) ? fabsf(__ldg(jb.b_norm + colb + lane)) : 0.f;
-    if (colb < jb.N) {
+    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float nb = __shfl_sync(0xffffffffu, nb_l, j);
-        const int col = colb + j;
-        const float acc = __uint_as_float(r[j]);
-        v[j] = round_out(acc, PREC);
-        bool amb = !(acc == acc);
-        if (PREC != 2) {
+    for (int j = 0; j < 32; j += 2) round_pair<PREC>(v[j], v[j + 1]);
+    if (PREC != 2 && ncol > 0) {
+      // column norms: one coalesced load per lane, broadcast by shuffles
+      const float nb_l = (jb.b_norm && colb + lane < jb.N) ? fabsf(__ldg(jb.b_norm + colb + lane)) : 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        float lo[2], hi[2];
+        bool chk[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const float nb = __shfl_sync(0xffffffffu, nb_l, j + t);
+          const float acc = __uint_as_float(r[j + t]);
           // E4M3 x E4M3 products are multiples of 2^-18; if every partial sum
           // is below 2^6 (|s_k| <= ||a|| ||b||) all of them are exact in
           // FP32, so the reference's sequential sum is the exact sum and so is
           // the tensor-core sum: the rounding is certified without a fixup.
-          const bool exact = ELEM == kTcE4M3 && na * nb < 63.99f;
-          if (!exact) {
-            const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
-            amb = amb || !(round_out(acc - m, PREC) == round_out(acc + m, PREC));
-          }
+          chk[t] = !(ELEM == kTcE4M3 && na * nb < 63.99f);
+          const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
+          lo[t] = acc - m, hi[t] = acc + m;
+          if (!(acc == acc)) fl |= 1u << (j + t);
         }
-        if (amb && rvalid && col < jb.N) fl |= 1u << j;
+        if (chk[0] || chk[1]) {
+          round_pair<PREC>(lo[0], lo[1]);
+          round_pair<PREC>(hi[0], hi[1]);
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+            if (chk[t] && !(lo[t] == hi[t])) fl |= 1u << (j + t);
+        }
       }
-      if (EPI == 1) {
-        if (PREC == 1) {
-          uint16_t g[32];
+      if (!rvalid) fl = 0;
+      if (ncol < 32) fl &= (1u << ncol) - 1u;
+    }
+    if (EPI == 1 && ncol > 0) {
+      if (PREC == 1) {
+        uint16_t g[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) g[j] = __ldg(L.gelu_lut + enc_bf16(v[j]));
+        for (int j = 0; j < 32; ++j) g[j] = __ldg(L.gelu_lut + enc_bf16(v[j]));
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = dec_bf16(g[j]);
+        for (int j = 0; j < 32; ++j) v[j] = dec_bf16(g[j]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = round_out(gelu_ref(v[j]), PREC);
+      }
+    }
+    // Stores: the 32 x 32 block is transposed through a warp-private smem
+    // tile with 16-byte accesses (row pitch padded by 4 words: conflict-free),
+    // then written as whole row segments with 16-byte global stores.
+    if (ncol > 0) {
+      uint32_t* sw = reinterpret_cast<uint32_t*>(stage);
+      if (jb.out_f32) {
+        const bool vec = ncol == 32 && ((reinterpret_cast<uintptr_t>(jb.out_f32) & 15) == 0) && (jb.ldo & 3) == 0;
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(stage + lane * 36 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int rr = it * 4 + (lane >> 3), cw = (lane & 7) * 4;
+            if (rr < nrow)
+              *reinterpret_cast<float4*>(jb.out_f32 + (int64_t)(row0 + rr) * jb.ldo + colb + cw) =
+                  *reinterpret_cast<const float4*>(stage + rr * 36 + cw);
+          }
+          __syncwarp();
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = round_out(gelu_ref(v[j]), PREC);
+          for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = v[j];
+          __syncwarp();
+          float* dst = jb.out_f32 + (int64_t)row0 * jb.ldo + colb + lane;
+          for (int rr = 0; rr < nrow; ++rr)
+            if (lane < ncol) dst[(int64_t)rr * jb.ldo] = stage[rr * 33 + lane];
+          __syncwarp();
         }
-      }
-    }
-    // Stores are staged through a warp-private smem tile and written row by
-    // row, so every store instruction covers one contiguous row segment.
-    const int row0 = mt * kTcBM + q * 32;
-    const int ncol = min(32, jb.N - colb);
-    if (ncol > 0) {
-      if (jb.out_f32) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = v_of(j);
-        __syncwarp();
-        for (int r = 0; r < 32 && row0 + r < jb.M; ++r)
-          if (lane < ncol) jb.out_f32[(int64_t)(row0 + r) * jb.ldo + colb + lane] = stage[r * 33 + lane];
-        __syncwarp();
       }
       if (jb.out_pack) {
-        uint32_t* sw = reinterpret_cast<uint32_t*>(stage);
-        if (PREC == 1) {  // 16 words of bf16 pairs per row
+        constexpr int esz = PREC == 1 ? 2 : 1;
+        constexpr int words = 32 * esz / 4;  // per row: 16 (bf16) or 8 (e4m3)
+        constexpr int pitch = words + 4;
+        uint32_t pk[words];
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            sw[lane * 17 + j] = enc_bf16(v_of(2 * j)) | ((uint32_t)enc_bf16(v_of(2 * j + 1)) << 16);
+        for (int w = 0; w < words; ++w) {
+          if (PREC == 1)
+            pk[w] = enc_bf16(v[2 * w]) | ((uint32_t)enc_bf16(v[2 * w + 1]) << 16);
+          else
+            pk[w] = enc_e4m3(v[4 * w]) | ((uint32_t)enc_e4m3(v[4 * w + 1]) << 8) |
+                    ((uint32_t)enc_e4m3(v[4 * w + 2]) << 16) | ((uint32_t)enc_e4m3(v[4 * w + 3]) << 24);
+        }
+        uint8_t* base = reinterpret_cast<uint8_t*>(jb.out_pack);
+        const bool vec = ncol == 32 && ((reinterpret_cast<uintptr_t>(base) & 15) == 0) &&
+                         ((int64_t)jb.ldo * esz) % 16 == 0 && (colb * esz) % 16 == 0;
+        if (vec) {
+#pragma unroll
+          for (int w = 0; w < words; w += 4)
+            *reinterpret_cast<uint4*>(sw + lane * pitch + w) = make_uint4(pk[w], pk[w + 1], pk[w + 2], pk[w + 3]);
           __syncwarp();
-          const bool w32 = ncol == 32 && (((reinterpret_cast<uintptr_t>(jb.out_pack) >> 1) + colb) & 1) == 0 &&
-                           (jb.ldo & 1) == 0;
-          for (int r = 0; r < 32 && row0 + r < jb.M; ++r) {
-            uint16_t* dst = reinterpret_cast<uint16_t*>(jb.out_pack) + (int64_t)(row0 + r) * jb.ldo + colb;
-            if (w32) {
-              if (lane < 16) reinterpret_cast<uint32_t*>(dst)[lane] = sw[r * 17 + lane];
-            } else if (lane < ncol) {
-              dst[lane] = (uint16_t)(sw[r * 17 + lane / 2] >> (16 * (lane & 1)));
-            }
+          constexpr int lanes_per_row = words / 4;  // 4 (bf16) or 2 (e4m3)
+          constexpr int rows_per_it = 32 / lanes_per_row;
+#pragma unroll
+          for (int it = 0; it < 32 / rows_per_it; ++it) {
+            const int rr = it * rows_per_it + lane / lanes_per_row, cw = (lane % lanes_per_row) * 4;
+            if (rr < nrow)
+              *reinterpret_cast<uint4*>(base + ((int64_t)(row0 + rr) * jb.ldo + colb) * esz + cw * 4) =
+                  *reinterpret_cast<const uint4*>(sw + rr * pitch + cw);
           }
           __syncwarp();
-        } else {  // 8 words of E4M3 quads per row
+        } else {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            sw[lane * 9 + j] = enc_e4m3(v_of(4 * j)) | ((uint32_t)enc_e4m3(v_of(4 * j + 1)) << 8) |
-                               ((uint32_t)enc_e4m3(v_of(4 * j + 2)) << 16) |
-                               ((uint32_t)enc_e4m3(v_of(4 * j + 3)) << 24);
+          for (int w = 0; w < words; ++w) sw[lane * (words + 1) + w] = pk[w];
           __syncwarp();
-          const bool w32 = ncol == 32 && ((reinterpret_cast<uintptr_t>(jb.out_pack) + colb) & 3) == 0 &&
-                           (jb.ldo & 3) == 0;
-          for (int r = 0; r < 32 && row0 + r < jb.M; ++r) {
-            uint8_t* dst = reinterpret_cast<uint8_t*>(jb.out_pack) + (int64_t)(row0 + r) * jb.ldo + colb;
-            if (w32) {
-              if (lane < 8) reinterpret_cast<uint32_t*>(dst)[lane] = sw[r * 9 + lane];
-            } else if (lane < ncol) {
-              dst[lane] = (uint8_t)(sw[r * 9 + lane / 4] >> (8 * (lane & 3)));
+          for (int rr = 0; rr < nrow; ++rr) {
+            if (lane < ncol) {
+              const uint32_t wv = sw[rr * (words + 1) + lane * esz / 4];
+              const int64_t o = (int64_t)(row0 + rr) * jb.ldo + colb + lane;
+              if (PREC == 1) reinterpret_cast<uint16_t*>(base)[o] = (uint16_t)(wv >> (16 * (lane & 1)));
+              else base[o] = (uint8_t)(wv >> (8 * (lane & 3)));
             }
           }
           __syncwarp();
         }
       }
     }
-#undef v_of
     flagged[cc] = fl;
   }
   // Record the flagged bits of this warp's 32 x 64 part; the first part of a
@@ -286,8 +342,9 @@ template <int ELEM, int PREC, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ TcLaunch L, const TcJob* __restrict__ jobs) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-byte alignment by pointer arithmetic on the shared array itself, so
+  // the compiler keeps every derived access in the shared address space
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kAStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
@@ -550,8 +607,9 @@ template <int ELEM>
 __global__ void __launch_bounds__(kFixThreads, 1)
     gemm_fixup_kernel(const __grid_constant__ TcLaunch L, const TcJob* __restrict__ jobs) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-byte alignment by pointer arithmetic on the shared array itself, so
+  // the compiler keeps every derived access in the shared address space
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + kFixStages * kAStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + kFixStages * kBStage);

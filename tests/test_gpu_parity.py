@@ -180,6 +180,33 @@ def test_tc_gemm_bitexact_incl_non_fma_rows(K):
             assert np.array_equal(bits(out), bits(_bf16_grid(seq)))
 
 
+def _e4m3_grid(x):
+    from oracle.oracle import Port
+    p = Port(TINY, make(TINY)[0].mats)
+    p.lib.cqo_round_f8.restype = C.c_float
+    p.lib.cqo_round_f8.argtypes = [C.c_float]
+    f = np.ascontiguousarray(x, np.float32).ravel()
+    out = np.array([p.lib.cqo_round_f8(float(v)) for v in f], np.float32)
+    return out.reshape(x.shape)
+
+
+@pytest.mark.parametrize("K,scale", [(768, 0.02), (768, 4.0), (64, 8.0)])
+def test_tc_gemm_e4m3_bitexact(K, scale):
+    """E4M3 x E4M3 on tcgen05 (kind::f8f6f4): small norms are certified exact
+    outright, large ones go through the margin test and the fixup; both must
+    equal the reference's sequential dot (kernels.cpp:44-52) rounded to E4M3."""
+    rng = np.random.RandomState(K + int(scale))
+    M, N = 192, 160
+    A = _e4m3_grid(rng.randn(M, K).astype(np.float32) * scale)
+    Bt = _e4m3_grid((rng.rand(N, K).astype(np.float32) - 0.5) * scale)
+    seq = np.zeros((M, N), np.float32)
+    for k in range(K):
+        seq = (seq + (A[:, k:k + 1] * Bt[:, k][None, :]).astype(np.float32)).astype(np.float32)
+    out, ex, nf = _tc_gemm(0, 0, 0, A, Bt)
+    assert np.array_equal(bits(out), bits(ex))
+    assert np.array_equal(bits(out), bits(_e4m3_grid(seq)))
+
+
 # --- scores (patching.cpp:227-264) ------------------------------------------------
 def test_tiny_scores_match_reference_golden():
     w, ds = make(TINY, 101, 3, 7)
