@@ -206,6 +206,9 @@ def main(argv=None):
     ap.add_argument("--config", default="gpt2s", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--acdc", action="store_true", help="also time a full PAHQ-ACDC run")
+    ap.add_argument("--ncu", action="store_true",
+                    help="profiling mode: one untimed scoring step, no JSON line (for ncu "
+                         "launch lists; no number from it is a bench value)")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)
@@ -246,6 +249,10 @@ def main(argv=None):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    if args.ncu:
+        e.score_edges(mask, edges, pol, True, eng.LOSS)
+        print(f"ncu step: {passes_per_step} passes, {e.stats()['kernel_launches']} launches")
+        return
     for _ in range(args.warmup):
         e.score_edges(mask, edges, pol, True, eng.LOSS)
     barrier()
