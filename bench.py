@@ -226,6 +226,9 @@ def main(argv=None):
     lo, hi = shard_mod.item_block(rank, world, items)
     shard = ds.subset(list(range(lo, hi)))
     e = eng.Engine(w, device=local)
+    for kv in filter(None, os.environ.get("CQG_OPTS", "").split(",")):  # e.g. exact_x2=0
+        k, v = kv.split("=")
+        e.set_option(k, int(v))
     e.set_dataset(shard, eng.KL, lo, items)
     if world > 1:
         import torch
@@ -275,9 +278,16 @@ def main(argv=None):
     # (cqg_set_dataset) + mask/edge list H2D + per-edge scores D2H each step
     barrier()
     t0 = time.perf_counter()
+    e2e_parts = []
     for _ in range(args.steps):
+        t1 = time.perf_counter()
         e.set_dataset(shard, eng.KL, lo, items)
+        t2 = time.perf_counter()
         e.score_edges(mask, edges, pol, True, eng.LOSS)
+        st = e.stats()
+        e2e_parts.append({"set_dataset_s": t2 - t1, "score_wall_s": time.perf_counter() - t2,
+                          "score_device_s": st["ms_device"] / 1e3,
+                          "baseline_s": st.get("ms_baseline", 0) / 1e3})
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     h2d = shard.clean.nbytes + shard.corrupt.nbytes + shard.answer.nbytes + \
         shard.distractor.nbytes + mask.size + edges.size * 4
@@ -337,7 +347,8 @@ def main(argv=None):
                "data": "synthetic (random-init weights per support.hpp, IOI-shaped prompts)",
                "config": config_block(args), "clocks": clk.summary(),
                "e2e": {"value": passes_per_step * args.steps / e2e_s, "unit": "passes/s",
-                       "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+                       "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                       "parts": e2e_parts},
                "gpu_launches": int(launches), "wall_s": wall, "roofline": roofline,
                "cpu_baseline": cb, "passes_per_step": passes_per_step,
                "acdc_end_to_end": acdc}

@@ -539,7 +539,9 @@ struct Engine {
   bool tc_dims_ok(int K, int elem) const { return (K * (elem == kTcBF16 ? 2 : 1)) % 32 == 0; }
 
   void gemm_tc(int elem, const void* A, int64_t a_rows, int a_k, const PackedB& B,
-               std::vector<TcJob>& jobs, const char* name) {
+               std::vector<TcJob>& jobs, const char* name, const float* a_norm = nullptr,
+               const float* a_ss = nullptr, const uint32_t* a_bad = nullptr, float* out_ss = nullptr,
+               uint32_t* out_bad = nullptr) {
     if (jobs.empty()) return;
     const int esz = elem == kTcBF16 ? 2 : 1;
     TcLaunch L{};
@@ -560,12 +562,15 @@ struct Engine {
       launched();
     }
     L.gelu_lut = gelu_lut.as<uint16_t>();
-    float* an = scratch("tc_anorm", (size_t)a_rows);
-    {
+    L.out_ss = out_ss, L.out_bad = out_bad;
+    if (a_norm || a_ss) {  // produced by the kernel that wrote A (fused)
+      L.a_norm = a_norm, L.a_ss = a_ss, L.a_bad = a_bad;
+    } else {
+      float* an = scratch("tc_anorm", (size_t)a_rows);
       Prof pf(this, "rownorm", 0, (double)a_rows * a_k * esz);
       launch_rownorm(L.A, L.lda, elem, (int)a_rows, 0, a_k, an, st);
+      L.a_norm = an;
     }
-    L.a_norm = an;
     int total = 0;
     double flops = 0, bytes = 0;
     for (TcJob& j : jobs) {
@@ -660,10 +665,12 @@ struct Engine {
     float* xq = tc ? nullptr : scratch("h_xq", nu * SEG);
     uint8_t* xq8 = tc ? reinterpret_cast<uint8_t*>(scratch("h_xq8", nu * SEG / 4 + 1)) : nullptr;
     float* xln = scratch("h_xln", std::max(n_xln, 1) * SEG);
+    float* xnorm = tc ? scratch("h_xnorm", nu * RB) : nullptr;
     std::vector<LnJob> lj;
     for (size_t u = 0; u < nu; ++u)
       lj.push_back({uin[u], xln_of[u] >= 0 ? xln + xln_of[u] * SEG : nullptr,
-                    xq ? xq + u * SEG : nullptr, RB, D, xq8 ? xq8 + u * SEG : nullptr, 1});
+                    xq ? xq + u * SEG : nullptr, RB, D, xq8 ? xq8 + u * SEG : nullptr, 1,
+                    xnorm ? xnorm + u * RB : nullptr});
     const bool r4 = rtn4(p_low, P);  // (tc is off for Rtn4)
     ln(lj, g.mat(2, l), g.mat(3, l), r4 ? 2 : p_low);
     std::vector<RtnJob> rq;
@@ -721,7 +728,7 @@ struct Engine {
         gj.push_back(q);
       }
     }
-    if (tc) gemm_tc(kTcE4M3, xq8, (int64_t)nu * RB, D, *bq, tj, "qkv");
+    if (tc) gemm_tc(kTcE4M3, xq8, (int64_t)nu * RB, D, *bq, tj, "qkv", xnorm);
     gemm(gj, "gemm_qkv");
     rtn_act(rq, nb);
     rq.clear();
@@ -795,10 +802,11 @@ struct Engine {
       const int esz = elem == kTcBF16 ? 2 : 1;
       uint8_t* xqp = reinterpret_cast<uint8_t*>(scratch("m_xqp", jobs.size() * SEG * esz / 4 + 1));
       uint8_t* hidp = reinterpret_cast<uint8_t*>(scratch("m_hidp", jobs.size() * SEG * esz + 1));
+      float* xnorm = scratch("m_xnorm", jobs.size() * RB);
       std::vector<LnJob> lj;
       for (size_t j = 0; j < jobs.size(); ++j)
         lj.push_back({jobs[j].in + i_off, nullptr, nullptr, RB, i_ld, xqp + j * RB * D * esz,
-                      elem == kTcBF16 ? 2 : 1});
+                      elem == kTcBF16 ? 2 : 1, xnorm + j * RB});
       ln(lj, g.mat(8, l), g.mat(9, l), p);
       const PackedB& bi = packedB(2, l, elem, p, P.mode);
       const PackedB& bo = packedB(3, l, elem, p, P.mode);
@@ -814,8 +822,13 @@ struct Engine {
         b.out_f32 = jobs[j].out + i_off, b.ldo = i_ld, b.b_norm = bo.norm.as<float>(), b.prec = p;
         t2.push_back(b);
       }
-      gemm_tc(elem, xqp, (int64_t)jobs.size() * RB, D, bi, t1, "mlp_in");
-      gemm_tc(elem, hidp, (int64_t)jobs.size() * RB, 4 * D, bo, t2, "mlp_out");
+      // the W_in epilogue accumulates the hidden rows' norms for W_out's certificate
+      float* hss = scratch("m_hss", 2 * jobs.size() * RB);
+      uint32_t* hbad = reinterpret_cast<uint32_t*>(hss + jobs.size() * RB);
+      CK(cudaMemsetAsync(hss, 0, sizeof(float) * 2 * jobs.size() * RB, st));
+      gemm_tc(elem, xqp, (int64_t)jobs.size() * RB, D, bi, t1, "mlp_in", xnorm, nullptr, nullptr,
+              hss, hbad);
+      gemm_tc(elem, hidp, (int64_t)jobs.size() * RB, 4 * D, bo, t2, "mlp_out", nullptr, hss, hbad);
       return;
     }
     float* xq = scratch("m_xq", jobs.size() * SEG);
@@ -1733,6 +1746,7 @@ int cqg_set_option(cqg_ctx* ctx, const char* key, int64_t value) {
     if (!ctx || !key) throw Error(1, "null argument");
     std::string k(key);
     if (k == "exact") ctx->e->opt_exact = value;
+    else if (k == "exact_x2") cqg::g_exact_x2 = (int)value;
     else if (k == "profile") ctx->e->opt_profile = value;
     else if (k == "mem_budget") ctx->e->opt_mem_budget = value;
     else throw Error(1, "cqg_set_option: unknown key " + k);

@@ -128,6 +128,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// ||A row|| bound and FMA safety of A row r (rownorm_kernel's encoding, or
+// the sum of squares accumulated by the producing GEMM's epilogue)
+__device__ __forceinline__ float a_norm_of(const TcLaunch& L, int r) {
+  return L.a_ss ? sqrtf(L.a_ss[r]) * 1.0001f : fabsf(L.a_norm[r]);
+}
+__device__ __forceinline__ bool a_fma_safe(const TcLaunch& L, int r) {
+  return L.a_ss ? L.a_bad[r] == 0u : (__float_as_uint(L.a_norm[r]) >> 31) == 0;
+}
+
 __device__ __forceinline__ float round_out(float x, int prec) {
   return prec == 2 ? x : round_p(x, prec);
 }
@@ -180,7 +189,9 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
   const int row = mt * kTcBM + q * 32 + lane;
   const bool rvalid = row < jb.M;
   const float sk = sqrtf((float)jb.K);
-  const float na = rvalid && L.a_norm ? fabsf(L.a_norm[jb.a_row0 + row]) : 0.f;
+  const float na = rvalid && (L.a_norm || L.a_ss) ? a_norm_of(L, jb.a_row0 + row) : 0.f;
+  float oss = 0.f;  // sum of squares of this lane's stored outputs (out_ss)
+  bool obad = false;
   const float ku = L.kappa * 5.9604644775390625e-08f * sk;
   const int row0 = mt * kTcBM + q * 32;
   const int nrow = min(32, jb.M - row0);
@@ -240,6 +251,18 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = round_out(gelu_ref(v[j]), PREC);
       }
+    }
+    if (L.out_ss && ncol > 0 && rvalid) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < ncol) {
+          // a flagged element is recomputed later: bound |final| by the
+          // neighbouring rounding candidates (GELU is 1.13-Lipschitz)
+          const float vb = (fl >> j) & 1u ? fabsf(v[j]) + 0.02f * fabsf(__uint_as_float(r[j])) : v[j];
+          oss = fmaf(vb, vb, oss);
+          const float ax = fabsf(v[j]);
+          obad = obad || !(ax == 0.f || (ax >= 6.7762635780344027e-21f && ax < 1.8446744073709552e19f));
+        }
     }
     // Stores: the 32 x 32 block is transposed through a warp-private smem
     // tile with 16-byte accesses (row pitch padded by 4 words: conflict-free),
@@ -319,6 +342,10 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
       }
     }
     flagged[cc] = fl;
+  }
+  if (L.out_ss && rvalid) {
+    atomicAdd(L.out_ss + jb.a_row0 + row, oss);
+    if (obad) atomicOr(L.out_bad + jb.a_row0 + row, 1u);
   }
   // Record the flagged bits of this warp's 32 x 64 part; the first part of a
   // tile to flag anything lists the tile for the fixup kernel.
@@ -710,7 +737,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)
         const uint64_t item = e < n ? items[e] : 0ull;
         w[j].row = e < n ? (int)(item & 0xFF) : -1;
         w[j].nc = (int)((item >> 8) & 0xFF);
-        bool ok = e < n && (ELEM == kTcE4M3 || fma_safe(L.a_norm[jb.a_row0 + mt * kTcBM + w[j].row]));
+        bool ok = e < n && (ELEM == kTcE4M3 || a_fma_safe(L, jb.a_row0 + mt * kTcBM + w[j].row));
 #pragma unroll
         for (int c = 0; c < kFixCols; ++c) {
           // missing columns of a short item repeat its first (results unused)

@@ -41,7 +41,11 @@ struct TcLaunch {
   const uint8_t* A;  // global base of A, row pitch lda bytes
   const uint8_t* B;
   int64_t lda, ldb;  // bytes
-  const float* a_norm;  // [rows of A] ||A row||
+  const float* a_norm;  // [rows of A] ||A row|| (sign bit: row not FMA-safe), or null with a_ss
+  const float* a_ss;     // alternative: [rows of A] sum of squares and
+  const uint32_t* a_bad; //   nonzero where the row is not FMA-safe (written by a producer epilogue)
+  float* out_ss;         // producer side: accumulate the output rows' sums of squares (atomics)
+  uint32_t* out_bad;     //   and their not-FMA-safe flags (both zeroed before the launch)
   int elem;          // TcElem
   int prec, epi;     // launch-uniform output rounding / GELU epilogue (== every job's)
   int n_jobs, total_tiles;

@@ -13,6 +13,8 @@
 
 namespace cqg {
 
+int g_exact_x2 = 1;  // paired-FP32 big exact GEMM (option "exact_x2")
+
 // ---------------------------------------------------------------------------
 // K2a: fold (sum_inputs, model.cpp:537-552). HBM-bound, float4-vectorised.
 // ---------------------------------------------------------------------------
@@ -155,6 +157,14 @@ constexpr int kLnStages = 4;
 constexpr int kLnWarps = 4;
 constexpr int kLnTile = 32 * 33;
 
+// Row norm bookkeeping of a packed tensor-core operand row (as rownorm_kernel
+// in gemm_tc.cu): ||q|| * 1.0001 with the sign bit set when a BF16 value's
+// products may be inexact in FP32 (|q| outside [2^-67, 2^64) and nonzero).
+__device__ __forceinline__ bool bf16_fma_bad(float x) {
+  const float ax = fabsf(x);
+  return !(ax == 0.f || (ax >= 6.7762635780344027e-21f && ax < 1.8446744073709552e19f));
+}
+
 __global__ void __launch_bounds__(32 * kLnWarps) ln_warp_kernel(const LnJob* __restrict__ jobs,
                                                               const float* __restrict__ gamma,
                                                               const float* __restrict__ beta,
@@ -178,8 +188,12 @@ __global__ void __launch_bounds__(32 * kLnWarps) ln_warp_kernel(const LnJob* __r
       cp_async4(t + r * 33 + cl, j.in + (int64_t)(r0 + rr) * j.in_stride + c);
     }
   };
+  // vectorised normalisation pass: D and the row pitch in float4 units
+  const bool vec = (D & 3) == 0 && (j.in_stride & 3) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(j.in) & 15) == 0);
   float mean = 0.f, acc = 0.f, inv = 0.f;
-  for (int pass = 0; pass < 3; ++pass) {
+  const int npass = vec ? 2 : 3;
+  for (int pass = 0; pass < npass; ++pass) {
     acc = 0.f;
 #pragma unroll
     for (int p = 0; p < kLnStages - 1; ++p) {
@@ -232,6 +246,70 @@ __global__ void __launch_bounds__(32 * kLnWarps) ln_warp_kernel(const LnJob* __r
       acc = __fdiv_rn(acc, (float)D);  // mean /= d  |  var /= d
       if (pass == 0) mean = acc;
       else inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(acc, 1e-5f)));
+    }
+  }
+  if (!vec) {
+    if (j.xnorm) {  // scalar path: norms from the written outputs (rare shapes)
+      for (int r = 0; r < nr; ++r) {
+        float ss = 0.f;
+        bool bad = false;
+        for (int c = lane; c < D; c += 32) {
+          const int64_t o = (int64_t)(r0 + r) * D + c;
+          const float q = j.xq ? j.xq[o]
+                               : (j.pack == 2 ? dec_bf16(reinterpret_cast<const uint16_t*>(j.xqp)[o])
+                                              : dec_e4m3(reinterpret_cast<const uint8_t*>(j.xqp)[o]));
+          ss = fmaf(q, q, ss);
+          bad = bad || bf16_fma_bad(q);
+        }
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        bad = __any_sync(0xffffffffu, bad) && j.pack == 2;
+        if (lane == 0) j.xnorm[r0 + r] = bad ? -(sqrtf(ss) * 1.0001f) : sqrtf(ss) * 1.0001f;
+      }
+    }
+    return;
+  }
+  // pass 3, row-major: the warp walks its rows; lane owns float4 column groups
+  // lane, lane + 32, ... Same per-element arithmetic (kernels.cpp:155-160),
+  // 16-byte loads / stores, and the row norm of the rounded output for the
+  // tensor-core exactness certificate.
+  const int D4 = D >> 2;
+  for (int r = 0; r < nr; ++r) {
+    const float m_r = __shfl_sync(0xffffffffu, mean, r), i_r = __shfl_sync(0xffffffffu, inv, r);
+    const float4* xin = reinterpret_cast<const float4*>(j.in + (int64_t)(r0 + r) * j.in_stride);
+    const int64_t ob = (int64_t)(r0 + r) * D;
+    float ss = 0.f;
+    bool bad = false;
+    for (int c4 = lane; c4 < D4; c4 += 32) {
+      const float4 x = xin[c4];
+      const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c4);
+      const float4 bt = __ldg(reinterpret_cast<const float4*>(beta) + c4);
+      float y[4] = {x.x, x.y, x.z, x.w};
+      const float gg[4] = {gm.x, gm.y, gm.z, gm.w}, bb[4] = {bt.x, bt.y, bt.z, bt.w};
+      float qv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        y[k] = __fadd_rn(__fmul_rn(gg[k], __fmul_rn(__fsub_rn(y[k], m_r), i_r)), bb[k]);
+        qv[k] = round_p(y[k], prec);
+        ss = fmaf(qv[k], qv[k], ss);
+        bad = bad || bf16_fma_bad(qv[k]);
+      }
+      if (j.xln) reinterpret_cast<float4*>(j.xln + ob)[c4] = make_float4(y[0], y[1], y[2], y[3]);
+      if (j.xq) reinterpret_cast<float4*>(j.xq + ob)[c4] = make_float4(qv[0], qv[1], qv[2], qv[3]);
+      if (j.xqp) {
+        if (j.pack == 2)
+          reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(j.xqp) + ob)[c4] =
+              make_uint2(enc_bf16(qv[0]) | ((uint32_t)enc_bf16(qv[1]) << 16),
+                         enc_bf16(qv[2]) | ((uint32_t)enc_bf16(qv[3]) << 16));
+        else
+          reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(j.xqp) + ob)[c4] =
+              enc_e4m3(qv[0]) | ((uint32_t)enc_e4m3(qv[1]) << 8) | ((uint32_t)enc_e4m3(qv[2]) << 16) |
+              ((uint32_t)enc_e4m3(qv[3]) << 24);
+      }
+    }
+    if (j.xnorm) {
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      bad = __any_sync(0xffffffffu, bad) && j.pack == 2;
+      if (lane == 0) j.xnorm[r0 + r] = bad ? -(sqrtf(ss) * 1.0001f) : sqrtf(ss) * 1.0001f;
     }
   }
 }
@@ -426,10 +504,130 @@ __global__ void __launch_bounds__(256) gemm_exact_big_kernel(const GemmJob* __re
   }
 }
 
+// Paired-FP32 variant of the big-tile kernel (sm_100a FFMA2 / FADD2): each
+// instruction advances two output chains. The product is formed as
+// fma(a, b, z) with z = -0.0 supplied at run time, which is exactly fl(a*b)
+// (x + -0 == x for every x, including +0) and which ptxas cannot contract
+// with the following add (it would for mul.rn.f32x2 + add.rn.f32x2); the add
+// is add.rn.f32x2. Per output element the chain is therefore still
+// acc = fl(acc + fl(a*b)) in k order, bit-identical to dot_col
+// (kernels.cpp:44-52). A is staged in shared memory as broadcast pairs
+// (a, a) so that each 16-byte load feeds two rows.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+  return (f2_t)__float_as_uint(lo) | ((f2_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float f2_lo(f2_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2_hi(f2_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+
+__global__ void __launch_bounds__(256) gemm_exact_x2_kernel(const GemmJob* __restrict__ jobs,
+                                                            const int* __restrict__ tile_start,
+                                                            int n_jobs, float negz) {
+  int lo = 0, hi = n_jobs - 1;
+  const int t = blockIdx.x;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_start[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmJob jb = jobs[lo];
+  const int local = t - tile_start[lo];
+  const int tiles_m = (jb.M + kXBM - 1) / kXBM;
+  const int m0 = (local % tiles_m) * kXBM, n0 = (local / tiles_m) * kXBN;
+  __shared__ __align__(16) float2 As[2][kXBK][kXBM];  // (a, a) broadcast pairs
+  __shared__ __align__(16) float Bs[2][kXBK][kXBN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int a_r = tid >> 1, a_k = (tid & 1) * 4;
+  const int b_k = tid >> 5, b_n = (tid & 31) * 4;
+  const f2_t z2 = f2_pack(negz, negz);
+  float ra[4], rb[4];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gm = m0 + a_r, gk = k0 + a_k + i;
+      ra[i] = (gm < jb.M && gk < jb.K) ? jb.A[(int64_t)gm * jb.lda + gk] : 0.f;
+      const int gk2 = k0 + b_k, gn = n0 + b_n + i;
+      rb[i] = (gk2 < jb.K && gn < jb.N) ? jb.B[(int64_t)gk2 * jb.ldb + gn] : 0.f;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) As[buf][a_k + i][a_r] = make_float2(ra[i], ra[i]);
+    *reinterpret_cast<float4*>(&Bs[buf][b_k][b_n]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
+  };
+  // acc[i][p]: row i (ty*4 + i, then 64 + ty*4 + i - 4), column pair p
+  // (tx*4 + {0,1}, tx*4 + {2,3}, 64 + tx*4 + {0,1}, 64 + tx*4 + {2,3})
+  f2_t acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) acc[i][p] = 0ull;
+  load(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < jb.K; k0 += kXBK) {
+    const bool more = k0 + kXBK < jb.K;
+    if (more) load(k0 + kXBK);
+    const int kl = min(kXBK, jb.K - k0);
+    for (int kk = 0; kk < kl; ++kk) {
+      f2_t a[8], b[4];
+      {
+        const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][ty * 4]);
+        const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][ty * 4 + 2]);
+        const ulonglong2 a2 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][64 + ty * 4]);
+        const ulonglong2 a3 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][64 + ty * 4 + 2]);
+        a[0] = a0.x, a[1] = a0.y, a[2] = a1.x, a[3] = a1.y;
+        a[4] = a2.x, a[5] = a2.y, a[6] = a3.x, a[7] = a3.y;
+        const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(&Bs[buf][kk][tx * 4]);
+        const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(&Bs[buf][kk][64 + tx * 4]);
+        b[0] = b0.x, b[1] = b0.y, b[2] = b1.x, b[3] = b1.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) acc[i][p] = f2_add(acc[i][p], f2_fma(a[i], b[p], z2));
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int gm = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (gm >= jb.M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int gn = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (gn >= jb.N) continue;
+      const f2_t pr = acc[i][j >> 1];
+      float v = round_p((j & 1) ? f2_hi(pr) : f2_lo(pr), jb.prec);
+      if (jb.epi == 1) v = round_p(gelu_ref(v), jb.prec);
+      jb.C[(int64_t)gm * jb.ldc + gn] = v;
+    }
+  }
+}
+
 void launch_gemm_exact_big(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs,
                            int total_tiles, cudaStream_t st) {
   if (n_jobs <= 0 || total_tiles <= 0) return;
-  gemm_exact_big_kernel<<<total_tiles, 256, 0, st>>>(d_jobs, d_tile_start, n_jobs);
+  if (g_exact_x2)
+    gemm_exact_x2_kernel<<<total_tiles, 256, 0, st>>>(d_jobs, d_tile_start, n_jobs, -0.0f);
+  else
+    gemm_exact_big_kernel<<<total_tiles, 256, 0, st>>>(d_jobs, d_tile_start, n_jobs);
 }
 
 // ---------------------------------------------------------------------------
@@ -700,9 +898,81 @@ __global__ void kl_kernel(const float* __restrict__ logits, const float* __restr
   if (threadIdx.x == 0) out[r] = kl;
 }
 
+// One 512-thread CTA per patched row, two passes over the row (the second
+// from L2): an online max / sum-of-exp pass (one exp per element, NaN check),
+// then the KL pass. Same per-element arithmetic as the reference
+// (patching.cpp:108-135); only the double reduction order differs.
+constexpr int kKlThreads = 512;
+
+__device__ __forceinline__ void lse_merge(double& m, double& s, double m2, double s2) {
+  if (m2 > m) {
+    s = s * exp(m - m2) + s2;
+    m = m2;
+  } else if (m2 > -INFINITY) {
+    s += s2 * exp(m2 - m);
+  }
+}
+
+__global__ void __launch_bounds__(kKlThreads) kl_online_kernel(const float* __restrict__ logits,
+                                                               const float* __restrict__ base,
+                                                               const double* __restrict__ base_lse,
+                                                               const int* __restrict__ item_of, int V,
+                                                               double* out, int* nan_flag) {
+  __shared__ double shm[kKlThreads / 32], shs[kKlThreads / 32];
+  __shared__ double sh[32];
+  __shared__ int shi[32];
+  const int r = blockIdx.x;
+  const float* q = logits + (int64_t)r * V;
+  const int it = item_of[r];
+  const float* c = base + (int64_t)it * V;
+  int nan = 0;
+  double m = -INFINITY, s = 0.0;
+  for (int i = threadIdx.x; i < V; i += kKlThreads) {
+    const float f = q[i];
+    if (f != f) {
+      nan = 1;
+      continue;
+    }
+    const double x = (double)f;
+    if (x > m) {
+      s = s * exp(m - x) + 1.0;
+      m = x;
+    } else {
+      s += exp(x - m);
+    }
+  }
+  nan = block_reduce(nan, OrOp(), shi, 0);
+  if (nan) {  // NaN logits: the score is rejected by the host (patching.cpp:120-123)
+    if (threadIdx.x == 0) {
+      atomicOr(nan_flag, 1);
+      out[r] = 0.0;
+    }
+    return;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    lse_merge(m, s, m2, s2);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) shm[w] = m, shs[w] = s;
+  __syncthreads();
+  m = shm[0], s = shs[0];
+  for (int k = 1; k < kKlThreads / 32; ++k) lse_merge(m, s, shm[k], shs[k]);
+  const double lse_q = m + log(s), lse_c = base_lse[it];
+  double kl = 0.0;
+  for (int i = threadIdx.x; i < V; i += kKlThreads) {
+    const double lp = (double)__ldg(c + i) - lse_c;
+    const double lq = (double)q[i] - lse_q;
+    kl += exp(lp) * (lp - lq);
+  }
+  kl = block_reduce(kl, SumOp(), sh, 0.0);
+  if (threadIdx.x == 0) out[r] = kl;
+}
+
 void launch_kl(const float* logits, const float* base, const double* base_lse, const int* item_of,
                int rows, int V, double* out, int* nan_flag, cudaStream_t st) {
-  if (rows > 0) kl_kernel<<<rows, 256, 0, st>>>(logits, base, base_lse, item_of, V, out, nan_flag);
+  if (rows <= 0) return;
+  kl_online_kernel<<<rows, kKlThreads, 0, st>>>(logits, base, base_lse, item_of, V, out, nan_flag);
 }
 
 __global__ void logitdiff_kernel(const float* __restrict__ logits, const float* __restrict__ base,

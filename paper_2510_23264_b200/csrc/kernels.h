@@ -36,6 +36,7 @@ struct LnJob {
   int in_stride;
   void* xqp;        // packed copy of xq for the tensor cores (may be null)
   int pack;         // 1: E4M3 bytes, 2: BF16
+  float* xnorm;     // [rows] ||xq row|| * 1.0001 (sign: BF16 row not FMA-safe) (may be null)
 };
 void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float* gamma,
                       const float* beta, int D, int prec, cudaStream_t st);
@@ -57,6 +58,7 @@ int gemm_exact_tiles(int M, int N);
 void launch_gemm_exact_big(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs,
                            int total_tiles, cudaStream_t st);
 int gemm_exact_big_tiles(int M, int N);
+extern int g_exact_x2;  // 1: FFMA2/FADD2 variant of the big exact GEMM
 
 // ---- K5: causal attention (kernels.cpp:167-219) + z rounding ---------------
 struct AttnJob {

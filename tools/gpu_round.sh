@@ -14,6 +14,17 @@ tests)
 bench)
   timeout 1200 python bench.py --acdc > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench exit $?"
   cat gpurun_out/bench.json ;;
+mb)
+  ./tools/mb/f32x2.bin > gpurun_out/mb_f32x2.txt 2>&1; cat gpurun_out/mb_f32x2.txt ;;
+ab)  # A/B of an engine option: CQG_OPTS for the second run, e.g. AB=exact_x2=0
+  timeout 900 python bench.py --no-cpu --steps 2 --warmup 3 > gpurun_out/bench_a.json 2>&1
+  CQG_OPTS="$AB" timeout 900 python bench.py --no-cpu --steps 2 --warmup 3 > gpurun_out/bench_b.json 2>&1
+  python -c "
+import json
+for f in ['a','b']:
+    d=json.loads(open(f'gpurun_out/bench_{f}.json').read().strip().splitlines()[-1])
+    print(f, round(d['value']), {k: round(v['ms']) for k, v in sorted(d['roofline']['per_kernel'].items(), key=lambda kv: -kv[1]['ms'])[:8]})
+" ;;
 reference)
   timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref exit $?"
   cat gpurun_out/bench_ref.json ;;
