@@ -305,11 +305,12 @@ def main(argv=None):
     # per multiply-add, counted as 2 flops
     simt_peak = 148 * 128 * 1.965e9 / 1e12
     traffic = None
+    cls = name.split(":")[-1]  # "base:" = per-source baseline runs
     if p["flops"] > 0:
         ach = p["flops"] / (p["ms"] / 1e3) / 1e12
-        if name.startswith("gemm_tc_fp8"):
+        if cls.startswith("gemm_tc_fp8"):
             peak, unit, bound, psrc = 2 * bf16, "TFLOP/s", "tensor", f"2x {src} sustained bf16 (fp8 rate)"
-        elif name.startswith("gemm_tc"):
+        elif cls.startswith("gemm_tc"):
             peak, unit, bound, psrc = bf16, "TFLOP/s", "tensor", f"{src} sustained bf16"
         else:
             peak, unit, bound, psrc = simt_peak, "TFLOP/s", "fp32-simt", \

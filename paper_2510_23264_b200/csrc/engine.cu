@@ -234,7 +234,7 @@ void DeviceBuf::ensure(size_t n) {
 struct Run {  // one evaluation context (a baseline) over nb items
   int nb = 0;
   size_t seg = 0;  // floats per node activation
-  DeviceBuf out, trie, logits, lse;
+  DeviceBuf out, trie, logits, lse, prob;  // prob: [nb][V] exp(lp) of the last rows (KL)
   float* o(int n) const { return out.as<float>() + (size_t)n * seg; }
   float* t(int n) const { return trie.as<float>() + (size_t)n * seg; }
 };
@@ -354,15 +354,17 @@ struct Engine {
   };
   std::vector<Pending> pending;
   int64_t opt_profile = 0;
+  std::string prof_tag;  // "base:" while a baseline run is being computed
   struct Prof {  // RAII region around one launch
     Engine* e;
     Pending p;
     Prof(Engine* en, const char* name, double flops = 0, double bytes = 0) : e(en) {
       e->launched();
-      auto& k = e->kprof[name];
+      const std::string key = e->prof_tag + name;
+      auto& k = e->kprof[key];
       k.launches++, k.flops += flops, k.bytes += bytes;
       if (!e->opt_profile) return;
-      p.name = name, p.flops = flops, p.bytes = bytes;
+      p.name = key, p.flops = flops, p.bytes = bytes;
       cudaEventCreate(&p.a);
       cudaEventCreate(&p.b);
       cudaEventRecord(p.a, e->st);
@@ -948,6 +950,12 @@ struct Engine {
 
   void forward_run(Run& R, const Trie& T, const Policy& P, const int* d_tok, int sigma0,
                    bool all_rows, int* d_nan, bool loss_only = false) {
+    struct Tag {
+      std::string& t;
+      std::string old;
+      Tag(std::string& x) : t(x), old(x) { t = "base:"; }
+      ~Tag() { t = old; }
+    } tag(prof_tag);
     for (int s = sigma0; s < g.n_stages; ++s) {
       const auto& nodes = g.stage_nodes[s];
       if (nodes.empty()) continue;  // MLP stages of attention-only models
@@ -964,7 +972,10 @@ struct Engine {
       } else {
         run_unembed(P, {{input_of(T, R, g.unembed), R.logits.as<float>()}}, R.nb, all_rows);
         if (!all_rows) {
-          launch_lse(R.logits.as<float>(), R.nb, g.V, R.lse.as<double>(), d_nan, st);
+          const bool kl = metric == 0;
+          if (kl) R.prob.ensure((size_t)R.nb * g.V * 8);
+          launch_lse(R.logits.as<float>(), R.nb, g.V, R.lse.as<double>(), d_nan, st,
+                     kl ? R.prob.as<double>() : nullptr);
           launched();
         }
       }
@@ -1244,18 +1255,20 @@ struct Engine {
         const int rows = (int)unembed_edges.size() * nb;
         std::vector<int> item_of(rows);
         for (int r = 0; r < rows; ++r) item_of[r] = r % nb;
-        double* tmp = reinterpret_cast<double*>(scratch("p_kl", (size_t)rows * 2));
+        bool ident = true;  // every edge's logits computed, in plan order: write in place
+        for (size_t j = 0; j < unembed_edges.size(); ++j) ident = ident && unembed_edges[j] == (int)j;
+        double* tmp = ident ? d_d : reinterpret_cast<double*>(scratch("p_kl", (size_t)rows * 2));
         reserve(up_bytes(item_of.size(), sizeof(int)));
         {
           Prof pf(this, metric == 0 ? "kl" : "logitdiff", 0, (double)rows * V * 4.0 * 2.0);
           if (metric == 0)
             launch_kl(logits, R.logits.as<float>(), R.lse.as<double>(), upload(item_of), rows, V,
-                      tmp, d_nan, st);
+                      tmp, d_nan, st, R.prob.as<double>());
           else
             launch_logitdiff(logits, R.logits.as<float>(), upload(item_of), d_ans.as<int>(),
                              d_dis.as<int>(), rows, V, tmp, d_nan, st);
         }
-        for (size_t j = 0; j < unembed_edges.size(); ++j)
+        for (size_t j = 0; j < unembed_edges.size() && !ident; ++j)
           CK(cudaMemcpyAsync(d_d + (size_t)unembed_edges[j] * nb, tmp + j * nb, sizeof(double) * nb,
                              cudaMemcpyDeviceToDevice, st));
       }
@@ -1354,8 +1367,12 @@ struct Engine {
     forward_run(base_run, T, base, tokens(base_tok), 0, need_all_rows, d_nan, loss);
     double ms_base = 0, ms_pass = 0;
     std::vector<double> sums(n, 0.0);
-    std::vector<double> hd;
-    DeviceBuf& dd = *pool_buf("d_scores", 8);
+    // Per-(edge, item) terms of every group land in one device array (row r =
+    // the r-th scored edge); a single D2H at the end, so the host plans the
+    // next group while the GPU is still running this one (no per-group sync).
+    DeviceBuf& dd = *pool_buf("d_scores", sizeof(double) * (size_t)std::max(n, 1) * B);
+    std::vector<int> row_edge;  // row -> index into edge_ids
+    row_edge.reserve(n);
     for (int src : order) {
       const auto& idx = by_src[src];
       const Policy P = per_edge ? policy_for_edge(g, edge_ids[idx[0]], base) : base;
@@ -1366,7 +1383,7 @@ struct Engine {
       } else if (per_edge && src >= 0 && g.kind[src] == kEmbed) {
         forward_run(base_run, T, P, tokens(base_tok), 0, need_all_rows, d_nan, loss);
       }
-      CK(cudaStreamSynchronize(st));
+      if (opt_profile) CK(cudaStreamSynchronize(st));
       auto tp = std::chrono::steady_clock::now();
       ms_base += std::chrono::duration<double, std::milli>(tp - tb).count();
       // plans, batched under the memory budget
@@ -1390,22 +1407,25 @@ struct Engine {
         }
         std::vector<EdgePlan> batch;
         for (size_t k = k0; k < k1; ++k) batch.push_back(std::move(plans[ord[k]]));
-        dd.ensure(sizeof(double) * batch.size() * B);
-        run_passes(T, P, base_run, batch, loss, dd.as<double>(), d_nan);
-        hd.resize(batch.size() * B);
-        CK(cudaMemcpyAsync(hd.data(), dd.p, sizeof(double) * hd.size(), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        stats.d2h_bytes += (int64_t)(sizeof(double) * hd.size());
-        for (size_t k = k0; k < k1; ++k) {
-          double acc = 0.0;  // delta_l's sequential item sum (patching.cpp:229-238)
-          for (int i = 0; i < B; ++i) acc += hd[(k - k0) * B + i];
-          sums[idx[ord[k]]] = acc;
-        }
+        run_passes(T, P, base_run, batch, loss, dd.as<double>() + row_edge.size() * (size_t)B, d_nan);
+        for (size_t k = k0; k < k1; ++k) row_edge.push_back(idx[ord[k]]);
         stats.passes += (int64_t)(k1 - k0) * B;
         k0 = k1;
       }
+      if (opt_profile) CK(cudaStreamSynchronize(st));
       tb = std::chrono::steady_clock::now();
       ms_pass += std::chrono::duration<double, std::milli>(tb - tp).count();
+    }
+    {
+      std::vector<double> hd(row_edge.size() * (size_t)B);
+      CK(cudaMemcpyAsync(hd.data(), dd.p, sizeof(double) * hd.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      stats.d2h_bytes += (int64_t)(sizeof(double) * hd.size());
+      for (size_t r = 0; r < row_edge.size(); ++r) {
+        double acc = 0.0;  // delta_l's sequential item sum (patching.cpp:229-238)
+        for (int i = 0; i < B; ++i) acc += hd[r * B + i];
+        sums[row_edge[r]] = acc;
+      }
     }
     int h_nan = 0;
     CK(cudaMemcpyAsync(&h_nan, d_nan, 4, cudaMemcpyDeviceToHost, st));

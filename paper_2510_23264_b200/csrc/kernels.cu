@@ -314,9 +314,108 @@ __global__ void __launch_bounds__(32 * kLnWarps) ln_warp_kernel(const LnJob* __r
   }
 }
 
+// Latency-optimised variant for launches with few rows (the per-source
+// baseline runs: one segment of B*S rows per launch). Each warp owns RW rows
+// and stages them whole in shared memory (all loads in flight at once, odd
+// row pitch so the RW chain lanes hit distinct banks); lanes 0..RW-1 then run
+// the two sequential reductions at FADD latency and the whole warp normalises
+// row-major from shared memory (same arithmetic as ln_warp_kernel).
+constexpr int kLsWarps = 4;
+
+template <int RW>
+__global__ void __launch_bounds__(32 * kLsWarps) ln_small_kernel(const LnJob* __restrict__ jobs,
+                                                                 const float* __restrict__ gamma,
+                                                                 const float* __restrict__ beta,
+                                                                 int D, int prec) {
+  extern __shared__ float ls_sm[];
+  const LnJob j = jobs[blockIdx.y];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = (blockIdx.x * kLsWarps + warp) * RW;
+  if (r0 >= j.rows) return;
+  const int P = D | 1;
+  float* t = ls_sm + (size_t)warp * RW * P;
+  const int nr = min(RW, j.rows - r0);
+  for (int r = 0; r < nr; ++r) {
+    const float* src = j.in + (int64_t)(r0 + r) * j.in_stride;
+    for (int c = lane; c < D; c += 32) cp_async4(t + r * P + c, src + c);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  float mean = 0.f, inv = 0.f;
+  if (lane < nr) {
+    const float* row = t + lane * P;
+    float acc = 0.f;
+    for (int c = 0; c < D; ++c) acc = __fadd_rn(acc, row[c]);
+    mean = __fdiv_rn(acc, (float)D);
+    acc = 0.f;
+    for (int c = 0; c < D; ++c) {
+      const float d = __fsub_rn(row[c], mean);
+      acc = __fadd_rn(acc, __fmul_rn(d, d));
+    }
+    acc = __fdiv_rn(acc, (float)D);
+    inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(acc, 1e-5f)));
+  }
+  const int D4 = D >> 2;
+  for (int r = 0; r < nr; ++r) {
+    const float m_r = __shfl_sync(0xffffffffu, mean, r), i_r = __shfl_sync(0xffffffffu, inv, r);
+    const float* row = t + r * P;
+    const int64_t ob = (int64_t)(r0 + r) * D;
+    float ss = 0.f;
+    bool bad = false;
+    for (int c4 = lane; c4 < D4; c4 += 32) {
+      const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c4);
+      const float4 bt = __ldg(reinterpret_cast<const float4*>(beta) + c4);
+      const float gg[4] = {gm.x, gm.y, gm.z, gm.w}, bb[4] = {bt.x, bt.y, bt.z, bt.w};
+      float y[4], qv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        y[k] = __fadd_rn(__fmul_rn(gg[k], __fmul_rn(__fsub_rn(row[4 * c4 + k], m_r), i_r)), bb[k]);
+        qv[k] = round_p(y[k], prec);
+        ss = fmaf(qv[k], qv[k], ss);
+        bad = bad || bf16_fma_bad(qv[k]);
+      }
+      if (j.xln) reinterpret_cast<float4*>(j.xln + ob)[c4] = make_float4(y[0], y[1], y[2], y[3]);
+      if (j.xq) reinterpret_cast<float4*>(j.xq + ob)[c4] = make_float4(qv[0], qv[1], qv[2], qv[3]);
+      if (j.xqp) {
+        if (j.pack == 2)
+          reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(j.xqp) + ob)[c4] =
+              make_uint2(enc_bf16(qv[0]) | ((uint32_t)enc_bf16(qv[1]) << 16),
+                         enc_bf16(qv[2]) | ((uint32_t)enc_bf16(qv[3]) << 16));
+        else
+          reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(j.xqp) + ob)[c4] =
+              enc_e4m3(qv[0]) | ((uint32_t)enc_e4m3(qv[1]) << 8) | ((uint32_t)enc_e4m3(qv[2]) << 16) |
+              ((uint32_t)enc_e4m3(qv[3]) << 24);
+      }
+    }
+    if (j.xnorm) {
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      bad = __any_sync(0xffffffffu, bad) && j.pack == 2;
+      if (lane == 0) j.xnorm[r0 + r] = bad ? -(sqrtf(ss) * 1.0001f) : sqrtf(ss) * 1.0001f;
+    }
+  }
+}
+
 void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float* gamma,
                       const float* beta, int D, int prec, cudaStream_t st) {
   if (n_jobs <= 0 || max_rows <= 0) return;
+  // few rows: latency-bound, stage whole rows (RW rows per warp) in shared memory
+  if ((int64_t)max_rows * n_jobs <= 32768 && (D & 3) == 0 && D <= 2048) {
+    const int rw = D <= 1024 ? 8 : 4;
+    const size_t smem = sizeof(float) * kLsWarps * rw * (D | 1);
+    static bool attr_s = false;
+    if (!attr_s) {
+      cudaFuncSetAttribute(ln_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(ln_small_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr_s = true;
+    }
+    for (int y0 = 0; y0 < n_jobs; y0 += 65535) {
+      dim3 grid((max_rows + rw * kLsWarps - 1) / (rw * kLsWarps), (unsigned)std::min(65535, n_jobs - y0));
+      if (rw == 8) ln_small_kernel<8><<<grid, 32 * kLsWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
+      else ln_small_kernel<4><<<grid, 32 * kLsWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
+    }
+    return;
+  }
   const size_t smem = sizeof(float) * kLnWarps * kLnStages * kLnTile;
   static bool attr = false;
   if (!attr) {
@@ -866,15 +965,21 @@ __device__ double row_lse(const float* x, int V, int* nan_flag, double* sh, int*
   return mx + log(s);
 }
 
-__global__ void lse_kernel(const float* __restrict__ base, int V, double* lse, int* nan_flag) {
+__global__ void lse_kernel(const float* __restrict__ base, int V, double* lse, int* nan_flag,
+                           double* p_out) {
   __shared__ double sh[32];
   __shared__ int shi[32];
-  const double l = row_lse(base + (int64_t)blockIdx.x * V, V, nan_flag, sh, shi);
+  const float* x = base + (int64_t)blockIdx.x * V;
+  const double l = row_lse(x, V, nan_flag, sh, shi);
   if (threadIdx.x == 0) lse[blockIdx.x] = l;
+  if (p_out)  // the baseline distribution exp(lp), reused by every patched row
+    for (int i = threadIdx.x; i < V; i += blockDim.x)
+      p_out[(int64_t)blockIdx.x * V + i] = exp((double)x[i] - l);
 }
 
-void launch_lse(const float* base, int rows, int V, double* lse, int* nan_flag, cudaStream_t st) {
-  if (rows > 0) lse_kernel<<<rows, 256, 0, st>>>(base, V, lse, nan_flag);
+void launch_lse(const float* base, int rows, int V, double* lse, int* nan_flag, cudaStream_t st,
+                double* p_out) {
+  if (rows > 0) lse_kernel<<<rows, 256, 0, st>>>(base, V, lse, nan_flag, p_out);
 }
 
 __global__ void kl_kernel(const float* __restrict__ logits, const float* __restrict__ base,
@@ -917,7 +1022,8 @@ __global__ void __launch_bounds__(kKlThreads) kl_online_kernel(const float* __re
                                                                const float* __restrict__ base,
                                                                const double* __restrict__ base_lse,
                                                                const int* __restrict__ item_of, int V,
-                                                               double* out, int* nan_flag) {
+                                                               double* out, int* nan_flag,
+                                                               const double* __restrict__ base_p) {
   __shared__ double shm[kKlThreads / 32], shs[kKlThreads / 32];
   __shared__ double sh[32];
   __shared__ int shi[32];
@@ -960,19 +1066,21 @@ __global__ void __launch_bounds__(kKlThreads) kl_online_kernel(const float* __re
   for (int k = 1; k < kKlThreads / 32; ++k) lse_merge(m, s, shm[k], shs[k]);
   const double lse_q = m + log(s), lse_c = base_lse[it];
   double kl = 0.0;
+  const double* pc = base_p ? base_p + (int64_t)it * V : nullptr;
   for (int i = threadIdx.x; i < V; i += kKlThreads) {
     const double lp = (double)__ldg(c + i) - lse_c;
     const double lq = (double)q[i] - lse_q;
-    kl += exp(lp) * (lp - lq);
+    kl += (pc ? __ldg(pc + i) : exp(lp)) * (lp - lq);
   }
   kl = block_reduce(kl, SumOp(), sh, 0.0);
   if (threadIdx.x == 0) out[r] = kl;
 }
 
 void launch_kl(const float* logits, const float* base, const double* base_lse, const int* item_of,
-               int rows, int V, double* out, int* nan_flag, cudaStream_t st) {
+               int rows, int V, double* out, int* nan_flag, cudaStream_t st, const double* base_p) {
   if (rows <= 0) return;
-  kl_online_kernel<<<rows, kKlThreads, 0, st>>>(logits, base, base_lse, item_of, V, out, nan_flag);
+  kl_online_kernel<<<rows, kKlThreads, 0, st>>>(logits, base, base_lse, item_of, V, out, nan_flag,
+                                                base_p);
 }
 
 __global__ void logitdiff_kernel(const float* __restrict__ logits, const float* __restrict__ base,

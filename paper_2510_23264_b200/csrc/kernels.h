@@ -82,9 +82,12 @@ void launch_embed(const int* tokens, const float* we, const float* wpos, float* 
 // ---- K8: KL / logit-diff against the baseline (patching.cpp:108-161) -------
 // logits: [rows][V] (patched last rows), row r belongs to item item_of[r];
 // base: [B][V] baseline last-row logits; base_lse[B]. out[r] (double).
+// base_p (optional): [B][V] exp(base - lse) from launch_lse's p_out
 void launch_kl(const float* logits, const float* base, const double* base_lse, const int* item_of,
-               int rows, int V, double* out, int* nan_flag, cudaStream_t st);
-void launch_lse(const float* base, int rows, int V, double* lse, int* nan_flag, cudaStream_t st);
+               int rows, int V, double* out, int* nan_flag, cudaStream_t st,
+               const double* base_p = nullptr);
+void launch_lse(const float* base, int rows, int V, double* lse, int* nan_flag, cudaStream_t st,
+                double* p_out = nullptr);
 void launch_logitdiff(const float* logits, const float* base, const int* item_of,
                       const int* answer, const int* distractor, int rows, int V, double* out,
                       int* nan_flag, cudaStream_t st);
