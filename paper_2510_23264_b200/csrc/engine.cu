@@ -235,6 +235,7 @@ struct Run {  // one evaluation context (a baseline) over nb items
   int nb = 0;
   size_t seg = 0;  // floats per node activation
   DeviceBuf out, trie, logits, lse, prob;  // prob: [nb][V] exp(lp) of the last rows (KL)
+  std::vector<int8_t> otype;                // OutType of each node's output in `out`
   float* o(int n) const { return out.as<float>() + (size_t)n * seg; }
   float* t(int n) const { return trie.as<float>() + (size_t)n * seg; }
 };
@@ -243,10 +244,12 @@ struct HeadIO {
   const float* in;
   int head;
   float* out;
+  int otype;  // OutType the output is stored as
 };
 struct SegIO {
   const float* in;
   float* out;
+  int otype;
 };
 
 struct Engine {
@@ -280,6 +283,7 @@ struct Engine {
   // stats/options
   cqg_stats stats{};
   int64_t opt_exact = 0;
+  int64_t opt_packed = 1;  // store E4M3/BF16-rounded node outputs as their codes
   int64_t opt_mem_budget = 0;
 
   Engine(const cqg_config& c) : g(c) {}
@@ -628,6 +632,26 @@ struct Engine {
     launched();
   }
 
+  // Storage type of node w's output under policy P when the caller accepts
+  // packed outputs: the tensor-core W_O (low-precision heads outside the
+  // target's layer) and W_out (BF16 / E4M3 MLP) epilogues write the codes.
+  int out_type(const Policy& P, int w) const {
+    if (opt_exact || !opt_packed) return kOutF32;
+    const int k = g.kind[w], l = g.layer[w];
+    if (k == kHead) {
+      const bool tc = P.att == 0 && P.mode == 0 && tc_dims_ok(g.D, kTcE4M3) && tc_dims_ok(g.dk, kTcE4M3);
+      return tc && P.wo_precision(l) == 0 ? kOutE4M3 : kOutF32;
+    }
+    if (k == kMlp) {
+      const int p = P.precision_of(g, w);
+      const int elem = p == 1 ? kTcBF16 : kTcE4M3;
+      const bool tc = (p == 1 || (p == 0 && P.mode == 0)) && tc_dims_ok(g.D, elem) &&
+                      tc_dims_ok(4 * g.D, elem);
+      return tc ? (p == 1 ? kOutBF16 : kOutE4M3) : kOutF32;
+    }
+    return kOutF32;
+  }
+
   // ---- node computations ----------------------------------------------------
   // attention layer (model.cpp:622-718) for a list of (input, head, output)
   // last_only: only row S-1 of each item is consumed downstream (the final
@@ -765,7 +789,9 @@ struct Engine {
         const int h = jobs[j].head;
         TcJob t{};
         t.a_row0 = (int)j * ZR, t.b_row0 = 0, t.b_k0 = h * dk, t.M = ZR, t.N = D, t.K = dk;
-        t.out_f32 = jobs[j].out + o_off, t.ldo = o_ld, t.b_norm = bo.norm.as<float>() + (size_t)h * D;
+        if (jobs[j].otype == kOutE4M3) t.out_pack = reinterpret_cast<uint8_t*>(jobs[j].out) + o_off;
+        else t.out_f32 = jobs[j].out + o_off;
+        t.ldo = o_ld, t.b_norm = bo.norm.as<float>() + (size_t)h * D;
         t.prec = p_low;
         tj.push_back(t);
       }
@@ -773,6 +799,7 @@ struct Engine {
     } else {
       const float* wo = W(g.mat(7, l), wo_prec, P.mode);
       for (size_t j = 0; j < jobs.size(); ++j) {
+        if (jobs[j].otype != kOutF32) throw Error(2, "internal: packed head output on the exact W_O path");
         const int h = jobs[j].head;
         const bool target = P.th_l == l && P.th_h == h;
         GemmJob o{};
@@ -821,7 +848,14 @@ struct Engine {
         t1.push_back(a);
         TcJob b{};
         b.a_row0 = (int)j * RB, b.M = RB, b.N = D, b.K = 4 * D;
-        b.out_f32 = jobs[j].out + i_off, b.ldo = i_ld, b.b_norm = bo.norm.as<float>(), b.prec = p;
+        if (jobs[j].otype != kOutF32) {
+          if (jobs[j].otype != (elem == kTcBF16 ? kOutBF16 : kOutE4M3))
+            throw Error(2, "internal: MLP output type does not match its precision");
+          b.out_pack = reinterpret_cast<uint8_t*>(jobs[j].out) + i_off * esz;
+        } else {
+          b.out_f32 = jobs[j].out + i_off;
+        }
+        b.ldo = i_ld, b.b_norm = bo.norm.as<float>(), b.prec = p;
         t2.push_back(b);
       }
       // the W_in epilogue accumulates the hidden rows' norms for W_out's certificate
@@ -833,6 +867,8 @@ struct Engine {
       gemm_tc(elem, hidp, (int64_t)jobs.size() * RB, 4 * D, bo, t2, "mlp_out", nullptr, hss, hbad);
       return;
     }
+    for (const SegIO& j : jobs)
+      if (j.otype != kOutF32) throw Error(2, "internal: packed MLP output on the exact path");
     float* xq = scratch("m_xq", jobs.size() * SEG);
     float* hid = scratch("m_hid", jobs.size() * SEG * 4);
     std::vector<LnJob> lj;
@@ -935,6 +971,7 @@ struct Engine {
     R.trie.ensure((size_t)T.size() * R.seg * 4);
     R.logits.ensure((size_t)(all_rows ? nb * g.S : nb) * g.V * 4);
     R.lse.ensure((size_t)nb * 8);
+    R.otype.assign(g.N, kOutF32);
   }
 
   const float* input_of(const Trie& T, const Run& R, int w) {
@@ -962,12 +999,17 @@ struct Engine {
       const int k = g.kind[nodes[0]];
       if (k == kEmbed) {
         run_embed(P, d_tok, R.o(0), R.nb);
+        R.otype[0] = kOutF32;
       } else if (k == kHead) {
         std::vector<HeadIO> hj;
-        for (int w : nodes) hj.push_back({input_of(T, R, w), g.head[w], R.o(w)});
+        for (int w : nodes) {
+          R.otype[w] = (int8_t)out_type(P, w);
+          hj.push_back({input_of(T, R, w), g.head[w], R.o(w), R.otype[w]});
+        }
         run_heads(g.layer[nodes[0]], P, hj, R.nb, last_rows(g.layer[nodes[0]], P, loss_only));
       } else if (k == kMlp) {
-        run_mlp(g.layer[nodes[0]], P, {{input_of(T, R, nodes[0]), R.o(nodes[0])}}, R.nb,
+        R.otype[nodes[0]] = (int8_t)out_type(P, nodes[0]);
+        run_mlp(g.layer[nodes[0]], P, {{input_of(T, R, nodes[0]), R.o(nodes[0]), R.otype[nodes[0]]}}, R.nb,
                 last_rows(g.layer[nodes[0]], P, loss_only));
       } else {
         run_unembed(P, {{input_of(T, R, g.unembed), R.logits.as<float>()}}, R.nb, all_rows);
@@ -986,7 +1028,7 @@ struct Engine {
         const int p = T.parent[t];
         const float* a = p == 0 ? nullptr : R.t(p);
         if (a && a == prev) a = CQG_REG_PREV;
-        ops.push_back({a, R.o(T.src[t]), R.t(t)});
+        ops.push_back({a, R.o(T.src[t]), R.t(t), R.otype[T.src[t]]});
         prev = R.t(t);
       }
       if (!ops.empty()) fold(ops, {{0, (int)ops.size()}}, R.seg);
@@ -1007,15 +1049,19 @@ struct Engine {
   }
 
   // out[s] of the full-graph run under policy_for_edge (target = s)
-  const float* patch_value(int s, const Policy& ps, bool per_edge) {
-    if (!per_edge || g.kind[s] == kEmbed) return patch_run.o(s);
+  const float* patch_value(int s, const Policy& ps, bool per_edge, int* otype) {
+    if (!per_edge || g.kind[s] == kEmbed) {
+      *otype = patch_run.otype[s];
+      return patch_run.o(s);
+    }
+    *otype = out_type(ps, s);
     auto& c = target_cache[s];
     if (c) return c->as<float>();
     c = std::make_unique<DeviceBuf>();
     c->ensure(patch_run.seg * 4);
     const float* in = input_of(full, patch_run, s);
-    if (g.kind[s] == kHead) run_heads(g.layer[s], ps, {{in, g.head[s], c->as<float>()}}, B);
-    else run_mlp(g.layer[s], ps, {{in, c->as<float>()}}, B);
+    if (g.kind[s] == kHead) run_heads(g.layer[s], ps, {{in, g.head[s], c->as<float>(), *otype}}, B);
+    else run_mlp(g.layer[s], ps, {{in, c->as<float>(), *otype}}, B);
     return c->as<float>();
   }
 
@@ -1023,6 +1069,7 @@ struct Engine {
   struct EdgePlan {
     int e, s, v, sv;
     const float* pv;
+    int pvt;  // OutType of pv
     std::vector<int8_t> nchg, tchg, virt;
     std::vector<int> nslot, tslot;
     int n_slots = 0;
@@ -1152,7 +1199,8 @@ struct Engine {
           if (i == k) a = T.parent[t] == 0 ? nullptr : R.t(T.parent[t]);
           else a = CQG_REG_PREV;
           const float* bsrc = (i == k) ? p.pv : R.o(T.src[t]);
-          ops.push_back({a, bsrc, i + 1 == path.size() ? p.sval() : nullptr});
+          ops.push_back({a, bsrc, i + 1 == path.size() ? p.sval() : nullptr,
+                         (i == k) ? p.pvt : (int)R.otype[T.src[t]]});
         }
         progs.push_back({b, (int)ops.size()});
       }
@@ -1176,11 +1224,11 @@ struct Engine {
         for (int w : nodes) {
           if (!p.nchg[w]) continue;
           const float* in = (w == p.v) ? p.sval() : p.slot(p.tslot[T.rec_in[w]], SEG);
-          if (k == kHead) hj.push_back({in, g.head[w], p.slot(p.nslot[w], SEG)});
-          else if (k == kMlp) mj.push_back({in, p.slot(p.nslot[w], SEG)});
+          if (k == kHead) hj.push_back({in, g.head[w], p.slot(p.nslot[w], SEG), out_type(P, w)});
+          else if (k == kMlp) mj.push_back({in, p.slot(p.nslot[w], SEG), out_type(P, w)});
           else if (k == kUnembed) {
             uj.push_back((int)pi);
-            mj.push_back({in, nullptr});
+            mj.push_back({in, nullptr, kOutF32});
           }
         }
       }
@@ -1208,8 +1256,14 @@ struct Engine {
               r.b = R.logits.as<float>() + i * n;
               r.n = (int64_t)n;
             } else {
-              r.a = p.slot(p.nslot[p.v], SEG) + (size_t)i * g.S * g.D;
-              r.b = R.o(p.v) + (size_t)i * g.S * g.D;
+              const int ta = out_type(P, p.v), tb = R.otype[p.v];
+              const size_t off = (size_t)i * g.S * g.D;  // elements
+              auto at = [&](const float* base, int t) {
+                return reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(base) +
+                                                      off * (t == kOutF32 ? 4 : t == kOutBF16 ? 2 : 1));
+              };
+              r.a = at(p.slot(p.nslot[p.v], SEG), ta), r.atype = ta;
+              r.b = at(R.o(p.v), tb), r.btype = tb;
               r.n = (int64_t)g.S * g.D;
             }
             r.out = d_d + pi * nb + i;
@@ -1240,8 +1294,9 @@ struct Engine {
           if (a != nullptr && a != CQG_REG_PREV && a == prev) a = CQG_REG_PREV;
           const int sn = T.src[t];
           const float* bsrc = p.nchg[sn] ? p.slot(p.nslot[sn], SEG) : R.o(sn);
+          const int bt = p.nchg[sn] ? out_type(P, sn) : (int)R.otype[sn];
           float* dst = p.virt[t] ? nullptr : p.slot(p.tslot[t], SEG);
-          ops.push_back({a, bsrc, dst});
+          ops.push_back({a, bsrc, dst, bt});
           prev = dst;
         }
         if ((int)ops.size() > b) progs.push_back({b, (int)ops.size()});
@@ -1391,7 +1446,7 @@ struct Engine {
       for (size_t k = 0; k < idx.size(); ++k) {
         const int e = edge_ids[idx[k]];
         plans[k].e = e, plans[k].s = g.esrc[e], plans[k].v = g.edst[e], plans[k].sv = g.stage[g.edst[e]];
-        plans[k].pv = patch_value(plans[k].s, policy_for_edge(g, e, base), per_edge);
+        plans[k].pv = patch_value(plans[k].s, policy_for_edge(g, e, base), per_edge, &plans[k].pvt);
         plan_edge(plans[k], T, loss);
       }
       std::vector<size_t> ord(idx.size());
@@ -1766,6 +1821,7 @@ int cqg_set_option(cqg_ctx* ctx, const char* key, int64_t value) {
     if (!ctx || !key) throw Error(1, "null argument");
     std::string k(key);
     if (k == "exact") ctx->e->opt_exact = value;
+    else if (k == "packed") ctx->e->opt_packed = value;
     else if (k == "exact_x2") cqg::g_exact_x2 = (int)value;
     else if (k == "profile") ctx->e->opt_profile = value;
     else if (k == "mem_budget") ctx->e->opt_mem_budget = value;

@@ -22,10 +22,24 @@ constexpr int kBKBytes = 128;  // one SW128 atom row
 constexpr int kAStage = kTcBM * kBKBytes;  // 16 KB
 constexpr int kBStage = kTcBN * kBKBytes;  // 16 KB
 constexpr int kEpiWarps = 8;
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kEpiWarp0 = 3;  // warps: 0 TMA, 1 MMA, 2 tile metadata, 3.. epilogue
+constexpr int kThreads = 32 * kEpiWarp0 + 32 * kEpiWarps;
 constexpr size_t kStageFloats = 32 * 36;  // per epilogue warp store staging
-constexpr size_t kSmemBytes =
-    1024 + (size_t)kStages * (kAStage + kBStage) + 256 + kEpiWarps * kStageFloats * sizeof(float);
+
+// Per-tile metadata staged in shared memory by the metadata warp one TMEM
+// buffer ahead of the epilogue (job lookup, row / column norms), so the
+// epilogue warps never wait on dependent global loads.
+struct TileMeta {
+  TcJob jb;
+  int mt, nt;
+  alignas(16) float na[kTcBM];  // ||A row|| bound per tile row (0 outside the job)
+  alignas(16) float nb[kTcBN];  // ||B row|| per tile column (0 outside the job)
+  float nbmax[kTcBN / 32];       // max of nb over each 32-column chunk
+};
+constexpr size_t kMetaBytes = (sizeof(TileMeta) + 15) & ~size_t(15);
+constexpr size_t kSmemBytes = 1024 + (size_t)kStages * (kAStage + kBStage) + 256 +
+                              kEpiWarps * kStageFloats * sizeof(float) + 2 * kMetaBytes +
+                              2 * 2 * 13 * 128;  // GELU LUT slice (kGeluSm uint16)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -181,15 +195,65 @@ __device__ __forceinline__ void round_pair(float& a, float& b) {
   }
 }
 
+// Paired E4M3 codes of (a, b) (cvt.rn.satfinite.e4m3x2; reference NaN code 0x7F)
+__device__ __forceinline__ uint32_t e4m3x2_code(float a, float b) {
+  uint32_t c = (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+  if (a != a) c = (c & 0xFF00u) | 0x7Fu;
+  if (b != b) c = (c & 0x00FFu) | 0x7F00u;
+  return c;
+}
+__device__ __forceinline__ float2 e4m3x2_value(uint32_t c) {
+  return __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)c, __NV_E4M3)));
+}
+
+// BF16 certificate in integer form: the reference's value lies in
+// [acc - m, acc + m]; its RNE rounding to BF16 can differ from acc's only if
+// that interval reaches the rounding midpoint nearest to acc, i.e. if the
+// distance from acc's discarded 16 bits to 0x8000 (in units of acc's FP32
+// ulp, 2^(E-150)) is at most m / ulp. Binade edges cannot matter because m is
+// far below a BF16 ulp. Non-finite, tiny (|acc| < 2^-95) or NaN-margin
+// elements are always flagged.
+__device__ __forceinline__ bool bf16_ambiguous(float acc, float m) {
+  // branch-free: |acc| minus its BF16 truncation is exact in FP32; its
+  // distance to half a BF16 ulp (2^(e-8)) is the distance to the midpoint
+  const uint32_t ab = __float_as_uint(acc) & 0x7FFFFFFFu;
+  const float dl = __uint_as_float(ab) - __uint_as_float(ab & 0xFFFF0000u);
+  const float h = __uint_as_float((ab & 0x7F800000u) - (8u << 23));  // 2^(e-8)
+  const bool odd = ab >= 0x7F800000u || ab < (32u << 23);
+  return odd | !(fabsf(dl - h) > m * 1.001f);  // (covers the FP32 rounding of m)
+}
+
+// round_bf16 of a GELU input's code through the shared-memory slice of the
+// LUT (|x| in [2^-10, 8), both signs) and the closed forms outside it
+// (checked against the full table for all 2^16 codes): x >= 8 -> x,
+// x <= -8 -> -0, |x| < 2^-10 -> round_bf16(0.5 x); Inf / NaN via the table.
+constexpr int kGeluE0 = 117, kGeluNE = 13;
+constexpr int kGeluSm = 2 * kGeluNE * 128;
+__device__ __forceinline__ uint32_t gelu_code(uint32_t c, const uint16_t* lut_s, const uint16_t* lut_g) {
+  const uint32_t E = (c >> 7) & 0xFFu;
+  const uint32_t t = E - kGeluE0;
+  const bool in = t < (uint32_t)kGeluNE;
+  const uint32_t g = lut_s[in ? (c >> 15) * (kGeluNE * 128) + (c & 0x7FFFu) - kGeluE0 * 128 : 0];
+  // |x| < 2^-10: round_bf16(0.5 x) (x is a BF16 value, 0.5 x is exact in FP32)
+  const uint32_t hb = __float_as_uint(0.5f * __uint_as_float(c << 16));
+  const uint32_t half = (hb + 0x7FFFu + ((hb >> 16) & 1u)) >> 16;
+  const uint32_t big = (c & 0x8000u) ? 0x8000u : c;  // x >= 8 -> x, x <= -8 -> -0
+  uint32_t r = in ? g : (E > kGeluE0 ? big : half);
+  if (E == 255u) r = __ldg(lut_g + c);  // Inf / NaN (rare)
+  return r;
+}
+
 // Epilogue of one tile for one warp: 32 TMEM lanes (rows) x 64 columns.
 template <int ELEM, int PREC, int EPI>
-__device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb, int tile, int mt,
-                                              int nt, uint32_t tacc, int q, int half, int lane,
-                                              float* stage) {
+__device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TileMeta& md, int tile,
+                                              uint32_t tacc, int q, int half, int lane, float* stage,
+                                              const uint16_t* gelu_s) {
+  const TcJob& jb = md.jb;
+  const int mt = md.mt, nt = md.nt;
   const int row = mt * kTcBM + q * 32 + lane;
   const bool rvalid = row < jb.M;
   const float sk = sqrtf((float)jb.K);
-  const float na = rvalid && (L.a_norm || L.a_ss) ? a_norm_of(L, jb.a_row0 + row) : 0.f;
+  const float na = md.na[q * 32 + lane];
   float oss = 0.f;  // sum of squares of this lane's stored outputs (out_ss)
   bool obad = false;
   const float ku = L.kappa * 5.9604644775390625e-08f * sk;
@@ -205,64 +269,111 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
     const int colb = nt * kTcBN + c0;
     const int ncol = min(32, jb.N - colb);
     float v[32];
+    uint32_t e8[8];  // E4M3 codes (PREC 0 fast path), 4 per word
+    bool have_codes = false;
+    // E4M3 x E4M3 products are multiples of 2^-18; if every partial sum is
+    // below 2^6 (|s_k| <= ||a|| ||b||) all of them are exact in FP32, so the
+    // reference's sequential sum is the exact sum and so is the tensor-core
+    // sum: the rounding is certified without a fixup. Checked for the whole
+    // warp chunk at once (uniform branch) with the chunk's largest column norm.
+    const bool cert_all = ELEM == kTcE4M3 && PREC == 0 &&
+                          __all_sync(0xffffffffu, na * md.nbmax[c0 >> 5] < 63.99f);
+    if (PREC == 0 && cert_all) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      for (int j = 0; j < 32; j += 4)
+        e8[j >> 2] = e4m3x2_code(__uint_as_float(r[j]), __uint_as_float(r[j + 1])) |
+                     (e4m3x2_code(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])) << 16);
+      have_codes = true;
+      if (jb.out_f32 || EPI == 1 || L.out_ss) {
 #pragma unroll
-    for (int j = 0; j < 32; j += 2) round_pair<PREC>(v[j], v[j + 1]);
-    if (PREC != 2 && ncol > 0) {
-      // column norms: one coalesced load per lane, broadcast by shuffles
-      const float nb_l = (jb.b_norm && colb + lane < jb.N) ? fabsf(__ldg(jb.b_norm + colb + lane)) : 0.f;
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        float lo[2], hi[2];
-        bool chk[2];
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const float nb = __shfl_sync(0xffffffffu, nb_l, j + t);
-          const float acc = __uint_as_float(r[j + t]);
-          // E4M3 x E4M3 products are multiples of 2^-18; if every partial sum
-          // is below 2^6 (|s_k| <= ||a|| ||b||) all of them are exact in
-          // FP32, so the reference's sequential sum is the exact sum and so is
-          // the tensor-core sum: the rounding is certified without a fixup.
-          chk[t] = !(ELEM == kTcE4M3 && na * nb < 63.99f);
-          const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
-          lo[t] = acc - m, hi[t] = acc + m;
-          if (!(acc == acc)) fl |= 1u << (j + t);
+        for (int j = 0; j < 32; j += 4) {
+          const float2 x = e4m3x2_value(e8[j >> 2] & 0xFFFFu), y = e4m3x2_value(e8[j >> 2] >> 16);
+          v[j] = x.x, v[j + 1] = x.y, v[j + 2] = y.x, v[j + 3] = y.y;
         }
-        if (chk[0] || chk[1]) {
-          round_pair<PREC>(lo[0], lo[1]);
-          round_pair<PREC>(hi[0], hi[1]);
+      }
+    } else if (PREC == 1 && ncol > 0) {
+      // BF16: RNE by integer add, certificate in integer form
+      const float nas = na / sk;
 #pragma unroll
-          for (int t = 0; t < 2; ++t)
-            if (chk[t] && !(lo[t] == hi[t])) fl |= 1u << (j + t);
+      for (int j = 0; j < 32; j += 4) {
+        const float4 t4 = *reinterpret_cast<const float4*>(md.nb + c0 + j);
+        const float nb4[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float acc = __uint_as_float(r[j + t]);
+          v[j + t] = round_bf16(acc);
+          const float m = ku * fmaxf(fabsf(acc), nas * nb4[t]);
+          if (bf16_ambiguous(acc, m)) fl |= 1u << (j + t);
         }
       }
       if (!rvalid) fl = 0;
       if (ncol < 32) fl &= (1u << ncol) - 1u;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) round_pair<PREC>(v[j], v[j + 1]);
+      if (PREC != 2 && ncol > 0) {
+        float nbv[32];  // uniform across the warp: broadcast shared loads
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          const float4 t4 = *reinterpret_cast<const float4*>(md.nb + c0 + j);
+          nbv[j] = t4.x, nbv[j + 1] = t4.y, nbv[j + 2] = t4.z, nbv[j + 3] = t4.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          float lo[2], hi[2];
+          bool chk[2];
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const float nb = nbv[j + t];
+            const float acc = __uint_as_float(r[j + t]);
+            chk[t] = !(ELEM == kTcE4M3 && na * nb < 63.99f);
+            const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
+            lo[t] = acc - m, hi[t] = acc + m;
+            if (!(acc == acc)) fl |= 1u << (j + t);
+          }
+          if (chk[0] || chk[1]) {
+            round_pair<PREC>(lo[0], lo[1]);
+            round_pair<PREC>(hi[0], hi[1]);
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+              if (chk[t] && !(lo[t] == hi[t])) fl |= 1u << (j + t);
+          }
+        }
+        if (!rvalid) fl = 0;
+        if (ncol < 32) fl &= (1u << ncol) - 1u;
+      }
     }
     if (EPI == 1 && ncol > 0) {
       if (PREC == 1) {
-        uint16_t g[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) g[j] = __ldg(L.gelu_lut + enc_bf16(v[j]));
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = dec_bf16(g[j]);
+        for (int j = 0; j < 32; ++j)
+          v[j] = __uint_as_float(gelu_code(__float_as_uint(v[j]) >> 16, gelu_s, L.gelu_lut) << 16);
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = round_out(gelu_ref(v[j]), PREC);
+        have_codes = false;
       }
     }
     if (L.out_ss && ncol > 0 && rvalid) {
+      // (columns >= ncol hold zero-padded accumulators: they add nothing)
+      uint32_t ebad = 0;
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < ncol) {
-          // a flagged element is recomputed later: bound |final| by the
-          // neighbouring rounding candidates (GELU is 1.13-Lipschitz)
-          const float vb = (fl >> j) & 1u ? fabsf(v[j]) + 0.02f * fabsf(__uint_as_float(r[j])) : v[j];
-          oss = fmaf(vb, vb, oss);
-          const float ax = fabsf(v[j]);
-          obad = obad || !(ax == 0.f || (ax >= 6.7762635780344027e-21f && ax < 1.8446744073709552e19f));
-        }
+      for (int j = 0; j < 32; ++j) {
+        oss = fmaf(v[j], v[j], oss);
+        // not FMA-safe: nonzero |v| outside [2^-67, 2^64) (exponent field)
+        const uint32_t e = (__float_as_uint(v[j]) >> 23) & 0xFFu;
+        ebad |= (e - 60u) >= 131u ? (e | (__float_as_uint(v[j]) & 0x7FFFFFu)) : 0u;
+      }
+      obad = obad || ebad != 0;
+      // a flagged element is recomputed later: bound |final| by the
+      // neighbouring rounding candidates (GELU is 1.13-Lipschitz)
+      for (uint32_t f = fl; f; f &= f - 1) {
+        const int j = __ffs(f) - 1;
+        const float vb = fabsf(v[j]) + 0.02f * fabsf(__uint_as_float(r[j]));
+        oss = fmaf(vb, vb, oss) - v[j] * v[j];
+      }
     }
     // Stores: the 32 x 32 block is transposed through a warp-private smem
     // tile with 16-byte accesses (row pitch padded by 4 words: conflict-free),
@@ -302,7 +413,9 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TcJob& jb
 #pragma unroll
         for (int w = 0; w < words; ++w) {
           if (PREC == 1)
-            pk[w] = enc_bf16(v[2 * w]) | ((uint32_t)enc_bf16(v[2 * w + 1]) << 16);
+            pk[w] = (__float_as_uint(v[2 * w]) >> 16) | (__float_as_uint(v[2 * w + 1]) & 0xFFFF0000u);
+          else if (have_codes)
+            pk[w] = e8[w];
           else
             pk[w] = enc_e4m3(v[4 * w]) | ((uint32_t)enc_e4m3(v[4 * w + 1]) << 8) |
                     ((uint32_t)enc_e4m3(v[4 * w + 2]) << 16) | ((uint32_t)enc_e4m3(v[4 * w + 3]) << 24);
@@ -378,8 +491,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* mfull = tempty + 2;   // [2] metadata ready (32 arrivals)
+  uint64_t* mempty = mfull + 2;   // [2] metadata consumed (kEpiWarps arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mempty + 2);
   float* stage_all = reinterpret_cast<float*>(smem + kStages * (kAStage + kBStage) + 256);
+  TileMeta* meta = reinterpret_cast<TileMeta*>(stage_all + (size_t)kEpiWarps * kStageFloats);
+  uint16_t* gelu_s = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(meta) + 2 * kMetaBytes);
+  if (EPI == 1 && PREC == 1)  // the GELU LUT slice |x| in [2^-10, 8) (made visible by the barrier below)
+    for (int i = threadIdx.x; i < kGeluSm; i += blockDim.x) {
+      const int sg = i / (kGeluNE * 128), rem = i % (kGeluNE * 128);
+      gelu_s[i] = L.gelu_lut[(sg << 15) | ((kGeluE0 + rem / 128) << 7) | (rem % 128)];
+    }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int esz = ELEM == kTcBF16 ? 2 : 1;
@@ -393,6 +515,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], kEpiWarps);
+      mbar_init(&mfull[b], 32);
+      mbar_init(&mempty[b], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -451,22 +575,55 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&tfull[b]);
       }
     }
-  } else {  // epilogue warps: lanes quarter (warp % 4), column half ((warp - 2) / 4)
-    const int q = warp & 3, half = (warp - 2) >> 2;
+  } else if (warp == 2) {  // tile metadata, one TMEM buffer ahead of the epilogue
     uint32_t ti = 0;
     for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x, ++ti) {
-      const int ji = find_job(jobs, L.n_jobs, tile);
-      const TcJob jb = jobs[ji];
-      const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
-      const int mt = (tile - jb.tile0) / tiles_n, nt = (tile - jb.tile0) % tiles_n;
       const uint32_t b = ti & 1, bph = (ti >> 1) & 1;
+      mbar_wait(&mempty[b], bph ^ 1);
+      TileMeta& md = meta[b];
+      const int ji = find_job(jobs, L.n_jobs, tile);
+      const TcJob& jg = jobs[ji];
+      const int M = jg.M, N = jg.N, a_row0 = jg.a_row0;
+      const float* bn = jg.b_norm;
+      const int tiles_n = (N + kTcBN - 1) / kTcBN;
+      const int mt = (tile - jg.tile0) / tiles_n, nt = (tile - jg.tile0) % tiles_n;
+      if (lane == 0) md.jb = jg, md.mt = mt, md.nt = nt;
+      const bool need = PREC != 2 && (L.a_norm || L.a_ss);
+#pragma unroll
+      for (int k = 0; k < kTcBM / 32; ++k) {
+        const int r = mt * kTcBM + k * 32 + lane;
+        md.na[k * 32 + lane] = need && r < M ? a_norm_of(L, a_row0 + r) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < kTcBN / 32; ++k) {
+        const int c = nt * kTcBN + k * 32 + lane;
+        float x = PREC != 2 && bn && c < N ? fabsf(__ldg(bn + c)) : 0.f;
+        md.nb[k * 32 + lane] = x;
+        // NaN-propagating max (a NaN norm must defeat the certificate shortcut)
+        for (int o = 16; o > 0; o >>= 1) {
+          const float y = __shfl_xor_sync(0xffffffffu, x, o);
+          x = (x != x || y != y) ? __int_as_float(0x7FC00000) : fmaxf(x, y);
+        }
+        if (lane == 0) md.nbmax[k] = x;
+      }
+      mbar_arrive(&mfull[b]);  // count 32: every lane's stores are released
+    }
+  } else {  // epilogue warps: lanes quarter (warp % 4), column half
+    const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
+    uint32_t ti = 0;
+    for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x, ++ti) {
+      const uint32_t b = ti & 1, bph = (ti >> 1) & 1;
+      mbar_wait(&mfull[b], bph);
       mbar_wait(&tfull[b], bph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      epilogue_tile<ELEM, PREC, EPI>(L, jb, tile, mt, nt, tmem + b * kTcBN, q, half, lane,
-                          stage_all + (size_t)(warp - 2) * kStageFloats);
+      epilogue_tile<ELEM, PREC, EPI>(L, meta[b], tile, tmem + b * kTcBN, q, half, lane,
+                                     stage_all + (size_t)(warp - kEpiWarp0) * kStageFloats, gelu_s);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[b]);
+      if (lane == 0) {
+        mbar_arrive(&tempty[b]);
+        mbar_arrive(&mempty[b]);
+      }
     }
   }
   __syncthreads();

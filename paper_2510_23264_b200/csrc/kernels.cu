@@ -18,6 +18,25 @@ int g_exact_x2 = 1;  // paired-FP32 big exact GEMM (option "exact_x2")
 // ---------------------------------------------------------------------------
 // K2a: fold (sum_inputs, model.cpp:537-552). HBM-bound, float4-vectorised.
 // ---------------------------------------------------------------------------
+// element i (float4 group i for VEC) of a node output of storage type t
+__device__ __forceinline__ float4 load_out4(const void* b, int t, int64_t i) {
+  if (t == kOutF32) return __ldg(reinterpret_cast<const float4*>(b) + i);
+  if (t == kOutE4M3) {
+    const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(b) + i);
+    const float2 lo = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w & 0xFFFFu), __NV_E4M3)));
+    const float2 hi = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w >> 16), __NV_E4M3)));
+    return make_float4(lo.x, lo.y, hi.x, hi.y);
+  }
+  const uint2 w = __ldg(reinterpret_cast<const uint2*>(b) + i);
+  return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                     __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+}
+__device__ __forceinline__ float load_out(const void* b, int t, int64_t i) {
+  if (t == kOutF32) return reinterpret_cast<const float*>(b)[i];
+  if (t == kOutE4M3) return dec_e4m3(reinterpret_cast<const uint8_t*>(b)[i]);
+  return dec_bf16(reinterpret_cast<const uint16_t*>(b)[i]);
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(256) fold_kernel(const FoldOp* __restrict__ ops,
                                                    const FoldProg* __restrict__ progs,
@@ -30,13 +49,12 @@ __global__ void __launch_bounds__(256) fold_kernel(const FoldOp* __restrict__ op
       float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int o = p.op_begin; o < p.op_end; ++o) {
         const float* a = ops[o].a;
-        const float* b = ops[o].b;
         float* d = ops[o].dst;
         float4 av;
         if (a == CQG_REG_PREV) av = r;
         else if (a == nullptr) av = make_float4(0.f, 0.f, 0.f, 0.f);
         else av = reinterpret_cast<const float4*>(a)[i];
-        float4 bv = __ldg(reinterpret_cast<const float4*>(b) + i);
+        const float4 bv = load_out4(ops[o].b, ops[o].btype, i);
         r.x = __fadd_rn(av.x, bv.x);
         r.y = __fadd_rn(av.y, bv.y);
         r.z = __fadd_rn(av.z, bv.z);
@@ -51,7 +69,7 @@ __global__ void __launch_bounds__(256) fold_kernel(const FoldOp* __restrict__ op
       for (int o = p.op_begin; o < p.op_end; ++o) {
         const float* a = ops[o].a;
         float av = (a == CQG_REG_PREV) ? r : (a == nullptr ? 0.f : a[i]);
-        r = __fadd_rn(av, ops[o].b[i]);
+        r = __fadd_rn(av, load_out(ops[o].b, ops[o].btype, i));
         if (ops[o].dst) ops[o].dst[i] = r;
       }
     }
@@ -1120,7 +1138,7 @@ __global__ void rms_kernel(const RmsJob* __restrict__ jobs) {
   const RmsJob j = jobs[blockIdx.x];
   double acc = 0.0;
   for (int64_t i = threadIdx.x; i < j.n; i += blockDim.x) {
-    const double d = (double)j.a[i] - (double)j.b[i];
+    const double d = (double)load_out(j.a, j.atype, i) - (double)load_out(j.b, j.btype, i);
     acc += d * d;
   }
   acc = block_reduce(acc, SumOp(), sh, 0.0);

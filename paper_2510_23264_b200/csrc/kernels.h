@@ -14,10 +14,16 @@ namespace cqg {
 // dst = (a ? a : 0.0f) + b elementwise, ops of a program run in order per
 // element (so a later op may read an earlier op's dst). a == kRegPrev reuses
 // the previous op's result held in a register; dst == nullptr keeps it there.
+// Node-output storage types: node outputs that the reference rounds to E4M3 or
+// BF16 (low-precision heads, the BF16 MLP) are stored as their 1- or 2-byte
+// codes (bit-exact: the codes decode to the rounded FP32 values).
+enum OutType { kOutF32 = 0, kOutE4M3 = 1, kOutBF16 = 2 };
+
 struct FoldOp {
   const float* a;
-  const float* b;
+  const float* b;  // element type btype (OutType)
   float* dst;
+  int btype;
 };
 struct FoldProg {
   int op_begin, op_end;
@@ -99,6 +105,7 @@ struct RmsJob {
   const float* b;
   int64_t n;
   double* out;
+  int atype, btype;  // OutType of a / b
 };
 void launch_rms(const RmsJob* d_jobs, int n_jobs, cudaStream_t st);
 
