@@ -283,7 +283,8 @@ struct Engine {
   // stats/options
   cqg_stats stats{};
   int64_t opt_exact = 0;
-  int64_t opt_packed = 1;  // store E4M3/BF16-rounded node outputs as their codes
+  int64_t opt_packed = 1;
+  int64_t opt_fix_cpi = 0;  // store E4M3/BF16-rounded node outputs as their codes
   int64_t opt_mem_budget = 0;
 
   Engine(const cqg_config& c) : g(c) {}
@@ -562,6 +563,7 @@ struct Engine {
     L.ldb = (int64_t)B.cols * esz;
     L.elem = elem;
     L.kappa = 8.0f;
+    L.fix_cpi = (int)opt_fix_cpi;
     if (!gelu_lut.p) {
       gelu_lut.ensure(65536 * 2);
       launch_gelu_lut(gelu_lut.as<uint16_t>(), st);
@@ -1822,6 +1824,10 @@ int cqg_set_option(cqg_ctx* ctx, const char* key, int64_t value) {
     std::string k(key);
     if (k == "exact") ctx->e->opt_exact = value;
     else if (k == "packed") ctx->e->opt_packed = value;
+    else if (k == "fix_cpi") {
+      if (value != 0 && value != 1 && value != 2 && value != 4) throw Error(1, "fix_cpi must be 0, 1, 2 or 4");
+      ctx->e->opt_fix_cpi = value;
+    }
     else if (k == "exact_x2") cqg::g_exact_x2 = (int)value;
     else if (k == "profile") ctx->e->opt_profile = value;
     else if (k == "mem_budget") ctx->e->opt_mem_budget = value;

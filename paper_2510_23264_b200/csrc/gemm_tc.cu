@@ -838,7 +838,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)
     __syncthreads();
     const int n_el = wsum[4] + wsum[5] + wsum[6] + wsum[7];
     const int need = (n_el + kFixThreads * kFixPer - 1) / (kFixThreads * kFixPer);
-    const int cpi = need <= 1 ? 1 : (need == 2 ? 2 : kFixCols);
+    const int cpi = L.fix_cpi ? L.fix_cpi : (need <= 1 ? 1 : (need == 2 ? 2 : kFixCols));
     const int cnt = (pc + cpi - 1) / cpi;
     int incl = cnt;
 #pragma unroll

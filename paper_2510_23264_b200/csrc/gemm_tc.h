@@ -56,6 +56,7 @@ struct TcLaunch {
   uint32_t* fix_count;  // [0] tiles listed by this launch (zeroed after it),
                         // [2..3] u64 running total of flagged elements
   float kappa;
+  int fix_cpi;  // fixup columns per work item: 0 adaptive, else 1 / 2 / 4
   const uint16_t* gelu_lut;  // bf16 -> round_bf16(gelu(x)) for all 2^16 inputs
 };
 
