@@ -418,7 +418,10 @@ void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float
                       const float* beta, int D, int prec, cudaStream_t st) {
   if (n_jobs <= 0 || max_rows <= 0) return;
   // few rows: latency-bound, stage whole rows (RW rows per warp) in shared memory
-  if ((int64_t)max_rows * n_jobs <= 32768 && (D & 3) == 0 && D <= 2048) {
+  // Whole rows staged in shared memory: every row is read from HBM once (the
+  // ring kernel below re-streams each row three times and thrashes L2 on big
+  // launches), and the chains run at FADD latency.
+  if ((D & 3) == 0 && D <= 2048) {
     const int rw = D <= 1024 ? 8 : 4;
     const size_t smem = sizeof(float) * kLsWarps * rw * (D | 1);
     static bool attr_s = false;
