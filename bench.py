@@ -319,7 +319,8 @@ def main(argv=None):
         ach = p["bytes"] / (p["ms"] / 1e3) / 1e9
         peak, unit, bound, psrc = hbm, "GB/s", "hbm", src
     roofline = {"bound": bound, "kernel": name, "achieved": ach, "peak": peak, "unit": unit,
-                "frac": ach / peak, "traffic": traffic, "peak_source": psrc,
+                "frac": ach / peak, "traffic": traffic, "traffic_note": traffic_note,
+                "peak_source": psrc,
                 "kernel_share_of_step": p["ms"] / max(1e-9, sum(v["ms"] for v in prof.values())),
                 "per_kernel": {k: {"ms": v["ms"], "launches": v["launches"],
                                    "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9,

@@ -303,3 +303,48 @@ def test_planted_known_answer_aucs_on_gpu(preset):
             pts.append((tp / len(gt), (len(kept) - tp) / (e.n_edges - len(gt))))
         assert float(auc_from_points(pts)).hex() == G["planted"][preset][mname]["auc"], mname
     e.close()
+
+
+# --- kernel variants: every engine option must give the oracle's scores -------
+# MID: a width where the tensor-core paths, packed node outputs and the fixup
+# kernels all run (D*esz % 32 == 0, several 128-row tiles, MLP K = 4D).
+MID = formats.ModelConfig(2, 4, 128, 32, 300, 16, 1, 1)
+
+
+@pytest.mark.parametrize("opts", [{}, {"packed": 0}, {"exact_x2": 0}, {"fix_cpi": 1},
+                                  {"fix_cpi": 2}, {"fix_cpi": 4}, {"exact": 1}])
+def test_engine_options_match_oracle(opts):
+    w, ds = make(MID, 3, 10, 4)
+    p = Port(MID, w.mats)
+    e = eng.Engine(w)
+    for k, v in opts.items():
+        e.set_option(k, v)
+    e.set_dataset(ds, KL)
+    mask = np.ones(p.n_edges, bool)
+    edges = np.nonzero(mask)[0]
+    want = p.score_edges(ds, edges, Policy.head_quantized(), per_edge=True, metric=KL)
+    got = e.score_edges(mask, edges, eng.PrecisionPolicy.head_quantized(), True, 0)
+    if "exact_x2" in opts:  # process-wide switch: restore the default
+        e.set_option("exact_x2", 1)
+    assert close(got, want), (opts, np.max(np.abs(got - want) / (np.abs(want) + 1e-300)))
+    e.close()
+
+
+def test_gpt2_width_slice_matches_reference():
+    """GPT-2-small layer width (D=768, H=12, d_k=64, MLP 3072, S=16) on 2
+    layers and a reduced vocabulary: the production tile shapes, shared-memory
+    LN rows, K=3072 fixups and the paired-FP32 unembed, on a sample of edges
+    from every stage, against scores of the reference library itself
+    (tests/golden/make_gpt2w.py)."""
+    g = json.load(open(os.path.join(GOLDEN, "gpt2w_slice.json")))
+    cfg = formats.ModelConfig(*g["config"])
+    w, ds = make(cfg, g["wseed"], g["items"], g["dseed"])
+    e = eng.Engine(w)
+    e.set_dataset(ds, KL)
+    mask = np.ones(e.n_edges, bool)
+    edges = np.array(g["edges"], np.int32)
+    want = np.array([float.fromhex(x) for x in g["scores"]])
+    got = e.score_edges(mask, edges, eng.PrecisionPolicy.head_quantized(), True, 0)
+    assert close(got, want), np.max(np.abs(got - want) / (np.abs(want) + 1e-300))
+    assert e.stats()["kernel_launches"] > 0
+    e.close()
