@@ -304,7 +304,14 @@ def main(argv=None):
     # dot_col semantics forbid FMA): 148 SMs x 128 lanes x 1 instr/clk, 2 instr
     # per multiply-add, counted as 2 flops
     simt_peak = 148 * 128 * 1.965e9 / 1e12
-    traffic = None
+    traffic, traffic_note = None, None
+    tp = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+    if os.path.exists(tp):  # committed ncu --set full capture of this kernel class
+        t = json.load(open(tp)).get(name.split(":")[-1])
+        if t:
+            traffic = t["traffic_bytes"]
+            traffic_note = (f"dram bytes of one captured launch ({t['launch']}); algorithmic "
+                            f"{t['algorithmic_bytes']} B for that launch")
     cls = name.split(":")[-1]  # "base:" = per-source baseline runs
     if p["flops"] > 0:
         ach = p["flops"] / (p["ms"] / 1e3) / 1e12

@@ -650,7 +650,7 @@ __device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
 __device__ __forceinline__ float f2_lo(f2_t v) { return __uint_as_float((uint32_t)v); }
 __device__ __forceinline__ float f2_hi(f2_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
 
-__global__ void __launch_bounds__(256) gemm_exact_x2_kernel(const GemmJob* __restrict__ jobs,
+__global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __restrict__ jobs,
                                                             const int* __restrict__ tile_start,
                                                             int n_jobs, float negz) {
   int lo = 0, hi = n_jobs - 1;
@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(256) gemm_exact_x2_kernel(const GemmJob* __res
     const bool more = k0 + kXBK < jb.K;
     if (more) load(k0 + kXBK);
     const int kl = min(kXBK, jb.K - k0);
-    for (int kk = 0; kk < kl; ++kk) {
+    auto step = [&](int kk) {
       f2_t a[8], b[4];
       {
         const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][ty * 4]);
@@ -718,6 +718,12 @@ __global__ void __launch_bounds__(256) gemm_exact_x2_kernel(const GemmJob* __res
       for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int p = 0; p < 4; ++p) acc[i][p] = f2_add(acc[i][p], f2_fma(a[i], b[p], z2));
+    };
+    if (kl == kXBK) {
+#pragma unroll
+      for (int kk = 0; kk < kXBK; ++kk) step(kk);
+    } else {
+      for (int kk = 0; kk < kl; ++kk) step(kk);
     }
     if (more) {
       store(buf ^ 1);
