@@ -259,8 +259,10 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TileMeta&
   const float ku = L.kappa * 5.9604644775390625e-08f * sk;
   const int row0 = mt * kTcBM + q * 32;
   const int nrow = min(32, jb.M - row0);
-  uint32_t flagged[2];
-#pragma unroll
+  uint32_t flagged0 = 0, flagged1 = 0;
+  // one 32-column chunk per iteration, not unrolled: the epilogue body is
+  // large and the unrolled pair thrashed the instruction cache
+#pragma unroll 1
   for (int cc = 0; cc < 2; ++cc) {
     const int c0 = half * 64 + cc * 32;
     uint32_t r[32];
@@ -361,19 +363,15 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TileMeta&
       uint32_t ebad = 0;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        oss = fmaf(v[j], v[j], oss);
+        // a flagged element is recomputed later: bound |final| by the
+        // neighbouring rounding candidates (GELU is 1.13-Lipschitz)
+        const float vb = (fl >> j) & 1u ? fabsf(v[j]) + 0.02f * fabsf(__uint_as_float(r[j])) : v[j];
+        oss = fmaf(vb, vb, oss);
         // not FMA-safe: nonzero |v| outside [2^-67, 2^64) (exponent field)
         const uint32_t e = (__float_as_uint(v[j]) >> 23) & 0xFFu;
         ebad |= (e - 60u) >= 131u ? (e | (__float_as_uint(v[j]) & 0x7FFFFFu)) : 0u;
       }
       obad = obad || ebad != 0;
-      // a flagged element is recomputed later: bound |final| by the
-      // neighbouring rounding candidates (GELU is 1.13-Lipschitz)
-      for (uint32_t f = fl; f; f &= f - 1) {
-        const int j = __ffs(f) - 1;
-        const float vb = fabsf(v[j]) + 0.02f * fabsf(__uint_as_float(r[j]));
-        oss = fmaf(vb, vb, oss) - v[j] * v[j];
-      }
     }
     // Stores: the 32 x 32 block is transposed through a warp-private smem
     // tile with 16-byte accesses (row pitch padded by 4 words: conflict-free),
@@ -454,8 +452,10 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TileMeta&
         }
       }
     }
-    flagged[cc] = fl;
+    if (cc == 0) flagged0 = fl;
+    else flagged1 = fl;
   }
+  const uint32_t flagged[2] = {flagged0, flagged1};
   if (L.out_ss && rvalid) {
     atomicAdd(L.out_ss + jb.a_row0 + row, oss);
     if (obad) atomicOr(L.out_bad + jb.a_row0 + row, 1u);
