@@ -76,9 +76,87 @@ __global__ void __launch_bounds__(256) fold_kernel(const FoldOp* __restrict__ op
   }
 }
 
+// 16 elements per thread: a packed (E4M3) node output is then one 16-byte
+// load per op, enough bytes in flight per thread to keep HBM busy (4-byte
+// loads per op left the fold latency-bound at ~3 TB/s).
+__device__ __forceinline__ void load_out16(const void* b, int t, int64_t i, float (&v)[16]) {
+  if (t == kOutF32) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(b) + 4 * i + q);
+      v[4 * q] = x.x, v[4 * q + 1] = x.y, v[4 * q + 2] = x.z, v[4 * q + 3] = x.w;
+    }
+  } else if (t == kOutE4M3) {
+    const uint4 w = __ldg(reinterpret_cast<const uint4*>(b) + i);
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 lo = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(ww[q] & 0xFFFFu), __NV_E4M3)));
+      const float2 hi = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(ww[q] >> 16), __NV_E4M3)));
+      v[4 * q] = lo.x, v[4 * q + 1] = lo.y, v[4 * q + 2] = hi.x, v[4 * q + 3] = hi.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(b) + 2 * i + q);
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        v[8 * q + 2 * h] = __uint_as_float(ww[h] << 16);
+        v[8 * q + 2 * h + 1] = __uint_as_float(ww[h] & 0xFFFF0000u);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) fold16_kernel(const FoldOp* __restrict__ ops,
+                                                     const FoldProg* __restrict__ progs,
+                                                     int64_t n_elems) {
+  const FoldProg p = progs[blockIdx.y];
+  const int64_t n16 = n_elems >> 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float r[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) r[k] = 0.f;
+    for (int o = p.op_begin; o < p.op_end; ++o) {
+      const float* a = ops[o].a;
+      float* d = ops[o].dst;
+      float bv[16];
+      load_out16(ops[o].b, ops[o].btype, i, bv);
+      if (a != CQG_REG_PREV) {
+        if (a == nullptr) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) r[k] = 0.f;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 x = reinterpret_cast<const float4*>(a)[4 * i + q];
+            r[4 * q] = x.x, r[4 * q + 1] = x.y, r[4 * q + 2] = x.z, r[4 * q + 3] = x.w;
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) r[k] = __fadd_rn(r[k], bv[k]);
+      if (d)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          reinterpret_cast<float4*>(d)[4 * i + q] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+    }
+  }
+}
+
 void launch_fold(const FoldOp* d_ops, const FoldProg* d_progs, int n_progs, int64_t n_elems,
                  cudaStream_t st) {
   if (n_progs <= 0) return;
+  if (n_elems % 16 == 0) {
+    int gx = (int)std::min<int64_t>((n_elems / 16 + 255) / 256, 4096);
+    for (int y0 = 0; y0 < n_progs; y0 += 65535) {
+      dim3 grid(gx, (unsigned)std::min(65535, n_progs - y0));
+      fold16_kernel<<<grid, 256, 0, st>>>(d_ops, d_progs + y0, n_elems);
+    }
+    return;
+  }
   const bool vec = (n_elems % 4) == 0;
   int64_t work = vec ? n_elems / 4 : n_elems;
   int gx = (int)((work + 255) / 256);
@@ -362,12 +440,47 @@ __global__ void __launch_bounds__(32 * kLsWarps) ln_small_kernel(const LnJob* __
   __syncwarp();
   float mean = 0.f, inv = 0.f;
   if (lane < nr) {
+    // sequential chains at FADD latency: the shared loads of the next 16
+    // elements are issued ahead of the dependent adds of the current 16
     const float* row = t + lane * P;
+    constexpr int U = 16;
     float acc = 0.f;
-    for (int c = 0; c < D; ++c) acc = __fadd_rn(acc, row[c]);
+    int c = 0;
+    float cur[U], nxt[U];
+    if (D >= U) {
+#pragma unroll
+      for (int k = 0; k < U; ++k) cur[k] = row[k];
+      for (c = 0; c + U <= D; c += U) {
+        const bool more = c + 2 * U <= D;
+#pragma unroll
+        for (int k = 0; k < U; ++k) nxt[k] = more ? row[c + U + k] : 0.f;
+#pragma unroll
+        for (int k = 0; k < U; ++k) acc = __fadd_rn(acc, cur[k]);
+#pragma unroll
+        for (int k = 0; k < U; ++k) cur[k] = nxt[k];
+      }
+    }
+    for (; c < D; ++c) acc = __fadd_rn(acc, row[c]);
     mean = __fdiv_rn(acc, (float)D);
     acc = 0.f;
-    for (int c = 0; c < D; ++c) {
+    c = 0;
+    if (D >= U) {
+#pragma unroll
+      for (int k = 0; k < U; ++k) cur[k] = row[k];
+      for (c = 0; c + U <= D; c += U) {
+        const bool more = c + 2 * U <= D;
+#pragma unroll
+        for (int k = 0; k < U; ++k) nxt[k] = more ? row[c + U + k] : 0.f;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const float d = __fsub_rn(cur[k], mean);
+          acc = __fadd_rn(acc, __fmul_rn(d, d));
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) cur[k] = nxt[k];
+      }
+    }
+    for (; c < D; ++c) {
       const float d = __fsub_rn(row[c], mean);
       acc = __fadd_rn(acc, __fmul_rn(d, d));
     }
