@@ -238,6 +238,11 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
                "l"(src)
                : "memory");
 }
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -428,59 +433,77 @@ __global__ void __launch_bounds__(32 * kLsWarps) ln_small_kernel(const LnJob* __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = (blockIdx.x * kLsWarps + warp) * RW;
   if (r0 >= j.rows) return;
-  const int P = D | 1;
+  // row pitch D + 4 floats: rows stay 16-byte aligned (16-byte cp.async in,
+  // float4 reads in the normalisation pass) and the RW chain lanes start 4
+  // banks apart (distinct banks for D % 32 == 0)
+  const int P = D + 4;
   float* t = ls_sm + (size_t)warp * RW * P;
   const int nr = min(RW, j.rows - r0);
+  const bool a16 = (j.in_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(j.in) & 15) == 0;
   for (int r = 0; r < nr; ++r) {
     const float* src = j.in + (int64_t)(r0 + r) * j.in_stride;
-    for (int c = lane; c < D; c += 32) cp_async4(t + r * P + c, src + c);
+    if (a16)
+      for (int c = 4 * lane; c < D; c += 128) cp_async16(t + r * P + c, src + c);
+    else
+      for (int c = lane; c < D; c += 32) cp_async4(t + r * P + c, src + c);
   }
   cp_async_commit();
   cp_async_wait<0>();
   __syncwarp();
   float mean = 0.f, inv = 0.f;
   if (lane < nr) {
-    // sequential chains at FADD latency: the shared loads of the next 16
-    // elements are issued ahead of the dependent adds of the current 16
+    // sequential chains at FADD latency: 16-byte shared loads (rows are
+    // 16-byte aligned, P % 4 == 0), the next 16 elements loaded ahead of the
+    // dependent adds of the current 16
     const float* row = t + lane * P;
     constexpr int U = 16;
     float acc = 0.f;
-    int c = 0;
-    float cur[U], nxt[U];
-    if (D >= U) {
+    float4 cur[U / 4], nxt[U / 4];
+    const int Dm = D & ~(U - 1);
+    if (Dm) {
 #pragma unroll
-      for (int k = 0; k < U; ++k) cur[k] = row[k];
-      for (c = 0; c + U <= D; c += U) {
-        const bool more = c + 2 * U <= D;
-#pragma unroll
-        for (int k = 0; k < U; ++k) nxt[k] = more ? row[c + U + k] : 0.f;
-#pragma unroll
-        for (int k = 0; k < U; ++k) acc = __fadd_rn(acc, cur[k]);
-#pragma unroll
-        for (int k = 0; k < U; ++k) cur[k] = nxt[k];
-      }
+      for (int k = 0; k < U / 4; ++k) cur[k] = reinterpret_cast<const float4*>(row)[k];
     }
-    for (; c < D; ++c) acc = __fadd_rn(acc, row[c]);
+    for (int c = 0; c < Dm; c += U) {
+      const bool more = c + U < Dm;
+#pragma unroll
+      for (int k = 0; k < U / 4; ++k)
+        nxt[k] = more ? reinterpret_cast<const float4*>(row + c + U)[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < U / 4; ++k) {
+        acc = __fadd_rn(acc, cur[k].x);
+        acc = __fadd_rn(acc, cur[k].y);
+        acc = __fadd_rn(acc, cur[k].z);
+        acc = __fadd_rn(acc, cur[k].w);
+      }
+#pragma unroll
+      for (int k = 0; k < U / 4; ++k) cur[k] = nxt[k];
+    }
+    for (int c = Dm; c < D; ++c) acc = __fadd_rn(acc, row[c]);
     mean = __fdiv_rn(acc, (float)D);
     acc = 0.f;
-    c = 0;
-    if (D >= U) {
+    if (Dm) {
 #pragma unroll
-      for (int k = 0; k < U; ++k) cur[k] = row[k];
-      for (c = 0; c + U <= D; c += U) {
-        const bool more = c + 2 * U <= D;
+      for (int k = 0; k < U / 4; ++k) cur[k] = reinterpret_cast<const float4*>(row)[k];
+    }
+    for (int c = 0; c < Dm; c += U) {
+      const bool more = c + U < Dm;
 #pragma unroll
-        for (int k = 0; k < U; ++k) nxt[k] = more ? row[c + U + k] : 0.f;
+      for (int k = 0; k < U / 4; ++k)
+        nxt[k] = more ? reinterpret_cast<const float4*>(row + c + U)[k] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const float d = __fsub_rn(cur[k], mean);
+      for (int k = 0; k < U / 4; ++k) {
+        const float xs[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const float d = __fsub_rn(xs[h], mean);
           acc = __fadd_rn(acc, __fmul_rn(d, d));
         }
-#pragma unroll
-        for (int k = 0; k < U; ++k) cur[k] = nxt[k];
       }
+#pragma unroll
+      for (int k = 0; k < U / 4; ++k) cur[k] = nxt[k];
     }
-    for (; c < D; ++c) {
+    for (int c = Dm; c < D; ++c) {
       const float d = __fsub_rn(row[c], mean);
       acc = __fadd_rn(acc, __fmul_rn(d, d));
     }
@@ -497,11 +520,13 @@ __global__ void __launch_bounds__(32 * kLsWarps) ln_small_kernel(const LnJob* __
     for (int c4 = lane; c4 < D4; c4 += 32) {
       const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c4);
       const float4 bt = __ldg(reinterpret_cast<const float4*>(beta) + c4);
+      const float4 xv = reinterpret_cast<const float4*>(row)[c4];
       const float gg[4] = {gm.x, gm.y, gm.z, gm.w}, bb[4] = {bt.x, bt.y, bt.z, bt.w};
+      const float xx[4] = {xv.x, xv.y, xv.z, xv.w};
       float y[4], qv[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        y[k] = __fadd_rn(__fmul_rn(gg[k], __fmul_rn(__fsub_rn(row[4 * c4 + k], m_r), i_r)), bb[k]);
+        y[k] = __fadd_rn(__fmul_rn(gg[k], __fmul_rn(__fsub_rn(xx[k], m_r), i_r)), bb[k]);
         qv[k] = round_p(y[k], prec);
         ss = fmaf(qv[k], qv[k], ss);
         bad = bad || bf16_fma_bad(qv[k]);
@@ -536,7 +561,7 @@ void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float
   // launches), and the chains run at FADD latency.
   if ((D & 3) == 0 && D <= 2048) {
     const int rw = D <= 1024 ? 8 : 4;
-    const size_t smem = sizeof(float) * kLsWarps * rw * (D | 1);
+    const size_t smem = sizeof(float) * kLsWarps * rw * (D + 4);
     static bool attr_s = false;
     if (!attr_s) {
       cudaFuncSetAttribute(ln_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
