@@ -461,16 +461,22 @@ struct Engine {
     std::vector<int> ts(jobs.size());
     int total = 0;
     double flops = 0;
-    bool big = true;
-    for (const GemmJob& j : jobs) big = big && j.M >= 128 && j.N >= 128;
+    bool big = true, wide = g_exact_x2 != 0;
+    for (const GemmJob& j : jobs) {
+      big = big && j.M >= 128 && j.N >= 128;
+      wide = wide && j.M <= 64 && j.N >= 256 && j.epi == 0;
+    }
     for (size_t i = 0; i < jobs.size(); ++i) {
       ts[i] = total;
-      total += big ? gemm_exact_big_tiles(jobs[i].M, jobs[i].N) : gemm_exact_tiles(jobs[i].M, jobs[i].N);
+      total += wide  ? gemm_exact_wide_tiles(jobs[i].M, jobs[i].N)
+               : big ? gemm_exact_big_tiles(jobs[i].M, jobs[i].N)
+                     : gemm_exact_tiles(jobs[i].M, jobs[i].N);
       flops += 2.0 * jobs[i].M * (double)jobs[i].N * jobs[i].K;
     }
     reserve(up_bytes(jobs.size(), sizeof(GemmJob)) + up_bytes(ts.size(), sizeof(int)));
     Prof pf(this, name, flops, 0);
-    if (big) launch_gemm_exact_big(upload(jobs), upload(ts), (int)jobs.size(), total, st);
+    if (wide) launch_gemm_exact_wide(upload(jobs), upload(ts), (int)jobs.size(), total, st);
+    else if (big) launch_gemm_exact_big(upload(jobs), upload(ts), (int)jobs.size(), total, st);
     else launch_gemm_exact(upload(jobs), upload(ts), (int)jobs.size(), total, st);
   }
   // Rtn4 activation groups (one per item), in place

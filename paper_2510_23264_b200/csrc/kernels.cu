@@ -560,18 +560,27 @@ void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float
   // ring kernel below re-streams each row three times and thrashes L2 on big
   // launches), and the chains run at FADD latency.
   if ((D & 3) == 0 && D <= 2048) {
-    const int rw = D <= 1024 ? 8 : 4;
+    // rows per warp: 8 (4 for D > 1024) on big launches; fewer when the
+    // launch would not give every SM several warps (the per-source baseline
+    // runs: 1024-row launches), so more chains run side by side
+    int rw = D <= 1024 ? 8 : 4;
+    const int64_t total = (int64_t)max_rows * n_jobs;
+    while (rw > 1 && total / rw < 4 * 148) rw >>= 1;
     const size_t smem = sizeof(float) * kLsWarps * rw * (D + 4);
     static bool attr_s = false;
     if (!attr_s) {
       cudaFuncSetAttribute(ln_small_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(ln_small_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(ln_small_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(ln_small_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr_s = true;
     }
     for (int y0 = 0; y0 < n_jobs; y0 += 65535) {
       dim3 grid((max_rows + rw * kLsWarps - 1) / (rw * kLsWarps), (unsigned)std::min(65535, n_jobs - y0));
       if (rw == 8) ln_small_kernel<8><<<grid, 32 * kLsWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
-      else ln_small_kernel<4><<<grid, 32 * kLsWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
+      else if (rw == 4) ln_small_kernel<4><<<grid, 32 * kLsWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
+      else if (rw == 2) ln_small_kernel<2><<<grid, 32 * kLsWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
+      else ln_small_kernel<1><<<grid, 32 * kLsWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
     }
     return;
   }
@@ -883,6 +892,117 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __
       jb.C[(int64_t)gm * jb.ldc + gn] = v;
     }
   }
+}
+
+// Short-and-wide variant (64 x 256 tiles, 4 rows x 16 columns per thread) of
+// the paired-FP32 kernel for jobs with at most 64 rows: the unembed of one
+// evaluation context (B last rows) would leave half of every 128-row tile
+// empty. Same per-element chain.
+constexpr int kSBM = 64, kSBN = 256, kSBK = 8;
+
+int gemm_exact_wide_tiles(int M, int N) { return ((M + kSBM - 1) / kSBM) * ((N + kSBN - 1) / kSBN); }
+
+__global__ void __launch_bounds__(256, 2) gemm_exact_wide_kernel(const GemmJob* __restrict__ jobs,
+                                                                 const int* __restrict__ tile_start,
+                                                                 int n_jobs, float negz) {
+  int lo = 0, hi = n_jobs - 1;
+  const int t = blockIdx.x;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_start[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmJob jb = jobs[lo];
+  const int local = t - tile_start[lo];
+  const int tiles_m = (jb.M + kSBM - 1) / kSBM;
+  const int m0 = (local % tiles_m) * kSBM, n0 = (local / tiles_m) * kSBN;
+  __shared__ __align__(16) float2 As[2][kSBK][kSBM];  // (a, a) broadcast pairs
+  __shared__ __align__(16) float Bs[2][kSBK][kSBN];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int a_r = tid >> 2, a_k = (tid & 3) * 2;
+  const int b_k = tid >> 5, b_n = (tid & 31) * 8;
+  const f2_t z2 = f2_pack(negz, negz);
+  float ra[2], rb[8];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int gm = m0 + a_r, gk = k0 + a_k + i;
+      ra[i] = (gm < jb.M && gk < jb.K) ? jb.A[(int64_t)gm * jb.lda + gk] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gk2 = k0 + b_k, gn = n0 + b_n + i;
+      rb[i] = (gk2 < jb.K && gn < jb.N) ? jb.B[(int64_t)gk2 * jb.ldb + gn] : 0.f;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) As[buf][a_k + i][a_r] = make_float2(ra[i], ra[i]);
+    *reinterpret_cast<float4*>(&Bs[buf][b_k][b_n]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
+    *reinterpret_cast<float4*>(&Bs[buf][b_k][b_n + 4]) = make_float4(rb[4], rb[5], rb[6], rb[7]);
+  };
+  // acc[i][p]: row ty*4 + i, column pair p (q*64 + tx*4 + {0,1} / {2,3}, q = p / 2)
+  f2_t acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int p = 0; p < 8; ++p) acc[i][p] = 0ull;
+  load(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < jb.K; k0 += kSBK) {
+    const bool more = k0 + kSBK < jb.K;
+    if (more) load(k0 + kSBK);
+    const int kl = min(kSBK, jb.K - k0);
+    auto step = [&](int kk) {
+      f2_t a[4], b[8];
+      const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][ty * 4]);
+      const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][ty * 4 + 2]);
+      a[0] = a0.x, a[1] = a0.y, a[2] = a1.x, a[3] = a1.y;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const ulonglong2 bq = *reinterpret_cast<const ulonglong2*>(&Bs[buf][kk][q * 64 + tx * 4]);
+        b[2 * q] = bq.x, b[2 * q + 1] = bq.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) acc[i][p] = f2_add(acc[i][p], f2_fma(a[i], b[p], z2));
+    };
+    if (kl == kSBK) {
+#pragma unroll
+      for (int kk = 0; kk < kSBK; ++kk) step(kk);
+    } else {
+      for (int kk = 0; kk < kl; ++kk) step(kk);
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty * 4 + i;
+    if (gm >= jb.M) continue;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int gn = n0 + (j >> 2) * 64 + tx * 4 + (j & 3);
+      if (gn >= jb.N) continue;
+      const f2_t pr = acc[i][j >> 1];
+      float v = round_p((j & 1) ? f2_hi(pr) : f2_lo(pr), jb.prec);
+      if (jb.epi == 1) v = round_p(gelu_ref(v), jb.prec);
+      jb.C[(int64_t)gm * jb.ldc + gn] = v;
+    }
+  }
+}
+
+void launch_gemm_exact_wide(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs,
+                            int total_tiles, cudaStream_t st) {
+  if (n_jobs <= 0 || total_tiles <= 0) return;
+  gemm_exact_wide_kernel<<<total_tiles, 256, 0, st>>>(d_jobs, d_tile_start, n_jobs, -0.0f);
 }
 
 void launch_gemm_exact_big(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs,

@@ -64,6 +64,10 @@ int gemm_exact_tiles(int M, int N);
 void launch_gemm_exact_big(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs,
                            int total_tiles, cudaStream_t st);
 int gemm_exact_big_tiles(int M, int N);
+// 64 x 256-tile paired-FP32 variant for jobs with at most 64 rows (same numerics)
+void launch_gemm_exact_wide(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs,
+                            int total_tiles, cudaStream_t st);
+int gemm_exact_wide_tiles(int M, int N);
 extern int g_exact_x2;  // 1: FFMA2/FADD2 variant of the big exact GEMM
 
 // ---- K5: causal attention (kernels.cpp:167-219) + z rounding ---------------
