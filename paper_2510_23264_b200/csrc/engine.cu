@@ -773,6 +773,7 @@ struct Engine {
     const size_t per = (size_t)ZR * dk;
     float* z = tc_wo ? nullptr : scratch("h_z", jobs.size() * per);
     uint8_t* z8 = tc_wo ? reinterpret_cast<uint8_t*>(scratch("h_z8", jobs.size() * per / 4 + 1)) : nullptr;
+    float* znorm = tc_wo ? scratch("h_znorm", jobs.size() * (size_t)ZR) : nullptr;  // W_O's ||a||
     std::vector<AttnJob> aj;
     for (size_t j = 0; j < jobs.size(); ++j) {
       const int h = jobs[j].head;
@@ -784,6 +785,7 @@ struct Engine {
       a.z = z ? z + j * per : nullptr;
       if (r4 && !target) rq.push_back({a.z, (int64_t)g.S * dk, g.S, dk, dk, 0});
       a.z8 = z8 ? z8 + j * per : nullptr;
+      a.znorm = znorm ? znorm + j * (size_t)ZR : nullptr;
       aj.push_back(a);
     }
     attn(aj, nb);
@@ -803,7 +805,7 @@ struct Engine {
         t.prec = p_low;
         tj.push_back(t);
       }
-      gemm_tc(kTcE4M3, z8, (int64_t)jobs.size() * ZR, dk, bo, tj, "wo");
+      gemm_tc(kTcE4M3, z8, (int64_t)jobs.size() * ZR, dk, bo, tj, "wo", znorm);
     } else {
       const float* wo = W(g.mat(7, l), wo_prec, P.mode);
       for (size_t j = 0; j < jobs.size(); ++j) {

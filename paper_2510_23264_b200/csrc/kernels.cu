@@ -1092,11 +1092,17 @@ __global__ void __launch_bounds__(128) attention_warp_kernel(const AttnJob* __re
       for (int c = 0; c < NT; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(pj, v[j * ldk + lane + 32 * c]));
     }
     const int64_t zr = (int64_t)item * (S - q0) + (i - q0);
+    float ss = 0.f;
 #pragma unroll
     for (int c = 0; c < NT; ++c) {
       const float zv = round_p(acc[c], jb.prec);
       if (jb.z) jb.z[zr * jb.ldz + lane + 32 * c] = zv;
       if (jb.z8) jb.z8[zr * jb.ldz + lane + 32 * c] = enc_e4m3(zv);
+      ss = fmaf(zv, zv, ss);
+    }
+    if (jb.znorm) {  // the row norm rownorm_kernel would compute (E4M3: no FMA-safety bit)
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) jb.znorm[zr] = sqrtf(ss) * 1.0001f;
     }
   }
 }
@@ -1137,13 +1143,16 @@ __global__ void attention_kernel(const AttnJob* __restrict__ jobs, int S, int dk
     }
     for (int jj = 0; jj <= i; ++jj) p[jj] = __fdiv_rn(p[jj], den);
     const int64_t zr = (int64_t)item * (S - jb.q0) + (i - jb.q0);
+    float ss = 0.f;
     for (int t = 0; t < dk; ++t) {
       float acc = 0.f;
       for (int jj = 0; jj <= i; ++jj) acc = __fadd_rn(acc, __fmul_rn(p[jj], v[jj * ldk + t]));
       const float zr_v = round_p(acc, jb.prec);
       if (jb.z) jb.z[zr * jb.ldz + t] = zr_v;
       if (jb.z8) jb.z8[zr * jb.ldz + t] = enc_e4m3(zr_v);
+      ss = fmaf(zr_v, zr_v, ss);
     }
+    if (jb.znorm) jb.znorm[zr] = sqrtf(ss) * 1.0001f;
   }
 }
 

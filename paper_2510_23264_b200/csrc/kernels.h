@@ -82,6 +82,7 @@ struct AttnJob {
   uint8_t* z8;  // packed E4M3 copy of z for the tensor-core W_O (may be null)
   int q0;       // first query row computed (S-1: last position only); z rows
                 // are compact: item * (S - q0) + (i - q0)
+  float* znorm;  // [z rows] ||z8 row|| * 1.0001 for W_O's certificate (may be null)
 };
 void launch_attention(const AttnJob* d_jobs, int n_jobs, int B, int S, int dk, cudaStream_t st);
 
