@@ -569,7 +569,9 @@ struct Engine {
     L.ldb = (int64_t)B.cols * esz;
     L.elem = elem;
     L.kappa = 8.0f;
-    L.fix_cpi = (int)opt_fix_cpi;
+    // fixup columns per work item: adaptive (0) by default; two columns share
+    // each A load for long chains (K >= 2048: measured faster on W_out)
+    L.fix_cpi = opt_fix_cpi ? (int)opt_fix_cpi : (a_k >= 2048 ? 2 : 0);
     if (!gelu_lut.p) {
       gelu_lut.ensure(65536 * 2);
       launch_gelu_lut(gelu_lut.as<uint16_t>(), st);

@@ -838,7 +838,10 @@ __global__ void __launch_bounds__(kFixThreads, 1)
     __syncthreads();
     const int n_el = wsum[4] + wsum[5] + wsum[6] + wsum[7];
     const int need = (n_el + kFixThreads * kFixPer - 1) / (kFixThreads * kFixPer);
-    const int cpi = L.fix_cpi ? L.fix_cpi : (need <= 1 ? 1 : (need == 2 ? 2 : kFixCols));
+    // a requested width is raised where the item list would overflow its
+    // shared-memory capacity (n_el / cpi + one partial item per row)
+    const int cap_cpi = n_el + kTcBM <= kFixMaxItems ? 1 : (n_el / 2 + kTcBM <= kFixMaxItems ? 2 : kFixCols);
+    const int cpi = L.fix_cpi ? max(L.fix_cpi, cap_cpi) : (need <= 1 ? 1 : (need == 2 ? 2 : kFixCols));
     const int cnt = (pc + cpi - 1) / cpi;
     int incl = cnt;
 #pragma unroll
