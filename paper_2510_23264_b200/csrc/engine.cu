@@ -717,7 +717,11 @@ struct Engine {
 
     // Q/K/V: per unique input a [RB][3D] block (q | k | v, head-major columns)
     const size_t QKV = (size_t)RB * 3 * D;
-    float* qkv = scratch("h_qkv", nu * QKV);
+    // no elevated head in this layer: every Q/K/V value is E4M3-rounded, so
+    // the tensor cores store the codes (1 byte) and attention decodes them
+    const bool qkv8 = tc && P.th_l != l && dk % 32 == 0 && dk <= 128 && g.S <= 128;  // (the warp attention kernel)
+    float* qkv = qkv8 ? nullptr : scratch("h_qkv", nu * QKV);
+    uint8_t* qkvb = qkv8 ? reinterpret_cast<uint8_t*>(scratch("h_qkv8", nu * QKV / 4 + 1)) : nullptr;
     std::vector<GemmJob> gj;
     std::vector<TcJob> tj;
     const PackedB* bq = tc ? &packedB(0, l, kTcE4M3, p_low, P.mode) : nullptr;
@@ -727,11 +731,14 @@ struct Engine {
         if (u_of[j] == (int)u && !(P.th_l == l && P.th_h == jobs[j].head)) hs.push_back(jobs[j].head);
       std::sort(hs.begin(), hs.end());
       hs.erase(std::unique(hs.begin(), hs.end()), hs.end());
-      float* blk = qkv + u * QKV;
+      float* blk = qkv8 ? nullptr : qkv + u * QKV;
+      uint8_t* blk8 = qkv8 ? qkvb + u * QKV : nullptr;
       if (tc && (int)hs.size() == H) {
         TcJob t{};
         t.a_row0 = (int)u * RB, t.b_row0 = 0, t.b_k0 = 0, t.M = RB, t.N = 3 * D, t.K = D;
-        t.out_f32 = blk, t.ldo = 3 * D, t.b_norm = bq->norm.as<float>(), t.prec = p_low;
+        if (qkv8) t.out_pack = blk8;
+        else t.out_f32 = blk;
+        t.ldo = 3 * D, t.b_norm = bq->norm.as<float>(), t.prec = p_low;
         tj.push_back(t);
         continue;
       }
@@ -740,7 +747,9 @@ struct Engine {
           if (tc) {
             TcJob t{};
             t.a_row0 = (int)u * RB, t.b_row0 = c * D + h * dk, t.b_k0 = 0, t.M = RB, t.N = dk, t.K = D;
-            t.out_f32 = blk + c * D + h * dk, t.ldo = 3 * D;
+            if (qkv8) t.out_pack = blk8 + c * D + h * dk;
+            else t.out_f32 = blk + c * D + h * dk;
+            t.ldo = 3 * D;
             t.b_norm = bq->norm.as<float>() + c * D + h * dk, t.prec = p_low;
             tj.push_back(t);
           } else {
@@ -780,9 +789,15 @@ struct Engine {
     for (size_t j = 0; j < jobs.size(); ++j) {
       const int h = jobs[j].head;
       const bool target = P.th_l == l && P.th_h == h;
-      float* blk = qkv + u_of[j] * QKV;
       AttnJob a{};
-      a.q = blk + h * dk, a.k = blk + D + h * dk, a.v = blk + 2 * D + h * dk, a.ld = 3 * D;
+      if (qkv8) {
+        const uint8_t* b8 = qkvb + u_of[j] * QKV;
+        a.q8 = b8 + h * dk, a.k8 = b8 + D + h * dk, a.v8 = b8 + 2 * D + h * dk;
+      } else {
+        float* blk = qkv + u_of[j] * QKV;
+        a.q = blk + h * dk, a.k = blk + D + h * dk, a.v = blk + 2 * D + h * dk;
+      }
+      a.ld = 3 * D;
       a.prec = (target || r4) ? 2 : p_low, a.ldz = dk, a.q0 = last_only ? g.S - 1 : 0;
       a.z = z ? z + j * per : nullptr;
       if (r4 && !target) rq.push_back({a.z, (int64_t)g.S * dk, g.S, dk, dk, 0});

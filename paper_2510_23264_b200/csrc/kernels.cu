@@ -1038,20 +1038,47 @@ __global__ void __launch_bounds__(128) attention_warp_kernel(const AttnJob* __re
   const int item = w % B;
   const int q0 = jb.q0;
   const int64_t base = (int64_t)item * S;
-  // every load in flight at once (cp.async: no register staging, no
-  // generic-pointer aliasing between the global loads and the smem stores)
-  for (int r = 0; r < S; ++r) {
-    const int64_t g = (base + r) * jb.ld;
+  if (jb.q8) {
+    // E4M3 codes: 16-byte loads (16 codes), decoded into the FP32 tiles
+    constexpr int vpr = dk / 16;  // 16-code vectors per row
+    for (int idx = lane; idx < S * vpr; idx += 32) {
+      const int r = idx / vpr, c0 = (idx % vpr) * 16;
+      const int64_t g = (base + r) * jb.ld + c0;
+      const uint4 kw = __ldg(reinterpret_cast<const uint4*>(jb.k8 + g));
+      const uint4 vw = __ldg(reinterpret_cast<const uint4*>(jb.v8 + g));
+      const uint4 qw = r >= q0 ? __ldg(reinterpret_cast<const uint4*>(jb.q8 + g)) : make_uint4(0, 0, 0, 0);
+      const uint32_t kk[4] = {kw.x, kw.y, kw.z, kw.w}, vv[4] = {vw.x, vw.y, vw.z, vw.w},
+                     qq[4] = {qw.x, qw.y, qw.z, qw.w};
 #pragma unroll
-    for (int c = 0; c < NT; ++c) {
-      const int t = lane + 32 * c;
-      if (r >= q0) cp_async4(q + r * ldk + t, jb.q + g + t);
-      cp_async4(k + r * ldk + t, jb.k + g + t);
-      cp_async4(v + r * ldk + t, jb.v + g + t);
+      for (int h = 0; h < 8; ++h) {
+        const int wi = h >> 1, sh = (h & 1) * 16;
+        const float2 kf = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)((kk[wi] >> sh) & 0xFFFFu), __NV_E4M3)));
+        const float2 vf = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)((vv[wi] >> sh) & 0xFFFFu), __NV_E4M3)));
+        k[r * ldk + c0 + 2 * h] = kf.x, k[r * ldk + c0 + 2 * h + 1] = kf.y;
+        v[r * ldk + c0 + 2 * h] = vf.x, v[r * ldk + c0 + 2 * h + 1] = vf.y;
+        if (r >= q0) {
+          const float2 qf = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)((qq[wi] >> sh) & 0xFFFFu), __NV_E4M3)));
+          q[r * ldk + c0 + 2 * h] = qf.x, q[r * ldk + c0 + 2 * h + 1] = qf.y;
+        }
+      }
     }
+    __syncwarp();
+  } else {
+    // every load in flight at once (cp.async: no register staging, no
+    // generic-pointer aliasing between the global loads and the smem stores)
+    for (int r = 0; r < S; ++r) {
+      const int64_t g = (base + r) * jb.ld;
+#pragma unroll
+      for (int c = 0; c < NT; ++c) {
+        const int t = lane + 32 * c;
+        if (r >= q0) cp_async4(q + r * ldk + t, jb.q + g + t);
+        cp_async4(k + r * ldk + t, jb.k + g + t);
+        cp_async4(v + r * ldk + t, jb.v + g + t);
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
   const float scale = __fdiv_rn(1.0f, __fsqrt_rn((float)dk));
   // scores for the causal pairs (i, j <= i), i >= q0
   const int p0 = q0 * (q0 + 1) / 2, np = S * (S + 1) / 2 - p0;

@@ -83,6 +83,9 @@ struct AttnJob {
   int q0;       // first query row computed (S-1: last position only); z rows
                 // are compact: item * (S - q0) + (i - q0)
   float* znorm;  // [z rows] ||z8 row|| * 1.0001 for W_O's certificate (may be null)
+  const uint8_t* q8;  // E4M3 codes of q/k/v instead of q/k/v (row stride ld bytes), or null
+  const uint8_t* k8;
+  const uint8_t* v8;
 };
 void launch_attention(const AttnJob* d_jobs, int n_jobs, int B, int S, int dk, cudaStream_t st);
 
