@@ -367,9 +367,9 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TileMeta&
         // neighbouring rounding candidates (GELU is 1.13-Lipschitz)
         const float vb = (fl >> j) & 1u ? fabsf(v[j]) + 0.02f * fabsf(__uint_as_float(r[j])) : v[j];
         oss = fmaf(vb, vb, oss);
-        // not FMA-safe: nonzero |v| outside [2^-67, 2^64) (exponent field)
-        const uint32_t e = (__float_as_uint(v[j]) >> 23) & 0xFFu;
-        ebad |= (e - 60u) >= 131u ? (e | (__float_as_uint(v[j]) & 0x7FFFFFu)) : 0u;
+        // not FMA-safe: nonzero |v| outside [2^-67, 2^64)
+        const uint32_t ab = __float_as_uint(v[j]) & 0x7FFFFFFFu;
+        ebad |= (uint32_t)(ab - (60u << 23) >= (131u << 23)) & (uint32_t)(ab != 0u);
       }
       obad = obad || ebad != 0;
     }

@@ -1328,6 +1328,48 @@ __global__ void kl_kernel(const float* __restrict__ logits, const float* __restr
 // from L2): an online max / sum-of-exp pass (one exp per element, NaN check),
 // then the KL pass. Same per-element arithmetic as the reference
 // (patching.cpp:108-135); only the double reduction order differs.
+// exp(y) for y <= 0 in double, table-driven: y = (64 k + j) ln2/64 + r with
+// |r| <= ln2/128, exp(y) = 2^k * 2^(j/64) * p(r), p the degree-5 Taylor
+// polynomial (truncation 3.5e-17 relative); ln2/64 split hi (32 bits) + lo so
+// n * hi is exact. ~2-3e-16 relative error, about half the instructions of
+// the libdevice exp. The table lives in shared memory (per-lane indices).
+__constant__ double kExp2Tab[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
+__device__ __forceinline__ double exp_nonpos(double y, const double* tab) {
+  if (y < -744.0) return 0.0;
+  const double n = rint(y * 92.33248261689366);
+  const int ni = (int)n;
+  double r = fma(n, -0.01083042469326756, y);
+  r = fma(n, -2.9815858269852933e-12, r);
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int kk = ni >> 6;  // floor division (arithmetic shift), kk in [-1074, 0]
+  const double t = tab[ni & 63] * p;
+  // 2^kk in two factors so that kk down to -1074 never leaves the exponent range
+  const int k1 = kk / 2, k2 = kk - k1;
+  return t * __longlong_as_double((long long)(k1 + 1023) << 52) *
+         __longlong_as_double((long long)(k2 + 1023) << 52);
+}
+
 constexpr int kKlThreads = 512;
 
 __device__ __forceinline__ void lse_merge(double& m, double& s, double m2, double s2) {
@@ -1348,6 +1390,9 @@ __global__ void __launch_bounds__(kKlThreads) kl_online_kernel(const float* __re
   __shared__ double shm[kKlThreads / 32], shs[kKlThreads / 32];
   __shared__ double sh[32];
   __shared__ int shi[32];
+  __shared__ double tab[64];
+  if (threadIdx.x < 64) tab[threadIdx.x] = kExp2Tab[threadIdx.x];
+  __syncthreads();
   const int r = blockIdx.x;
   const float* q = logits + (int64_t)r * V;
   const int it = item_of[r];
@@ -1362,10 +1407,10 @@ __global__ void __launch_bounds__(kKlThreads) kl_online_kernel(const float* __re
     }
     const double x = (double)f;
     if (x > m) {
-      s = s * exp(m - x) + 1.0;
+      s = s * exp_nonpos(m - x, tab) + 1.0;
       m = x;
     } else {
-      s += exp(x - m);
+      s += exp_nonpos(x - m, tab);
     }
   }
   nan = block_reduce(nan, OrOp(), shi, 0);

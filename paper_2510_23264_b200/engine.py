@@ -413,6 +413,37 @@ class DeltaLEngine:
     def score(self, edge: int, policy: PrecisionPolicy, mode: int) -> float:
         return self.delta_l(edge, policy) if mode == LOSS else self.act_diff(edge, policy)
 
+    def epsilon_precision(self, edge: int, low: PrecisionPolicy) -> float:
+        """|delta_l(e, all_fp32) - delta_l(e, low)| (patching.cpp:266-268)."""
+        return abs(self.delta_l(edge, PrecisionPolicy.all_fp32()) - self.delta_l(edge, low))
+
+
+@dataclass
+class EpsilonReport:
+    eps: np.ndarray   # per present edge, sweep order
+    edges: np.ndarray
+    eps_mean: float
+    eps_max: float
+
+
+def epsilon_report(engine: Engine, mask, prune: PruneConfig) -> EpsilonReport:
+    """The run-acdc epsilon post-pass (proj/tools/circuitquant_main.cpp:280-299):
+    over the edges that survived, the score error the method's precision
+    introduces, |delta_l(e, all_fp32) - delta_l(e, policy(e))|, as two batched
+    device calls (FP32 and the method's per-edge policies) instead of two
+    delta_l per edge."""
+    mask = np.asarray(mask, bool)
+    edges = sweep_order(engine.cfg, mask)
+    if edges.size == 0:
+        return EpsilonReport(np.zeros(0), edges, 0.0, 0.0)
+    full = engine.score_edges(mask, edges, PrecisionPolicy.all_fp32(), False, LOSS)
+    low = engine.score_edges(mask, edges, prune.base_policy, prune.per_edge_policy, LOSS)
+    eps = np.abs(full - low)
+    total = 0.0
+    for x in eps:  # sequential, as the reference accumulates
+        total += float(x)
+    return EpsilonReport(eps, edges, total / eps.size, float(eps.max()))
+
 
 def run_acdc(engine: Engine, prune: PruneConfig) -> CircuitResult:
     """run_acdc (acdc.cpp:23-88): greedy loop in C++ inside libcqg.so."""

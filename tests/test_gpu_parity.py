@@ -348,3 +348,23 @@ def test_gpt2_width_slice_matches_reference():
     assert close(got, want), np.max(np.abs(got - want) / (np.abs(want) + 1e-300))
     assert e.stats()["kernel_launches"] > 0
     e.close()
+
+
+def test_epsilon_report_matches_oracle():
+    """run-acdc's epsilon post-pass (circuitquant_main.cpp:280-299,
+    patching.cpp:266-268) over a partially pruned mask."""
+    w, ds = make(SMALL, 2, 4, 6)
+    p = Port(SMALL, w.mats)
+    e = eng.Engine(w)
+    e.set_dataset(ds, KL)
+    mask = random_mask(p.n_edges, 21, 0.7)
+    cfg = eng.method_prune_config(eng.PAHQ)
+    r = eng.epsilon_report(e, mask, cfg)
+    edges = r.edges
+    full = p.score_edges(ds, edges, Policy.all_fp32(), per_edge=False, metric=KL, mask=mask)
+    low = p.score_edges(ds, edges, Policy.head_quantized(), per_edge=True, metric=KL, mask=mask)
+    want = np.abs(full - low)
+    scale = np.maximum(np.abs(full), np.abs(low))
+    assert np.all(np.abs(r.eps - want) <= RTOL * scale + ATOL), np.max(np.abs(r.eps - want))
+    assert abs(r.eps_max - want.max()) <= RTOL * scale.max() + ATOL
+    e.close()
