@@ -275,7 +275,15 @@ struct Engine {
   bool patch_valid = false;
   Policy patch_policy;
   int patch_tokens = -1;           // 0 clean, 1 corrupt
-  std::map<int, std::unique_ptr<DeviceBuf>> target_cache;  // per source node (per-edge policies)
+  // per source node (per-edge policies). Invalidation bumps target_gen
+  // instead of freeing: the buffers are reused (cudaFree / cudaMalloc of ~150
+  // buffers per new dataset cost ~1 s).
+  struct TargetVal {
+    DeviceBuf buf;
+    uint64_t gen = 0;
+  };
+  std::map<int, TargetVal> target_cache;
+  uint64_t target_gen = 1;
   Trie full;
   // comm
   ncclComm_t comm = nullptr;
@@ -1072,7 +1080,7 @@ struct Engine {
     patch_valid = true;
     patch_policy = base;
     patch_tokens = which;
-    target_cache.clear();
+    ++target_gen;
   }
 
   // out[s] of the full-graph run under policy_for_edge (target = s)
@@ -1083,13 +1091,13 @@ struct Engine {
     }
     *otype = out_type(ps, s);
     auto& c = target_cache[s];
-    if (c) return c->as<float>();
-    c = std::make_unique<DeviceBuf>();
-    c->ensure(patch_run.seg * 4);
+    if (c.gen == target_gen) return c.buf.as<float>();
+    c.buf.ensure(patch_run.seg * 4);
+    c.gen = target_gen;
     const float* in = input_of(full, patch_run, s);
-    if (g.kind[s] == kHead) run_heads(g.layer[s], ps, {{in, g.head[s], c->as<float>(), *otype}}, B);
-    else run_mlp(g.layer[s], ps, {{in, c->as<float>(), *otype}}, B);
-    return c->as<float>();
+    if (g.kind[s] == kHead) run_heads(g.layer[s], ps, {{in, g.head[s], c.buf.as<float>(), *otype}}, B);
+    else run_mlp(g.layer[s], ps, {{in, c.buf.as<float>(), *otype}}, B);
+    return c.buf.as<float>();
   }
 
   // ---- the patched passes of one policy group -------------------------------
@@ -1402,7 +1410,7 @@ struct Engine {
     CK(cudaMemcpyAsync(d_dis.p, dis, (size_t)n * 4, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     patch_valid = false;
-    target_cache.clear();
+    ++target_gen;
   }
 
   void score_edges(const uint8_t* mask, const int* edge_ids, int n, const Policy& base,
