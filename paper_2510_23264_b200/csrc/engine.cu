@@ -1521,7 +1521,7 @@ struct Engine {
     CK(cudaMemcpyAsync(&h_nan, d_nan, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (h_nan) throw Error(2, metric == 0 ? "metric_kl: NaN logits" : "metric_logit_diff: NaN logits");
-    if (world > 1) {
+    if (comm) {  // any communicator, including a 1-rank one (tests the NCCL path on one GPU)
       DeviceBuf& ar = *pool_buf("allreduce", sizeof(double) * std::max(n, 1));
       CK(cudaMemcpyAsync(ar.p, sums.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
       NK(nccl().AllReduce(ar.p, ar.p, (size_t)n, ncclDouble, ncclSum, comm, st));
@@ -1762,7 +1762,6 @@ int cqg_init_comm(cqg_ctx* ctx, const void* unique_id, int rank, int world) {
     if (world < 1 || rank < 0 || rank >= world) throw Error(1, "cqg_init_comm: bad rank/world");
     auto& E = *ctx->e;
     E.rank = rank, E.world = world;
-    if (world == 1) return;
     ncclUniqueId id;
     std::memcpy(&id, unique_id, sizeof id);
     CK(cudaSetDevice(E.device));

@@ -368,3 +368,24 @@ def test_epsilon_report_matches_oracle():
     assert np.all(np.abs(r.eps - want) <= RTOL * scale + ATOL), np.max(np.abs(r.eps - want))
     assert abs(r.eps_max - want.max()) <= RTOL * scale.max() + ATOL
     e.close()
+
+
+def test_nccl_allreduce_path_single_rank():
+    """The multi-GPU combine (per-edge partial sums, ncclAllReduce inside
+    libcqg.so) on a 1-rank communicator: NCCL is resolved from the process,
+    the communicator initialises, and the all-reduced scores equal the
+    single-process ones bit for bit (a sum over one rank)."""
+    w, ds = make(SMALL, 3, 4, 5)
+    a = eng.Engine(w)
+    a.set_dataset(ds, KL)
+    b = eng.Engine(w)
+    b.set_dataset(ds, KL, 0, len(ds))
+    b.init_comm(eng.Engine.unique_id(), 0, 1)
+    mask = np.ones(a.n_edges, bool)
+    edges = np.nonzero(mask)[0]
+    pol = eng.PrecisionPolicy.head_quantized()
+    sa = a.score_edges(mask, edges, pol, True, 0)
+    sb = b.score_edges(mask, edges, pol, True, 0)
+    assert np.array_equal(sa, sb)
+    a.close()
+    b.close()
