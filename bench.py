@@ -39,6 +39,9 @@ CONFIGS = {
                   data="ioi"),
     # configs[0]: toy attention-only transformer, batch 16
     "toy": dict(cfg=formats.ModelConfig(2, 4, 128, 32, 512, 16, 1, 0), items=16, data="random"),
+    # configs[2]: GPT-2-small shape, Greater-Than-shaped prompts (S = 12), E4M3 heads
+    "gpt2s_gt": dict(cfg=formats.ModelConfig(12, 12, 768, 64, 50257, 12, 1, 1), items=64,
+                     data="greater_than"),
     # configs[3]: GPT-2-medium shape, batch 256
     "gpt2m": dict(cfg=formats.ModelConfig(24, 16, 1024, 64, 50257, 16, 1, 1), items=256,
                   data="ioi"),
@@ -62,6 +65,8 @@ def make_inputs(name):
     w = synth.random_weights(cfg, 1)
     if c["data"] == "ioi":
         ds = synth.ioi_dataset(cfg, c["items"], 1)
+    elif c["data"] == "greater_than":
+        ds = synth.greater_than_dataset(cfg, c["items"], 1)
     else:
         ds = synth.random_dataset(cfg, c["items"], 2)
     return cfg, w, ds

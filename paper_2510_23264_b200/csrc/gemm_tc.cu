@@ -652,6 +652,7 @@ constexpr int kFixThreads = 512;
 constexpr int kFixCols = 4;   // flagged columns of one row per work item
 constexpr int kFixPer = 2;    // work items per thread per round
 constexpr int kFixStages = 4;
+constexpr int kFixMaxSplit = 4;  // CTAs sharing one flagged tile when tiles are few
 constexpr int kFixMaxItems = kTcBM * kTcBN / kFixCols + kTcBM;
 constexpr size_t kFixSmem = 1024 + (size_t)kFixStages * (kAStage + kBStage) + 256 +
                             (size_t)kFixMaxItems * sizeof(uint64_t) + 1024;
@@ -814,7 +815,12 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   __syncthreads();
   const uint32_t n_tiles = *L.fix_count;
   uint32_t ld = 0, it = 0;  // TMA loads issued / chunks consumed (ring phases)
-  for (uint32_t ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+  // Few flagged tiles (small launches): split each tile's work items over up
+  // to kFixMaxSplit CTAs (each streams the tile's operands; L2 absorbs the
+  // repeats) so every SM has work.
+  const uint32_t split = n_tiles ? min((uint32_t)kFixMaxSplit, max(1u, gridDim.x / n_tiles)) : 1u;
+  for (uint32_t vt = blockIdx.x; vt < n_tiles * split; vt += gridDim.x) {
+    const uint32_t ti = vt / split, part = vt % split;
     const int tile = (int)L.fix_tiles[ti];
     // ---- work items: row | ncol << 8 | col_c << (16 + 12 c). Columns per item
     // adapt to the tile's flagged count: one per item while the CTA has idle
@@ -871,8 +877,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)
       }
       if (nc) items[pos++] = item | (uint64_t)tid | ((uint64_t)nc << 8);
     }
-    if (tid == 0) L.tile_mark[tile] = 0u;  // ready for the next launch
-    __syncthreads();
+    __syncthreads();  // (tile_mark is cleared by fix_reset_kernel after the launch)
     const int n = wsum[0] + wsum[1] + wsum[2] + wsum[3];
     const TcJob jb = jobs[find_job(jobs, L.n_jobs, tile)];
     const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
@@ -880,7 +885,8 @@ __global__ void __launch_bounds__(kFixThreads, 1)
     const int arow = jb.a_row0 + mt * kTcBM, brow = jb.b_row0 + nt * kTcBN;
     const int kbytes = jb.K * esz;
     const int nk = (kbytes + kBKBytes - 1) / kBKBytes;
-    for (int e0 = 0; e0 < n; e0 += kFixThreads * kFixPer) {
+    const int e_lo = (int)((uint64_t)n * part / split), e_hi = (int)((uint64_t)n * (part + 1) / split);
+    for (int e0 = e_lo; e0 < e_hi; e0 += kFixThreads * kFixPer) {
       if (tid == 0) {  // prologue: fill the ring
         for (int kb = 0; kb < min(kFixStages, nk); ++kb, ++ld) {
           const int s = ld % kFixStages;
@@ -894,10 +900,10 @@ __global__ void __launch_bounds__(kFixThreads, 1)
 #pragma unroll
       for (int j = 0; j < kFixPer; ++j) {
         const int e = e0 + j * kFixThreads + tid;
-        const uint64_t item = e < n ? items[e] : 0ull;
-        w[j].row = e < n ? (int)(item & 0xFF) : -1;
+        const uint64_t item = e < e_hi ? items[e] : 0ull;
+        w[j].row = e < e_hi ? (int)(item & 0xFF) : -1;
         w[j].nc = (int)((item >> 8) & 0xFF);
-        bool ok = e < n && (ELEM == kTcE4M3 || a_fma_safe(L, jb.a_row0 + mt * kTcBM + w[j].row));
+        bool ok = e < e_hi && (ELEM == kTcE4M3 || a_fma_safe(L, jb.a_row0 + mt * kTcBM + w[j].row));
 #pragma unroll
         for (int c = 0; c < kFixCols; ++c) {
           // missing columns of a short item repeat its first (results unused)
@@ -1035,7 +1041,7 @@ void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
 
 void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
   if (L.total_tiles <= 0) return;
-  const int grid = std::min(L.total_tiles, 148);
+  const int grid = std::min(L.total_tiles * kFixMaxSplit, 148);
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFixSmem);
     kern<<<grid, kFixThreads, kFixSmem, st>>>(L, d_jobs);
@@ -1046,10 +1052,16 @@ void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) 
 
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st) { gelu_lut_kernel<<<256, 256, 0, st>>>(lut); }
 
-__global__ void fix_account_kernel(uint32_t* cnt) { cnt[0] = 0; }
+// After a fixup launch: clear the marks of the listed tiles, then the count.
+__global__ void fix_reset_kernel(const uint32_t* tiles, uint32_t* mark, uint32_t* cnt) {
+  const uint32_t n = cnt[0];
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) mark[tiles[i]] = 0u;
+  __syncthreads();
+  if (threadIdx.x == 0) cnt[0] = 0;
+}
 
-void launch_fix_account(uint32_t* cnt, cudaStream_t st) {
-  fix_account_kernel<<<1, 1, 0, st>>>(cnt);
+void launch_fix_account(const uint32_t* tiles, uint32_t* mark, uint32_t* cnt, cudaStream_t st) {
+  fix_reset_kernel<<<1, 256, 0, st>>>(tiles, mark, cnt);
 }
 
 void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,

@@ -68,8 +68,8 @@ void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
 void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
 // lut[b] = enc_bf16(round_bf16(gelu_ref(dec_bf16(b)))) (glibc-exact erff)
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st);
-// cnt[0] = 0 (the listed-tile count, after the fixup has consumed it)
-void launch_fix_account(uint32_t* cnt, cudaStream_t st);
+// tile_mark[t] = 0 for the listed tiles, then cnt[0] = 0 (after the fixup)
+void launch_fix_account(const uint32_t* tiles, uint32_t* mark, uint32_t* cnt, cudaStream_t st);
 // ||row|| of a packed [rows][K] operand (elements starting at col k0)
 void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,
                     cudaStream_t st);
