@@ -563,7 +563,7 @@ void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float
     // rows per warp: 8 (4 for D > 1024) on big launches; fewer when the
     // launch would not give every SM several warps (the per-source baseline
     // runs: 1024-row launches), so more chains run side by side
-    int rw = D <= 1024 ? 8 : 4;
+    int rw = D <= 1024 ? 4 : 2;  // measured: 4 rows per warp beats 8 and 2 at D = 768
     const int64_t total = (int64_t)max_rows * n_jobs;
     while (rw > 1 && total / rw < 4 * 148) rw >>= 1;
     const size_t smem = sizeof(float) * kLsWarps * rw * (D + 4);
