@@ -11,6 +11,9 @@ for w in $what; do case $w in
 tests)
   timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
   tail -5 gpurun_out/pytest_gpu.log ;;
+smoke)
+  timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
+  tail -3 gpurun_out/smoke.log ;;
 bench)
   timeout 1200 python bench.py --acdc > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench exit $?"
   cat gpurun_out/bench.json ;;
