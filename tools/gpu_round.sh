@@ -15,7 +15,7 @@ smoke)
   timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
   tail -3 gpurun_out/smoke.log ;;
 bench)
-  timeout 1200 python bench.py --acdc > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench exit $?"
+  timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench exit $?"
   cat gpurun_out/bench.json ;;
 mb)
   ./tools/mb/f32x2.bin > gpurun_out/mb_f32x2.txt 2>&1; cat gpurun_out/mb_f32x2.txt ;;
