@@ -102,6 +102,15 @@ int cqg_quantize_matrix(cqg_ctx* ctx, int matrix_index, int precision, int low_m
 int cqg_forward(cqg_ctx* ctx, const int32_t* tokens, const uint8_t* mask, const cqg_policy* pol,
                 int patch_edge, const float* patch_value, float* outs_host);
 
+/* circuit_stats (proj/src/eval.cpp:960-985) over the dataset's local items,
+ * at FP32: the clean, corrupt and circuit runs' last-row logit differences
+ * (metric_logit_diff, patching.cpp:140-149). The circuit run keeps the full
+ * graph and gives every edge absent from `mask` its source's output from the
+ * corrupt run. faithfulness / task_accuracy (eval.cpp:1240-1254) follow on the
+ * host. Each output array has one entry per local item. */
+int cqg_circuit_stats(cqg_ctx* ctx, const uint8_t* mask, double* clean_ld, double* corrupt_ld,
+                      double* circuit_ld);
+
 /* Graph facts (model.cpp:166-246). */
 int cqg_graph_info(const cqg_config* cfg, int* n_nodes, int* n_edges);
 int cqg_graph_edges(const cqg_config* cfg, int32_t* edge_src, int32_t* edge_dst);

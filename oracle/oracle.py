@@ -170,6 +170,14 @@ class Ref:
                                             C.byref(auc)))
         return auc.value, tpr, fpr, kept
 
+    def faithfulness(self, taskdir, mask):
+        """(faithfulness, task_accuracy) of the reference (eval.cpp:1240-1254)."""
+        m = np.ascontiguousarray(mask, np.uint8)
+        f, a = C.c_double(), C.c_double()
+        self.check(self.lib.cqref_faithfulness(taskdir.encode(), m.ctypes.data_as(C.c_void_p), m.size,
+                                               C.byref(f), C.byref(a)))
+        return f.value, a.value
+
     def method_config(self, method, bits=8) -> Prune:
         p = Prune()
         self.check(self.lib.cqref_method_config(method, bits, C.byref(p)))

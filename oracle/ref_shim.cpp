@@ -246,6 +246,17 @@ int cqref_roc_sweep(const char* dir, int method, int bits, int metric, const dou
   });
 }
 
+// faithfulness / task_accuracy (eval.cpp:1240-1254) of a saved planted task
+// under an edge mask (FP32 circuit runs; absent edges read the corrupt run).
+int cqref_faithfulness(const char* dir, const uint8_t* mask, int n, double* faith, double* acc) {
+  return guarded([&] {
+    PlantedTask t = load_task(dir);
+    std::vector<bool> m(mask, mask + n);
+    *faith = faithfulness(t, m);
+    *acc = task_accuracy(t, m);
+  });
+}
+
 int cqref_method_config(int method, int bits, cqref_prune* out) {
   return guarded([&] {
     PruneConfig pc = method_prune_config(static_cast<Method>(method), bits);

@@ -262,6 +262,7 @@ struct Engine {
   // dataset
   int B = 0, item_off = 0, item_total = 0, metric = 0;
   DeviceBuf d_clean, d_corrupt, d_ans, d_dis;
+  std::vector<int> h_ans, h_dis;
   // scratch
   std::map<std::string, std::unique_ptr<DeviceBuf>> pool;
   DeviceBuf zero;
@@ -1400,6 +1401,8 @@ struct Engine {
     }
     if (total < n || off < 0 || off + n > total) throw Error(1, "set_dataset: bad shard bounds");
     B = n, item_off = off, item_total = total, metric = met;
+    h_ans.assign(ans, ans + n);
+    h_dis.assign(dis, dis + n);
     d_clean.ensure((size_t)n * g.S * 4);
     d_corrupt.ensure((size_t)n * g.S * 4);
     d_ans.ensure((size_t)n * 4);
@@ -1557,6 +1560,50 @@ struct Engine {
 
   // Debug forward of one item (model.cpp:556-757) with direct per-receiver
   // folds (independent of the trie planner; used to cross-check it).
+  // One item's forward (model.cpp:556-757) with direct per-receiver folds
+  // (independent of the trie planner; used to cross-check it). Node outputs
+  // go to O ([N][SEG], FP32 outputs: packed types are not requested here),
+  // the receiver inputs to I, the logits ([S][V]) to LG. An edge that the mask
+  // drops contributes nothing -- unless absent_src is given, in which case it
+  // contributes absent_src's output of its source (circuit_stats'
+  // "absent edges read the corrupt run", eval.cpp:960-980).
+  void forward_item(const int* d_tok, const uint8_t* mask, const Policy& P, int patch_edge,
+                    const float* d_patch, float* O, float* I, float* LG, const float* absent_src) {
+    const size_t SEG = segf(1);
+    auto input = [&](int w) {
+      std::vector<FoldOp> ops;
+      for (int e : g.in_edges[w]) {
+        const float* b;
+        if (mask && !mask[e]) {
+          if (!absent_src) continue;
+          b = absent_src + (size_t)g.esrc[e] * SEG;
+        } else {
+          b = e == patch_edge ? d_patch : O + (size_t)g.esrc[e] * SEG;
+        }
+        ops.push_back({ops.empty() ? nullptr : CQG_REG_PREV, b, nullptr});
+      }
+      if (ops.empty()) {
+        CK(cudaMemsetAsync(I + (size_t)w * SEG, 0, SEG * 4, st));
+      } else {
+        ops.back().dst = I + (size_t)w * SEG;
+        fold(ops, {{0, (int)ops.size()}}, SEG);
+      }
+      return (const float*)(I + (size_t)w * SEG);
+    };
+    for (int s = 0; s < g.n_stages; ++s) {
+      const auto& nodes = g.stage_nodes[s];
+      if (nodes.empty()) continue;  // MLP stages of attention-only models
+      const int k = g.kind[nodes[0]];
+      if (k == kEmbed) run_embed(P, d_tok, O, 1);
+      else if (k == kHead) {
+        std::vector<HeadIO> hj;
+        for (int w : nodes) hj.push_back({input(w), g.head[w], O + (size_t)w * SEG, kOutF32});
+        run_heads(g.layer[nodes[0]], P, hj, 1);
+      } else if (k == kMlp) run_mlp(g.layer[nodes[0]], P, {{input(nodes[0]), O + (size_t)nodes[0] * SEG, kOutF32}}, 1);
+      else run_unembed(P, {{input(g.unembed), LG, kOutF32}}, 1, true);
+    }
+  }
+
   void forward_single(const int* tok_host, const uint8_t* mask, const Policy& P, int patch_edge,
                       const float* patch_host, float* outs_host) {
     check_policy(P);
@@ -1574,40 +1621,48 @@ struct Engine {
     DeviceBuf& pv = *pool_buf("f_patch", SEG * 4);
     CK(cudaMemcpyAsync(tk.p, tok_host, (size_t)g.S * 4, cudaMemcpyHostToDevice, st));
     if (patch_edge >= 0) CK(cudaMemcpyAsync(pv.p, patch_host, SEG * 4, cudaMemcpyHostToDevice, st));
-    float* O = outs.as<float>();
-    float* I = ins.as<float>();
-    auto input = [&](int w) {
-      std::vector<FoldOp> ops;
-      for (int e : g.in_edges[w]) {
-        if (mask && !mask[e]) continue;
-        const float* b = e == patch_edge ? pv.as<float>() : O + (size_t)g.esrc[e] * SEG;
-        ops.push_back({ops.empty() ? nullptr : CQG_REG_PREV, b, nullptr});
-      }
-      if (ops.empty()) {
-        CK(cudaMemsetAsync(I + (size_t)w * SEG, 0, SEG * 4, st));
-      } else {
-        ops.back().dst = I + (size_t)w * SEG;
-        fold(ops, {{0, (int)ops.size()}}, SEG);
-      }
-      return (const float*)(I + (size_t)w * SEG);
-    };
-    for (int s = 0; s < g.n_stages; ++s) {
-      const auto& nodes = g.stage_nodes[s];
-      if (nodes.empty()) continue;  // MLP stages of attention-only models
-      const int k = g.kind[nodes[0]];
-      if (k == kEmbed) run_embed(P, tk.as<int>(), O, 1);
-      else if (k == kHead) {
-        std::vector<HeadIO> hj;
-        for (int w : nodes) hj.push_back({input(w), g.head[w], O + (size_t)w * SEG});
-        run_heads(g.layer[nodes[0]], P, hj, 1);
-      } else if (k == kMlp) run_mlp(g.layer[nodes[0]], P, {{input(nodes[0]), O + (size_t)nodes[0] * SEG}}, 1);
-      else run_unembed(P, {{input(g.unembed), lg.as<float>()}}, 1, true);
-    }
-    CK(cudaMemcpyAsync(outs_host, O, (size_t)(g.N - 1) * SEG * 4, cudaMemcpyDeviceToHost, st));
+    forward_item(tk.as<int>(), mask, P, patch_edge, pv.as<float>(), outs.as<float>(), ins.as<float>(),
+                 lg.as<float>(), nullptr);
+    CK(cudaMemcpyAsync(outs_host, outs.p, (size_t)(g.N - 1) * SEG * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(outs_host + (size_t)(g.N - 1) * SEG, lg.p, (size_t)g.S * g.V * 4,
                        cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   }
+
+  // circuit_stats (eval.cpp:960-985) for the local items at FP32: the clean,
+  // corrupt and circuit runs' last-row logit differences. The circuit run
+  // keeps the full graph and feeds every absent edge its source's output from
+  // the corrupt run.
+  void circuit_stats(const uint8_t* mask, double* clean_ld, double* corrupt_ld, double* circuit_ld) {
+    if (B == 0) throw Error(1, "circuit_stats: no dataset (call cqg_set_dataset)");
+    if (!mask) throw Error(1, "circuit_stats: null mask");
+    const Policy P = Policy::from(cqg_policy{2, 2, 2, 2, 0, -1, -1, -1});  // all_fp32
+    const size_t SEG = segf(1);
+    DeviceBuf& oc = *pool_buf("cs_corr", (size_t)g.N * SEG * 4);
+    DeviceBuf& o = *pool_buf("f_outs", (size_t)g.N * SEG * 4);
+    DeviceBuf& ins = *pool_buf("f_ins", (size_t)g.N * SEG * 4);
+    DeviceBuf& lg = *pool_buf("f_logits", (size_t)g.S * g.V * 4);
+    std::vector<float> row(g.V);
+    auto ld = [&](int i) {  // metric_logit_diff of the last row (patching.cpp:140-149)
+      CK(cudaMemcpyAsync(row.data(), lg.as<float>() + (size_t)(g.S - 1) * g.V, (size_t)g.V * 4,
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (float x : row)
+        if (x != x) throw Error(2, "metric_logit_diff: NaN logits");
+      return (double)row[h_ans[i]] - (double)row[h_dis[i]];
+    };
+    for (int i = 0; i < B; ++i) {
+      const int* clean = d_clean.as<int>() + (size_t)i * g.S;
+      const int* corr = d_corrupt.as<int>() + (size_t)i * g.S;
+      forward_item(corr, nullptr, P, -1, nullptr, oc.as<float>(), ins.as<float>(), lg.as<float>(), nullptr);
+      corrupt_ld[i] = ld(i);
+      forward_item(clean, nullptr, P, -1, nullptr, o.as<float>(), ins.as<float>(), lg.as<float>(), nullptr);
+      clean_ld[i] = ld(i);
+      forward_item(clean, mask, P, -1, nullptr, o.as<float>(), ins.as<float>(), lg.as<float>(), oc.as<float>());
+      circuit_ld[i] = ld(i);
+    }
+  }
+
 
   void run_acdc(const cqg_prune& c, int* steps, uint8_t* final_mask, double* last_score, int* n_rec,
                 int* rs, int* re, double* rsc, uint8_t* rk, int cap) {
@@ -1811,6 +1866,15 @@ int cqg_forward(cqg_ctx* ctx, const int32_t* tokens, const uint8_t* mask, const 
     if (!ctx || !tokens || !pol || !outs_host) throw Error(1, "cqg_forward: null argument");
     CK(cudaSetDevice(ctx->e->device));
     ctx->e->forward_single(tokens, mask, cqg::Policy::from(*pol), patch_edge, patch_value, outs_host);
+  });
+}
+
+int cqg_circuit_stats(cqg_ctx* ctx, const uint8_t* mask, double* clean_ld, double* corrupt_ld,
+                      double* circuit_ld) {
+  return guarded([&] {
+    if (!ctx || !mask || !clean_ld || !corrupt_ld || !circuit_ld) throw Error(1, "cqg_circuit_stats: null argument");
+    CK(cudaSetDevice(ctx->e->device));
+    ctx->e->circuit_stats(mask, clean_ld, corrupt_ld, circuit_ld);
   });
 }
 

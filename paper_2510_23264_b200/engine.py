@@ -186,6 +186,7 @@ def load_library():
                                  C.POINTER(C.c_int), vp, vp, vp, vp, C.c_int]
     lib.cqg_quantize_matrix.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
     lib.cqg_forward.argtypes = [vp, vp, vp, C.POINTER(CqgPolicy), C.c_int, vp, vp]
+    lib.cqg_circuit_stats.argtypes = [vp, vp, vp, vp, vp]
     lib.cqg_graph_info.argtypes = [C.POINTER(CqgConfig), C.POINTER(C.c_int), C.POINTER(C.c_int)]
     lib.cqg_graph_edges.argtypes = [C.POINTER(CqgConfig), vp, vp]
     lib.cqg_last_stats.argtypes = [vp, C.POINTER(CqgStats)]
@@ -416,6 +417,48 @@ class DeltaLEngine:
     def epsilon_precision(self, edge: int, low: PrecisionPolicy) -> float:
         """|delta_l(e, all_fp32) - delta_l(e, low)| (patching.cpp:266-268)."""
         return abs(self.delta_l(edge, PrecisionPolicy.all_fp32()) - self.delta_l(edge, low))
+
+
+@dataclass
+class CircuitStats:
+    clean_ld: np.ndarray
+    corrupt_ld: np.ndarray
+    circuit_ld: np.ndarray
+
+
+def _mean(xs) -> float:
+    s = 0.0
+    for x in xs:  # sequential, as eval.cpp's mean()
+        s += float(x)
+    return s / len(xs)
+
+
+def circuit_stats(engine: "Engine", mask) -> CircuitStats:
+    """eval.cpp:960-985 on the GPU: clean / corrupt / circuit last-row logit
+    differences at FP32 for the engine's dataset (absent edges read the
+    corrupt run)."""
+    m = np.ascontiguousarray(np.asarray(mask, bool), np.uint8)
+    if m.size != engine.n_edges:
+        raise ValueError("circuit_stats: mask size mismatch")
+    n = engine.n_items
+    cl, co, ci = np.empty(n), np.empty(n), np.empty(n)
+    _check(engine.lib.cqg_circuit_stats(engine.h, _vp(m), _vp(cl), _vp(co), _vp(ci)))
+    return CircuitStats(cl, co, ci)
+
+
+def faithfulness(engine: "Engine", mask) -> float:
+    """eval.cpp:1240-1247"""
+    st = circuit_stats(engine, mask)
+    denom = _mean(st.clean_ld) - _mean(st.corrupt_ld)
+    if abs(denom) < 1e-9:
+        raise RuntimeError("faithfulness: degenerate clean-corrupt gap")
+    return (_mean(st.circuit_ld) - _mean(st.corrupt_ld)) / denom
+
+
+def task_accuracy(engine: "Engine", mask) -> float:
+    """eval.cpp:1249-1254"""
+    st = circuit_stats(engine, mask)
+    return float(sum(1 for ld in st.circuit_ld if ld > 0.0)) / len(st.circuit_ld)
 
 
 @dataclass

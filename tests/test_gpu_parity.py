@@ -389,3 +389,23 @@ def test_nccl_allreduce_path_single_rank():
     assert np.array_equal(sa, sb)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("preset", ["standard", "underflow", "interference", "two_hop", "carrier"])
+def test_faithfulness_and_accuracy_match_reference(preset):
+    """circuit_stats / faithfulness / task_accuracy (eval.cpp:960-985,
+    1240-1254) on the GPU against the reference library's values
+    (tests/golden/make_faithfulness.py)."""
+    gold = json.load(open(os.path.join(GOLDEN, "faithfulness.json")))
+    d = os.path.join(GOLDEN, f"planted_{preset}_s1")
+    w = formats.load_weights(os.path.join(d, "weights.bin"))
+    ds = formats.load_dataset_jsonl(os.path.join(d, "dataset.jsonl"))
+    e = eng.Engine(w)
+    e.set_dataset(ds, LOGITDIFF)
+    for name in ("ground_truth", "random"):
+        g = gold[f"{preset}/{name}"]
+        mask = np.array(g["mask"], bool)
+        f, a = float.fromhex(g["faithfulness"]), float.fromhex(g["task_accuracy"])
+        assert abs(eng.faithfulness(e, mask) - f) <= RTOL * abs(f) + 1e-12, (name, f)
+        assert eng.task_accuracy(e, mask) == a, name
+    e.close()
