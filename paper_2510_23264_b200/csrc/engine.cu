@@ -647,8 +647,7 @@ struct Engine {
       CK(cudaMemcpy(&fixed1, fix_cnt.as<uint8_t>() + 8, 8, cudaMemcpyDeviceToHost));
       kprof[fname].flops += 2.0 * jobs[0].K * (double)(fixed1 - fixed0);
     }
-    launch_fix_account(L.fix_tiles, L.tile_mark, L.fix_count, st);
-    launched();
+    launched();  // (the fixup kernel's last CTA resets the tile marks and count)
   }
 
   // Storage type of node w's output under policy P when the caller accepts

@@ -877,7 +877,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)
       }
       if (nc) items[pos++] = item | (uint64_t)tid | ((uint64_t)nc << 8);
     }
-    __syncthreads();  // (tile_mark is cleared by fix_reset_kernel after the launch)
+    __syncthreads();  // (tile_mark is cleared by the last CTA at the end)
     const int n = wsum[0] + wsum[1] + wsum[2] + wsum[3];
     const TcJob jb = jobs[find_job(jobs, L.n_jobs, tile)];
     const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
@@ -932,6 +932,23 @@ __global__ void __launch_bounds__(kFixThreads, 1)
       }
     }
     __syncthreads();  // item list reuse
+  }
+  // The last CTA to finish clears the listed tiles' marks and the count for
+  // the next launch (fix_count[1] counts finished CTAs).
+  __shared__ int last_cta;
+  if (tid == 0) {
+    __threadfence();
+    last_cta = atomicAdd(L.fix_count + 1, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last_cta) {
+    __threadfence();
+    for (uint32_t i = tid; i < n_tiles; i += blockDim.x) L.tile_mark[L.fix_tiles[i]] = 0u;
+    __syncthreads();
+    if (tid == 0) {
+      L.fix_count[0] = 0u;
+      L.fix_count[1] = 0u;
+    }
   }
 }
 
@@ -1052,17 +1069,6 @@ void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) 
 
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st) { gelu_lut_kernel<<<256, 256, 0, st>>>(lut); }
 
-// After a fixup launch: clear the marks of the listed tiles, then the count.
-__global__ void fix_reset_kernel(const uint32_t* tiles, uint32_t* mark, uint32_t* cnt) {
-  const uint32_t n = cnt[0];
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) mark[tiles[i]] = 0u;
-  __syncthreads();
-  if (threadIdx.x == 0) cnt[0] = 0;
-}
-
-void launch_fix_account(const uint32_t* tiles, uint32_t* mark, uint32_t* cnt, cudaStream_t st) {
-  fix_reset_kernel<<<1, 256, 0, st>>>(tiles, mark, cnt);
-}
 
 void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,
                     cudaStream_t st) {

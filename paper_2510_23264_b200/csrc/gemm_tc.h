@@ -53,7 +53,8 @@ struct TcLaunch {
                         // valid for the 32 x 64 parts whose bit is set in tile_mark
   uint32_t* fix_tiles;  // [total_tiles] tiles with flagged elements
   uint32_t* tile_mark;  // [total_tiles] flagged-part bits (q + 4*half); zero between launches
-  uint32_t* fix_count;  // [0] tiles listed by this launch (zeroed after it),
+  uint32_t* fix_count;  // [0] tiles listed by this launch, [1] fixup CTAs finished (both
+                        //   zeroed by the fixup's last CTA),
                         // [2..3] u64 running total of flagged elements
   float kappa;
   int fix_cpi;  // fixup columns per work item: 0 adaptive, else 1 / 2 / 4
@@ -68,8 +69,6 @@ void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
 void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
 // lut[b] = enc_bf16(round_bf16(gelu_ref(dec_bf16(b)))) (glibc-exact erff)
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st);
-// tile_mark[t] = 0 for the listed tiles, then cnt[0] = 0 (after the fixup)
-void launch_fix_account(const uint32_t* tiles, uint32_t* mark, uint32_t* cnt, cudaStream_t st);
 // ||row|| of a packed [rows][K] operand (elements starting at col k0)
 void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,
                     cudaStream_t st);
