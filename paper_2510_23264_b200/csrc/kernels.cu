@@ -794,6 +794,12 @@ __device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
 __device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
   return (f2_t)__float_as_uint(lo) | ((f2_t)__float_as_uint(hi) << 32);
 }
+// (a, a) through mov.b64: ptxas folds it into FFMA2's scalar-broadcast operand
+__device__ __forceinline__ f2_t f2_dup(float a) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(a));
+  return r;
+}
 __device__ __forceinline__ float f2_lo(f2_t v) { return __uint_as_float((uint32_t)v); }
 __device__ __forceinline__ float f2_hi(f2_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
 
@@ -811,7 +817,7 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __
   const int local = t - tile_start[lo];
   const int tiles_m = (jb.M + kXBM - 1) / kXBM;
   const int m0 = (local % tiles_m) * kXBM, n0 = (local / tiles_m) * kXBN;
-  __shared__ __align__(16) float2 As[2][kXBK][kXBM];  // (a, a) broadcast pairs
+  __shared__ __align__(16) float As[2][kXBK][kXBM];  // used as the FFMA2 scalar-broadcast operand
   __shared__ __align__(16) float Bs[2][kXBK][kXBN];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
@@ -830,7 +836,7 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __
   };
   auto store = [&](int buf) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) As[buf][a_k + i][a_r] = make_float2(ra[i], ra[i]);
+    for (int i = 0; i < 4; ++i) As[buf][a_k + i][a_r] = ra[i];
     *reinterpret_cast<float4*>(&Bs[buf][b_k][b_n]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
   };
   // acc[i][p]: row i (ty*4 + i, then 64 + ty*4 + i - 4), column pair p
@@ -851,12 +857,11 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __
     auto step = [&](int kk) {
       f2_t a[8], b[4];
       {
-        const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][ty * 4]);
-        const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][ty * 4 + 2]);
-        const ulonglong2 a2 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][64 + ty * 4]);
-        const ulonglong2 a3 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][64 + ty * 4 + 2]);
-        a[0] = a0.x, a[1] = a0.y, a[2] = a1.x, a[3] = a1.y;
-        a[4] = a2.x, a[5] = a2.y, a[6] = a3.x, a[7] = a3.y;
+        // (a, a): ptxas folds the pair into FFMA2's scalar-broadcast operand
+        const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+        const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
+        a[0] = f2_dup(a0.x), a[1] = f2_dup(a0.y), a[2] = f2_dup(a0.z), a[3] = f2_dup(a0.w);
+        a[4] = f2_dup(a1.x), a[5] = f2_dup(a1.y), a[6] = f2_dup(a1.z), a[7] = f2_dup(a1.w);
         const ulonglong2 b0 = *reinterpret_cast<const ulonglong2*>(&Bs[buf][kk][tx * 4]);
         const ulonglong2 b1 = *reinterpret_cast<const ulonglong2*>(&Bs[buf][kk][64 + tx * 4]);
         b[0] = b0.x, b[1] = b0.y, b[2] = b1.x, b[3] = b1.y;
@@ -916,7 +921,7 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_wide_kernel(const GemmJob* 
   const int local = t - tile_start[lo];
   const int tiles_m = (jb.M + kSBM - 1) / kSBM;
   const int m0 = (local % tiles_m) * kSBM, n0 = (local / tiles_m) * kSBN;
-  __shared__ __align__(16) float2 As[2][kSBK][kSBM];  // (a, a) broadcast pairs
+  __shared__ __align__(16) float As[2][kSBK][kSBM];  // FFMA2 scalar-broadcast operand
   __shared__ __align__(16) float Bs[2][kSBK][kSBN];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
@@ -938,7 +943,7 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_wide_kernel(const GemmJob* 
   };
   auto store = [&](int buf) {
 #pragma unroll
-    for (int i = 0; i < 2; ++i) As[buf][a_k + i][a_r] = make_float2(ra[i], ra[i]);
+    for (int i = 0; i < 2; ++i) As[buf][a_k + i][a_r] = ra[i];
     *reinterpret_cast<float4*>(&Bs[buf][b_k][b_n]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
     *reinterpret_cast<float4*>(&Bs[buf][b_k][b_n + 4]) = make_float4(rb[4], rb[5], rb[6], rb[7]);
   };
@@ -958,9 +963,8 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_wide_kernel(const GemmJob* 
     const int kl = min(kSBK, jb.K - k0);
     auto step = [&](int kk) {
       f2_t a[4], b[8];
-      const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][ty * 4]);
-      const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(&As[buf][kk][ty * 4 + 2]);
-      a[0] = a0.x, a[1] = a0.y, a[2] = a1.x, a[3] = a1.y;
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      a[0] = f2_dup(a0.x), a[1] = f2_dup(a0.y), a[2] = f2_dup(a0.z), a[3] = f2_dup(a0.w);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const ulonglong2 bq = *reinterpret_cast<const ulonglong2*>(&Bs[buf][kk][q * 64 + tx * 4]);
