@@ -37,8 +37,12 @@ struct TileMeta {
   float nbmax[kTcBN / 32];       // max of nb over each 32-column chunk
 };
 constexpr size_t kMetaBytes = (sizeof(TileMeta) + 15) & ~size_t(15);
+// TMEM accumulator buffers (128 columns each; 4 = all 512 columns): the MMA
+// and the metadata warp run up to kAccBufs - 1 tiles ahead of the epilogue,
+// which hides the per-tile TMA -> MMA -> commit latency of short-K GEMMs (W_O).
+constexpr int kAccBufs = 4;
 constexpr size_t kSmemBytes = 1024 + (size_t)kStages * (kAStage + kBStage) + 256 +
-                              kEpiWarps * kStageFloats * sizeof(float) + 2 * kMetaBytes +
+                              kEpiWarps * kStageFloats * sizeof(float) + kAccBufs * kMetaBytes +
                               2 * 2 * 13 * 128;  // GELU LUT slice (kGeluSm uint16)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -489,14 +493,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sB = smem + kStages * kAStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBStage);
   uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;  // [2]
-  uint64_t* tempty = tfull + 2;       // [2]
-  uint64_t* mfull = tempty + 2;   // [2] metadata ready (32 arrivals)
-  uint64_t* mempty = mfull + 2;   // [2] metadata consumed (kEpiWarps arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mempty + 2);
+  uint64_t* tfull = empty + kStages;   // [kAccBufs]
+  uint64_t* tempty = tfull + kAccBufs;  // [kAccBufs]
+  uint64_t* mfull = tempty + kAccBufs;  // [kAccBufs] metadata ready (32 arrivals)
+  uint64_t* mempty = mfull + kAccBufs;  // [kAccBufs] metadata consumed (kEpiWarps arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mempty + kAccBufs);
   float* stage_all = reinterpret_cast<float*>(smem + kStages * (kAStage + kBStage) + 256);
   TileMeta* meta = reinterpret_cast<TileMeta*>(stage_all + (size_t)kEpiWarps * kStageFloats);
-  uint16_t* gelu_s = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(meta) + 2 * kMetaBytes);
+  uint16_t* gelu_s = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(meta) + kAccBufs * kMetaBytes);
   if (EPI == 1 && PREC == 1)  // the GELU LUT slice |x| in [2^-10, 8) (made visible by the barrier below)
     for (int i = threadIdx.x; i < kGeluSm; i += blockDim.x) {
       const int sg = i / (kGeluNE * 128), rem = i % (kGeluNE * 128);
@@ -512,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kAccBufs; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], kEpiWarps);
       mbar_init(&mfull[b], 32);
@@ -523,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(2 * kTcBN));
+                 "r"(kAccBufs * kTcBN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -557,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const TcJob& jb = jobs[find_job(jobs, L.n_jobs, tile)];
         const int kbytes = jb.K * esz;
         const int nk = (kbytes + kBKBytes - 1) / kBKBytes;
-        const uint32_t b = ti & 1, bph = (ti >> 1) & 1;
+        const uint32_t b = ti % kAccBufs, bph = (ti / kAccBufs) & 1;
         mbar_wait(&tempty[b], bph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t tacc = tmem + b * kTcBN;
@@ -578,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 2) {  // tile metadata, one TMEM buffer ahead of the epilogue
     uint32_t ti = 0;
     for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x, ++ti) {
-      const uint32_t b = ti & 1, bph = (ti >> 1) & 1;
+      const uint32_t b = ti % kAccBufs, bph = (ti / kAccBufs) & 1;
       mbar_wait(&mempty[b], bph ^ 1);
       TileMeta& md = meta[b];
       const int ji = find_job(jobs, L.n_jobs, tile);
@@ -612,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
     uint32_t ti = 0;
     for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x, ++ti) {
-      const uint32_t b = ti & 1, bph = (ti >> 1) & 1;
+      const uint32_t b = ti % kAccBufs, bph = (ti / kAccBufs) & 1;
       mbar_wait(&mfull[b], bph);
       mbar_wait(&tfull[b], bph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kTcBN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kAccBufs * kTcBN));
   }
 }
 
