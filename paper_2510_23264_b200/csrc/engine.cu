@@ -628,8 +628,14 @@ struct Engine {
       CK(cudaStreamSynchronize(st));
       CK(cudaMemcpy(&fixed0, fix_cnt.as<uint8_t>() + 8, 8, cudaMemcpyDeviceToHost));
     }
-    reserve(up_bytes(jobs.size(), sizeof(TcJob)));
+    std::vector<int> tj_map((size_t)total);
+    for (size_t j = 0; j < jobs.size(); ++j) {
+      const int end = j + 1 < jobs.size() ? jobs[j + 1].tile0 : total;
+      for (int t = jobs[j].tile0; t < end; ++t) tj_map[(size_t)t] = (int)j;
+    }
+    reserve(up_bytes(jobs.size(), sizeof(TcJob)) + up_bytes(tj_map.size(), sizeof(int)));
     const TcJob* dj = upload(jobs);
+    L.tile_job = upload(tj_map);
     {
       Prof pf(this, elem == kTcBF16 ? (std::string("gemm_tc_bf16_") + name).c_str()
                                     : (std::string("gemm_tc_fp8_") + name).c_str(),

@@ -169,6 +169,14 @@ __device__ __forceinline__ int find_job(const TcJob* jobs, int n, int t) {
   return lo;
 }
 
+// job owning a tile: one load from the host-built tile -> job map (the
+// binary search over the job list is a chain of dependent loads, a visible
+// per-tile latency for the single-thread producer / MMA and the metadata warp
+// on short-K launches with thousands of jobs)
+__device__ __forceinline__ int job_of(const TcLaunch& L, const TcJob* jobs, int t) {
+  return L.tile_job ? __ldg(L.tile_job + t) : find_job(jobs, L.n_jobs, t);
+}
+
 __device__ __forceinline__ void store_out(const TcJob& jb, int row, int col, float v) {
   const int64_t o = (int64_t)row * jb.ldo + col;
   if (jb.out_f32) jb.out_f32[o] = v;
@@ -539,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {  // TMA producer
       uint32_t it = 0;
       for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x) {
-        const TcJob& jb = jobs[find_job(jobs, L.n_jobs, tile)];
+        const TcJob& jb = jobs[job_of(L, jobs, tile)];
         const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
         const int mt = (tile - jb.tile0) / tiles_n, nt = (tile - jb.tile0) % tiles_n;
         const int nk = (jb.K * esz + kBKBytes - 1) / kBKBytes;
@@ -558,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = instr_desc<ELEM>();
       uint32_t it = 0, ti = 0;
       for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x, ++ti) {
-        const TcJob& jb = jobs[find_job(jobs, L.n_jobs, tile)];
+        const TcJob& jb = jobs[job_of(L, jobs, tile)];
         const int kbytes = jb.K * esz;
         const int nk = (kbytes + kBKBytes - 1) / kBKBytes;
         const uint32_t b = ti % kAccBufs, bph = (ti / kAccBufs) & 1;
@@ -585,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t b = ti % kAccBufs, bph = (ti / kAccBufs) & 1;
       mbar_wait(&mempty[b], bph ^ 1);
       TileMeta& md = meta[b];
-      const int ji = find_job(jobs, L.n_jobs, tile);
+      const int ji = job_of(L, jobs, tile);
       const TcJob& jg = jobs[ji];
       const int M = jg.M, N = jg.N, a_row0 = jg.a_row0;
       const float* bn = jg.b_norm;
@@ -883,7 +891,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)
     }
     __syncthreads();  // (tile_mark is cleared by the last CTA at the end)
     const int n = wsum[0] + wsum[1] + wsum[2] + wsum[3];
-    const TcJob jb = jobs[find_job(jobs, L.n_jobs, tile)];
+    const TcJob jb = jobs[job_of(L, jobs, tile)];
     const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
     const int mt = (tile - jb.tile0) / tiles_n, nt = (tile - jb.tile0) % tiles_n;
     const int arow = jb.a_row0 + mt * kTcBM, brow = jb.b_row0 + nt * kTcBN;

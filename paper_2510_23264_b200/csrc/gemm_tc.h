@@ -58,6 +58,7 @@ struct TcLaunch {
                         // [2..3] u64 running total of flagged elements
   float kappa;
   int fix_cpi;  // fixup columns per work item: 0 adaptive, else 1 / 2 / 4
+  const int* tile_job;  // [total_tiles] job index of each tile (may be null: binary search)
   const uint16_t* gelu_lut;  // bf16 -> round_bf16(gelu(x)) for all 2^16 inputs
 };
 
