@@ -284,6 +284,7 @@ struct Engine {
     uint64_t gen = 0;
   };
   std::map<int, TargetVal> target_cache;
+  std::map<const float*, std::unique_ptr<DeviceBuf>> wu_pad;  // padded unembed images
   uint64_t target_gen = 1;
   Trie full;
   // comm
@@ -975,7 +976,19 @@ struct Engine {
       lj.push_back({jobs[j].in + (all_rows ? 0 : (size_t)(g.S - 1) * D), nullptr,
                     xq + j * (size_t)rows * D, rows, all_rows ? D : g.S * D});
     ln(lj, g.mat(12, 0), g.mat(13, 0), p);
-    const float* wu = W(g.mat(14, 0), p, P.mode);
+    // W_u with its row pitch padded to a multiple of 4 floats (one resident
+    // copy per image): 16-byte loads in the exact GEMM's B staging
+    const float* wu0 = W(g.mat(14, 0), p, P.mode);
+    const int ldu = (V + 3) & ~3;
+    auto& pad = wu_pad[wu0];
+    if (!pad) {
+      pad = std::make_unique<DeviceBuf>();
+      pad->ensure((size_t)D * ldu * 4);
+      CK(cudaMemsetAsync(pad->p, 0, (size_t)D * ldu * 4, st));
+      CK(cudaMemcpy2DAsync(pad->p, (size_t)ldu * 4, wu0, (size_t)V * 4, (size_t)V * 4, D,
+                           cudaMemcpyDeviceToDevice, st));
+    }
+    const float* wu = pad->as<float>();
     std::vector<GemmJob> gj;
     bool contiguous = true;  // all segments' logits back to back: one tall GEMM
     for (size_t j = 0; j < jobs.size(); ++j)
@@ -983,13 +996,13 @@ struct Engine {
     if (contiguous) {
       GemmJob a{};
       a.A = xq, a.B = wu, a.C = jobs[0].out;
-      a.M = rows * (int)jobs.size(), a.N = V, a.K = D, a.lda = D, a.ldb = V, a.ldc = V, a.prec = p;
+      a.M = rows * (int)jobs.size(), a.N = V, a.K = D, a.lda = D, a.ldb = ldu, a.ldc = V, a.prec = p;
       gj.push_back(a);
     } else {
       for (size_t j = 0; j < jobs.size(); ++j) {
         GemmJob a{};
         a.A = xq + j * (size_t)rows * D, a.B = wu, a.C = jobs[j].out;
-        a.M = rows, a.N = V, a.K = D, a.lda = D, a.ldb = V, a.ldc = V, a.prec = p, a.epi = 0;
+        a.M = rows, a.N = V, a.K = D, a.lda = D, a.ldb = ldu, a.ldc = V, a.prec = p, a.epi = 0;
         gj.push_back(a);
       }
     }

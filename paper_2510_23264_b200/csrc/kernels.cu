@@ -825,13 +825,27 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __
   const int b_k = tid >> 5, b_n = (tid & 31) * 4;
   const f2_t z2 = f2_pack(negz, negz);
   float ra[4], rb[4];
+  // 16-byte loads where the rows are 16-byte aligned and the 4 values in range
+  const bool va4 = (jb.lda & 3) == 0 && (reinterpret_cast<uintptr_t>(jb.A) & 15) == 0;
+  const bool vb4 = (jb.ldb & 3) == 0 && (reinterpret_cast<uintptr_t>(jb.B) & 15) == 0;
   auto load = [&](int k0) {
+    const int gm = m0 + a_r, gka = k0 + a_k;
+    if (va4 && gm < jb.M && gka + 3 < jb.K) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(jb.A + (int64_t)gm * jb.lda + gka));
+      ra[0] = x.x, ra[1] = x.y, ra[2] = x.z, ra[3] = x.w;
+    } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int gm = m0 + a_r, gk = k0 + a_k + i;
-      ra[i] = (gm < jb.M && gk < jb.K) ? jb.A[(int64_t)gm * jb.lda + gk] : 0.f;
-      const int gk2 = k0 + b_k, gn = n0 + b_n + i;
-      rb[i] = (gk2 < jb.K && gn < jb.N) ? jb.B[(int64_t)gk2 * jb.ldb + gn] : 0.f;
+      for (int i = 0; i < 4; ++i)
+        ra[i] = (gm < jb.M && gka + i < jb.K) ? jb.A[(int64_t)gm * jb.lda + gka + i] : 0.f;
+    }
+    const int gk2 = k0 + b_k, gnb = n0 + b_n;
+    if (vb4 && gk2 < jb.K && gnb + 3 < jb.N) {
+      const float4 y = __ldg(reinterpret_cast<const float4*>(jb.B + (int64_t)gk2 * jb.ldb + gnb));
+      rb[0] = y.x, rb[1] = y.y, rb[2] = y.z, rb[3] = y.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        rb[i] = (gk2 < jb.K && gnb + i < jb.N) ? jb.B[(int64_t)gk2 * jb.ldb + gnb + i] : 0.f;
     }
   };
   auto store = [&](int buf) {
