@@ -601,13 +601,37 @@ void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float
 // acc = fl(acc + fl(a*b)) of dot_col (kernels.cpp:44-52). 64x64 tiles,
 // 256 threads, 4x4 micro-tiles, one launch for a whole job list.
 // ---------------------------------------------------------------------------
+// Paired-FP32 helpers (sm_100a FFMA2 / FADD2), see gemm_exact_x2_kernel.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+  return (f2_t)__float_as_uint(lo) | ((f2_t)__float_as_uint(hi) << 32);
+}
+// (a, a) through mov.b64: ptxas folds it into FFMA2's scalar-broadcast operand
+__device__ __forceinline__ f2_t f2_dup(float a) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(a));
+  return r;
+}
+__device__ __forceinline__ float f2_lo(f2_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2_hi(f2_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+
 constexpr int kBM = 64, kBN = 64, kBK = 16;
 
 int gemm_exact_tiles(int M, int N) { return ((M + kBM - 1) / kBM) * ((N + kBN - 1) / kBN); }
 
 __global__ void __launch_bounds__(256) gemm_exact_kernel(const GemmJob* __restrict__ jobs,
                                                          const int* __restrict__ tile_start,
-                                                         int n_jobs) {
+                                                         int n_jobs, float negz) {
   // locate the job owning this tile
   int lo = 0, hi = n_jobs - 1;
   const int t = blockIdx.x;
@@ -625,11 +649,11 @@ __global__ void __launch_bounds__(256) gemm_exact_kernel(const GemmJob* __restri
   __shared__ __align__(16) float Bs[kBK][kBN];
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
-  float acc[4][4];
+  // paired FP32 chains: acc[i][p] holds columns tx*4 + 2p, + 2p + 1 of row ty*4 + i
+  const f2_t z2 = f2_pack(negz, negz);
+  f2_t acc[4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) acc[i][jj] = 0.f;
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0ull;
 
   for (int k0 = 0; k0 < jb.K; k0 += kBK) {
     // A tile: 64 rows x 16 k -> As[k][m]
@@ -649,11 +673,11 @@ __global__ void __launch_bounds__(256) gemm_exact_kernel(const GemmJob* __restri
       const float4 a4 = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
       const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
       const float a[4] = {a4.x, a4.y, a4.z, a4.w};
-      const float b[4] = {b4.x, b4.y, b4.z, b4.w};
+      const f2_t b[2] = {f2_pack(b4.x, b4.y), f2_pack(b4.z, b4.w)};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = __fadd_rn(acc[i][jj], __fmul_rn(a[i], b[jj]));
+        for (int pp = 0; pp < 2; ++pp) acc[i][pp] = f2_add(acc[i][pp], f2_fma(f2_dup(a[i]), b[pp], z2));
     }
     __syncthreads();
   }
@@ -665,7 +689,7 @@ __global__ void __launch_bounds__(256) gemm_exact_kernel(const GemmJob* __restri
     for (int jj = 0; jj < 4; ++jj) {
       const int gn = n0 + tx * 4 + jj;
       if (gn >= jb.N) continue;
-      float v = round_p(acc[i][jj], jb.prec);
+      float v = round_p((jj & 1) ? f2_hi(acc[i][jj >> 1]) : f2_lo(acc[i][jj >> 1]), jb.prec);
       if (jb.epi == 1) v = round_p(gelu_ref(v), jb.prec);
       jb.C[(int64_t)gm * jb.ldc + gn] = v;
     }
@@ -675,7 +699,7 @@ __global__ void __launch_bounds__(256) gemm_exact_kernel(const GemmJob* __restri
 void launch_gemm_exact(const GemmJob* d_jobs, const int* d_tile_start, int n_jobs, int total_tiles,
                        cudaStream_t st) {
   if (n_jobs <= 0 || total_tiles <= 0) return;
-  gemm_exact_kernel<<<total_tiles, 256, 0, st>>>(d_jobs, d_tile_start, n_jobs);
+  gemm_exact_kernel<<<total_tiles, 256, 0, st>>>(d_jobs, d_tile_start, n_jobs, -0.0f);
 }
 
 // Large-tile variant (128 x 128, 8 x 8 per thread, register-prefetched k
@@ -780,28 +804,6 @@ __global__ void __launch_bounds__(256) gemm_exact_big_kernel(const GemmJob* __re
 // acc = fl(acc + fl(a*b)) in k order, bit-identical to dot_col
 // (kernels.cpp:44-52). A is staged in shared memory as broadcast pairs
 // (a, a) so that each 16-byte load feeds two rows.
-typedef unsigned long long f2_t;
-__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
-  f2_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
-  f2_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
-  return (f2_t)__float_as_uint(lo) | ((f2_t)__float_as_uint(hi) << 32);
-}
-// (a, a) through mov.b64: ptxas folds it into FFMA2's scalar-broadcast operand
-__device__ __forceinline__ f2_t f2_dup(float a) {
-  f2_t r;
-  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(a));
-  return r;
-}
-__device__ __forceinline__ float f2_lo(f2_t v) { return __uint_as_float((uint32_t)v); }
-__device__ __forceinline__ float f2_hi(f2_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
 
 __global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __restrict__ jobs,
                                                             const int* __restrict__ tile_start,
