@@ -144,11 +144,11 @@ def cpu_sample(cfg, w, ds, steps, warmup, threads=None):
     ref.set_threads(nthreads)
     with tempfile.TemporaryDirectory() as t:
         wp, dp = os.path.join(t, "w.bin"), os.path.join(t, "d.jsonl")
-        formats.save_weights(w, wp)
-        formats.save_dataset_jsonl(ds.subset([0]), dp)
+        write_ref_inputs(ref, cfg, ds.subset([0]), wp, dp)
         m = ref.open(wp, dp, 0)
-        from paper_2510_23264_b200.engine import graph_edges
-        _, src, dst = graph_edges(cfg)
+        # edges from the reference's own ComputationalGraph (model.cpp:182-203):
+        # this arm never loads libcqg.so
+        _, _, _, src, _ = ref.graph(cfg.fields8())
         cand = np.nonzero(src == 1)[0]  # node 1 = head a0.0
         n = int(min(len(cand), max(8, nthreads)))
         edges = cand[:n]
@@ -161,10 +161,77 @@ def cpu_sample(cfg, w, ds, steps, warmup, threads=None):
     passes = n * 1
     value = passes * len(times) / sum(times)
     return {"value": value, "unit": "passes/s", "cores": nthreads, "kind": kind,
+            "cpu_model": cpu_model(),
             "sample": f"delta_l of {n} out-edges of a0.0 x 1 IOI prompt per step "
                       f"(reference library compiled in place, OpenMP {nthreads} threads; "
                       f"refresh_baselines excluded), {len(times)} steps",
             "s_per_step": float(np.mean(times))}
+
+
+def self_launch(n, argv):
+    """`python bench.py --gpus N` without torchrun: start N ranks (one per
+    GPU) with torch.distributed.run on 127.0.0.1 and pass rank 0's line through."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
+
+
+def toy_acdc_pair(eng):
+    """BASELINE config 1 end to end on both sides: full PAHQ-ACDC (tau=0.01,
+    acdc.cpp:23-88) through cqg_run_acdc on the GPU and the reference library's
+    own run_acdc on all host threads, wall seconds each, and whether the two
+    pruned edge sets are identical."""
+    from oracle.oracle import Ref
+    cfg, w, ds = make_inputs("toy")
+    ref = Ref()
+    nthreads = ref.max_threads()
+    ref.set_threads(nthreads)
+    with tempfile.TemporaryDirectory() as t:
+        wp, dp = os.path.join(t, "w.bin"), os.path.join(t, "d.jsonl")
+        write_ref_inputs(ref, cfg, ds, wp, dp)
+        m = ref.open(wp, dp, 0)
+        pc = ref.method_config(2, 8)
+        t0 = time.perf_counter()
+        rr = m.run_acdc(pc)
+        cpu_s = time.perf_counter() - t0
+        m.close()
+    e = eng.Engine(w, device=int(os.environ.get("LOCAL_RANK", 0)))
+    e.set_dataset(ds, eng.KL)
+    c = eng.method_prune_config(eng.PAHQ)
+    e.run_acdc(c)  # warm-up (weight images, packed operands, buffers)
+    t0 = time.perf_counter()
+    r = e.run_acdc(c)
+    gpu_s = time.perf_counter() - t0
+    e.close()
+    return {"workload": "toy L2 H4 d128 V512 S16, random prompts batch 16, PAHQ tau=0.01",
+            "gpu_s": gpu_s, "cpu_s": cpu_s, "cpu_threads": nthreads, "steps": r.steps,
+            "kept_edges": int(r.final_mask.sum()),
+            "same_circuit": bool(np.array_equal(r.final_mask, rr.final_mask)),
+            "same_steps": r.steps == rr.steps}
+
+
+def write_ref_inputs(ref, cfg, ds, wp, dp):
+    """weights.bin by the reference's own generator and writer (support.hpp
+    random_weights(seed 1) -> save_weights, byte-identical to synth.random_weights,
+    tests/test_formats.py), then this workload's prompts as dataset.jsonl: the
+    reference arm needs nothing from the product library."""
+    ref.gen_random(cfg.fields8(), 1, 1, 1, wp, dp)
+    formats.save_dataset_jsonl(ds, dp)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(args):
@@ -216,12 +283,19 @@ def main(argv=None):
     ap.add_argument("--ncu", action="store_true",
                     help="profiling mode: one untimed scoring step, no JSON line (for ncu "
                          "launch lists; no number from it is a bench value)")
+    ap.add_argument("--acdc-quantile", type=float, default=0.99,
+                    help="ACDC end-to-end threshold = this quantile of the iteration-1 scores "
+                         "(a non-trivial circuit survives); tau=0.01 is timed as well")
     args = ap.parse_args(argv)
+    rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus, argv if argv is not None else sys.argv[1:])
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args)
 
     from paper_2510_23264_b200 import engine as eng
-    rank, world, local = dist_env()
     dist = None
     if world > 1:
         import torch
@@ -343,22 +417,37 @@ def main(argv=None):
 
     acdc = None
     if args.acdc:  # every rank runs the loop on its item block; scores are all-reduced per iteration
-        c = eng.method_prune_config(eng.PAHQ)
-        barrier()
-        t0 = time.perf_counter()
-        r = e.run_acdc(c)
-        barrier()
-        acdc = {"seconds": max_over_ranks(time.perf_counter() - t0), "steps": r.steps,
-                "kept_edges": int(r.final_mask.sum()), "tau": c.tau,
-                "passes": int(sum(len(it.scores) for it in r.iterations)) * items}
+        def timed_acdc(tau):
+            c = eng.method_prune_config(eng.PAHQ)
+            c.tau = float(tau)
+            barrier()
+            t0 = time.perf_counter()
+            r = e.run_acdc(c)
+            barrier()
+            return {"seconds": max_over_ranks(time.perf_counter() - t0), "steps": r.steps,
+                    "kept_edges": int(r.final_mask.sum()), "tau": c.tau,
+                    "kept_per_iteration": [it.present_after for it in r.iterations],
+                    "passes": int(sum(len(it.scores) for it in r.iterations)) * items}
+        # tau at a high quantile of this workload's iteration-1 scores, so a
+        # non-trivial circuit survives and several iterations run
+        tau_q = float(np.quantile(scores, args.acdc_quantile))
+        acdc = timed_acdc(tau_q)
+        acdc["tau_rule"] = f"quantile {args.acdc_quantile} of the iteration-1 scores"
+        acdc["tau_0.01"] = timed_acdc(0.01)
 
     if rank == 0:
         cb = None
+        toy = None
         if not args.no_cpu:
             try:
                 cb = cpu_sample(cfg, w, ds, steps=1, warmup=0)
             except Exception as ex:
                 cb = {"unavailable": f"{type(ex).__name__}: {ex}"}
+            if world == 1 and args.acdc:
+                try:
+                    toy = toy_acdc_pair(eng)
+                except Exception as ex:
+                    toy = {"unavailable": f"{type(ex).__name__}: {ex}"}
         out = {"metric": METRIC, "value": value, "unit": "passes/s", "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
@@ -370,7 +459,7 @@ def main(argv=None):
                        "parts": e2e_parts},
                "gpu_launches": int(launches), "wall_s": wall, "roofline": roofline,
                "cpu_baseline": cb, "passes_per_step": passes_per_step,
-               "acdc_end_to_end": acdc}
+               "acdc_end_to_end": acdc, "acdc_toy_gpu_vs_cpu": toy}
         print(json.dumps(out))
     if dist:
         dist.destroy_process_group()

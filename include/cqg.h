@@ -91,6 +91,16 @@ int cqg_run_acdc(cqg_ctx* ctx, const cqg_prune* cfg, int* steps, uint8_t* final_
                  double* last_score, int* n_rec, int32_t* rec_step, int32_t* rec_edge,
                  double* rec_score, uint8_t* rec_kept, int rec_cap);
 
+/* roc_sweep (proj/src/eval.cpp:1193-1226): cqg_run_acdc at every threshold
+ * taus[n_taus] with `cfg` otherwise unchanged; per tau the final mask's TPR /
+ * FPR against the ground-truth edge ids, the kept-edge count and the
+ * iteration count; *auc = auc_from_points (eval.cpp:1149-1166). Iteration 1
+ * (full mask) does not depend on tau: it is scored once and shared by every
+ * threshold. Output arrays may be null. */
+int cqg_roc_sweep(cqg_ctx* ctx, const cqg_prune* cfg, const double* taus, int n_taus,
+                  const int32_t* ground_truth, int n_gt, double* tpr, double* fpr, int32_t* kept,
+                  int32_t* steps, double* auc);
+
 /* Quantized image of one canonical matrix as FP32 values (bit-exact to
  * ImageBank::get(name, precision, low_mode), model.cpp:505-519). */
 int cqg_quantize_matrix(cqg_ctx* ctx, int matrix_index, int precision, int low_mode,

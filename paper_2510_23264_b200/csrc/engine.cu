@@ -1391,11 +1391,12 @@ struct Engine {
     return fr / 3;
   }
 
-  size_t edge_bytes(const EdgePlan& p, int nb) const {
+  size_t edge_bytes(const EdgePlan& p, int nb, bool loss) const {
     const size_t SEG = segf(nb);
-    // arena + per-edge scratch of the widest step (heads: xq + qkv + z; mlp: xq + hid; logits)
+    // arena + per-edge scratch of the widest step (heads: xq + qkv + z; mlp: xq + hid; logits:
+    // the last row only under loss metrics, patching.cpp:155-157)
     size_t scratch_b = std::max({SEG + (size_t)g.H * 4 * nb * g.S * g.dk, 5 * SEG,
-                                 (size_t)nb * g.S * g.V});
+                                 (size_t)nb * (loss ? 1 : g.S) * g.V});
     return ((size_t)(1 + p.n_slots) * SEG + scratch_b) * 4;
   }
 
@@ -1434,23 +1435,40 @@ struct Engine {
     ++target_gen;
   }
 
-  void score_edges(const uint8_t* mask, const int* edge_ids, int n, const Policy& base,
+  struct EventPair {  // RAII: no leak on the error paths
+    cudaEvent_t a = nullptr, b = nullptr;
+    EventPair() {
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+    }
+    ~EventPair() {
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  };
+
+  void score_edges(const uint8_t* mask, const int* edge_ids, int n, const Policy& base_in,
                    bool per_edge, int mode, double* out) {
     auto t0 = std::chrono::steady_clock::now();
     stats = cqg_stats{};
     kprof.clear();
-    cudaEvent_t ev0, ev1;
-    CK(cudaEventCreate(&ev0));
-    CK(cudaEventCreate(&ev1));
-    CK(cudaEventRecord(ev0, st));
     if (B == 0) throw Error(1, "score_edges: no dataset (call cqg_set_dataset)");
     if (mode != 0 && mode != 1) throw Error(1, "score_mode must be 0 (loss) or 1 (act)");
-    check_policy(base);
+    check_policy(base_in);
     for (int i = 0; i < n; ++i) {
       if (edge_ids[i] < 0 || edge_ids[i] >= g.E) throw Error(1, "forward: patch references unknown edge");
       if (!mask[edge_ids[i]])
         throw Error(1, "forward: patch references masked edge " + std::to_string(edge_ids[i]));
     }
+    // policy_for_edge (pahq.cpp:198-209) resets the base's targets before it
+    // elevates the edge's source, so under per-edge policies no scored pass
+    // ever runs the base's own target: every shared run (the masked baseline
+    // prefix, the full-graph patch run) uses the target-free base.
+    Policy base = base_in;
+    if (per_edge) base.th_l = base.th_h = base.tm = -1;
+    EventPair ev;
+    cudaEvent_t ev0 = ev.a, ev1 = ev.b;
+    CK(cudaEventRecord(ev0, st));
     const bool loss = mode == 0;
     DeviceBuf& nanbuf = *pool_buf("nan", 4);
     int* d_nan = nanbuf.as<int>();
@@ -1512,8 +1530,8 @@ struct Engine {
       size_t k0 = 0;
       while (k0 < ord.size()) {
         size_t bytes = 0, k1 = k0;
-        while (k1 < ord.size() && (k1 == k0 || bytes + edge_bytes(plans[ord[k1]], B) <= budget)) {
-          bytes += edge_bytes(plans[ord[k1]], B);
+        while (k1 < ord.size() && (k1 == k0 || bytes + edge_bytes(plans[ord[k1]], B, loss) <= budget)) {
+          bytes += edge_bytes(plans[ord[k1]], B, loss);
           ++k1;
         }
         std::vector<EdgePlan> batch;
@@ -1541,14 +1559,20 @@ struct Engine {
     int h_nan = 0;
     CK(cudaMemcpyAsync(&h_nan, d_nan, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (h_nan) throw Error(2, metric == 0 ? "metric_kl: NaN logits" : "metric_logit_diff: NaN logits");
     if (comm) {  // any communicator, including a 1-rank one (tests the NCCL path on one GPU)
-      DeviceBuf& ar = *pool_buf("allreduce", sizeof(double) * std::max(n, 1));
-      CK(cudaMemcpyAsync(ar.p, sums.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
-      NK(nccl().AllReduce(ar.p, ar.p, (size_t)n, ncclDouble, ncclSum, comm, st));
-      CK(cudaMemcpyAsync(sums.data(), ar.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+      // the NaN flag travels with the partial sums (element n), so a NaN on
+      // one rank fails the call on every rank instead of leaving the others
+      // blocked in the collective
+      DeviceBuf& ar = *pool_buf("allreduce", sizeof(double) * (n + 1));
+      sums.push_back(h_nan ? 1.0 : 0.0);
+      CK(cudaMemcpyAsync(ar.p, sums.data(), sizeof(double) * (n + 1), cudaMemcpyHostToDevice, st));
+      NK(nccl().AllReduce(ar.p, ar.p, (size_t)(n + 1), ncclDouble, ncclSum, comm, st));
+      CK(cudaMemcpyAsync(sums.data(), ar.p, sizeof(double) * (n + 1), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      h_nan = sums[n] != 0.0;
+      sums.pop_back();
     }
+    if (h_nan) throw Error(2, metric == 0 ? "metric_kl: NaN logits" : "metric_logit_diff: NaN logits");
     for (int i = 0; i < n; ++i) out[i] = sums[i] / (double)item_total;
     if (fix_cnt.p) {  // elements recomputed by the exact fixup
       uint64_t c[2] = {0, 0};
@@ -1563,8 +1587,6 @@ struct Engine {
     float dms = 0;
     CK(cudaEventElapsedTime(&dms, ev0, ev1));
     stats.ms_device = dms;
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
     collect_profile();
     stats.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
@@ -1682,8 +1704,11 @@ struct Engine {
   }
 
 
+  // iter0_raw: iteration-1 scores of the full mask's sweep order (after the
+  // heads_only filter), already computed -- they do not depend on tau, so a
+  // threshold sweep scores them once (roc_sweep below).
   void run_acdc(const cqg_prune& c, int* steps, uint8_t* final_mask, double* last_score, int* n_rec,
-                int* rs, int* re, double* rsc, uint8_t* rk, int cap) {
+                int* rs, int* re, double* rsc, uint8_t* rk, int cap, const double* iter0_raw = nullptr) {
     // PruneConfig::validate (acdc.cpp:14-21)
     if (!(c.tau >= 0.0)) throw Error(1, "PruneConfig: tau must be >= 0");
     if (c.max_steps < 1) throw Error(1, "PruneConfig: max_steps must be >= 1");
@@ -1702,8 +1727,11 @@ struct Engine {
                     order.end());
       if (order.empty()) break;
       std::vector<double> raw(order.size());
-      score_edges(mask.data(), order.data(), (int)order.size(), base, c.per_edge_policy != 0, c.mode,
-                  raw.data());
+      if (t == 0 && iter0_raw)
+        std::copy(iter0_raw, iter0_raw + order.size(), raw.begin());
+      else
+        score_edges(mask.data(), order.data(), (int)order.size(), base, c.per_edge_policy != 0, c.mode,
+                    raw.data());
       int removed = 0;
       for (size_t i = 0; i < order.size(); ++i) {
         double s = raw[i];
@@ -1724,6 +1752,73 @@ struct Engine {
     std::copy(mask.begin(), mask.end(), final_mask);
     *steps = t;
     *n_rec = k;
+  }
+
+  std::vector<int> first_order(const cqg_prune& c) const {
+    std::vector<int> order = g.sweep_order(std::vector<uint8_t>(g.E, 1));
+    if (c.heads_only)
+      order.erase(std::remove_if(order.begin(), order.end(),
+                                 [&](int e) { return g.kind[g.esrc[e]] != kHead; }),
+                  order.end());
+    return order;
+  }
+
+  // roc_sweep (eval.cpp:1193-1226): run_acdc at every threshold, TPR/FPR of
+  // the final mask against the ground truth, AUC (auc_from_points,
+  // eval.cpp:1149-1166). Iteration 1 runs on the full mask for every tau, so
+  // its scores are computed once and shared; later iterations run per tau.
+  double roc_sweep(const cqg_prune& c, const double* taus, int n, const int* gt, int n_gt, double* tpr,
+                   double* fpr, int* kept, int* steps) {
+    if (n < 1) throw Error(1, "roc_sweep: no thresholds");
+    std::vector<uint8_t> is_gt(g.E, 0);
+    for (int i = 0; i < n_gt; ++i) {
+      if (gt[i] < 0 || gt[i] >= g.E) throw Error(1, "roc_sweep: ground-truth edge out of range");
+      is_gt[gt[i]] = 1;
+    }
+    const int n_pos = (int)std::count(is_gt.begin(), is_gt.end(), 1), n_neg = g.E - n_pos;
+    if (n_pos == 0 || n_neg == 0) throw Error(1, "roc_sweep: degenerate ground truth");
+    cqg_prune c0 = c;
+    c0.tau = taus[0];
+    if (!(c0.tau >= 0.0)) throw Error(1, "PruneConfig: tau must be >= 0");
+    const std::vector<int> order = first_order(c);
+    std::vector<double> raw0(order.size());
+    if (!order.empty())
+      score_edges(std::vector<uint8_t>(g.E, 1).data(), order.data(), (int)order.size(), Policy::from(c.base),
+                  c.per_edge_policy != 0, c.mode, raw0.data());
+    std::vector<uint8_t> fm(g.E);
+    std::vector<double> ls(g.E);
+    struct Pt { double tpr, fpr; };
+    std::vector<Pt> pts(n);
+    for (int i = 0; i < n; ++i) {
+      cqg_prune ci = c;
+      ci.tau = taus[i];
+      int st = 0, nr = 0;
+      run_acdc(ci, &st, fm.data(), ls.data(), &nr, nullptr, nullptr, nullptr, nullptr, 0, raw0.data());
+      int tp = 0, fp = 0, k = 0;
+      for (int e = 0; e < g.E; ++e) {
+        if (!fm[e]) continue;
+        ++k;
+        (is_gt[e] ? tp : fp) += 1;
+      }
+      pts[i] = {(double)tp / n_pos, (double)fp / n_neg};
+      if (tpr) tpr[i] = pts[i].tpr;
+      if (fpr) fpr[i] = pts[i].fpr;
+      if (kept) kept[i] = k;
+      if (steps) steps[i] = st;
+    }
+    std::sort(pts.begin(), pts.end(), [](const Pt& a, const Pt& b) {
+      return a.fpr != b.fpr ? a.fpr < b.fpr : a.tpr < b.tpr;
+    });
+    double x = 0.0, y = 0.0, area = 0.0;
+    for (const Pt& p : pts) {
+      if (p.tpr <= y) continue;
+      if (p.fpr > x) {
+        area += (p.fpr - x) * y;
+        x = p.fpr;
+      }
+      y = p.tpr;
+    }
+    return area + (1.0 - x) * y;
   }
 };
 
@@ -1861,6 +1956,17 @@ int cqg_run_acdc(cqg_ctx* ctx, const cqg_prune* cfg, int* steps, uint8_t* final_
     CK(cudaSetDevice(ctx->e->device));
     ctx->e->run_acdc(*cfg, steps, final_mask, last_score, n_rec, rec_step, rec_edge, rec_score,
                      rec_kept, rec_cap);
+  });
+}
+
+int cqg_roc_sweep(cqg_ctx* ctx, const cqg_prune* cfg, const double* taus, int n_taus,
+                  const int32_t* ground_truth, int n_gt, double* tpr, double* fpr, int32_t* kept,
+                  int32_t* steps, double* auc) {
+  return guarded([&] {
+    if (!ctx || !cfg || !taus || (!ground_truth && n_gt > 0) || !auc)
+      throw Error(1, "cqg_roc_sweep: null argument");
+    CK(cudaSetDevice(ctx->e->device));
+    *auc = ctx->e->roc_sweep(*cfg, taus, n_taus, ground_truth, n_gt, tpr, fpr, kept, steps);
   });
 }
 

@@ -161,6 +161,38 @@ class CircuitResult:
     steps: int
 
 
+@dataclass
+class RocPoint:
+    """RocPoint (eval.hpp): threshold, TPR, FPR, kept edges (+ iterations)."""
+    tau: float
+    tpr: float
+    fpr: float
+    kept: int
+    steps: int = 0
+
+
+@dataclass
+class RocCurve:
+    points: List[RocPoint]
+    auc: float
+
+
+def auc_from_points(points) -> float:
+    """eval.cpp:1149-1166 (points: RocPoint or (tpr, fpr) pairs)."""
+    pts = [(p.tpr, p.fpr) if isinstance(p, RocPoint) else tuple(p) for p in points]
+    if not pts:
+        raise ValueError("auc_from_points: no points")
+    x = y = area = 0.0
+    for tpr, fpr in sorted(pts, key=lambda p: (p[1], p[0])):
+        if tpr <= y:
+            continue
+        if fpr > x:
+            area += (fpr - x) * y
+            x = fpr
+        y = tpr
+    return area + (1.0 - x) * y
+
+
 _lib = None
 
 
@@ -185,6 +217,8 @@ def load_library():
     lib.cqg_run_acdc.argtypes = [vp, C.POINTER(CqgPrune), C.POINTER(C.c_int), vp, vp,
                                  C.POINTER(C.c_int), vp, vp, vp, vp, C.c_int]
     lib.cqg_quantize_matrix.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
+    lib.cqg_roc_sweep.argtypes = [vp, C.POINTER(CqgPrune), vp, C.c_int, vp, C.c_int, vp, vp, vp, vp,
+                                  C.POINTER(C.c_double)]
     lib.cqg_forward.argtypes = [vp, vp, vp, C.POINTER(CqgPolicy), C.c_int, vp, vp]
     lib.cqg_circuit_stats.argtypes = [vp, vp, vp, vp, vp]
     lib.cqg_graph_info.argtypes = [C.POINTER(CqgConfig), C.POINTER(C.c_int), C.POINTER(C.c_int)]
@@ -333,6 +367,22 @@ class Engine:
                 present -= 1
             its[-1].present_after = present
         return CircuitResult(its, fm.astype(bool), ls, steps.value)
+
+    def roc_sweep(self, prune: PruneConfig, taus: Sequence[float], ground_truth) -> "RocCurve":
+        """roc_sweep (eval.cpp:1193-1226) through cqg_roc_sweep: iteration 1 is
+        scored once and shared across the thresholds."""
+        t = np.ascontiguousarray(taus, np.float64)
+        gt = np.ascontiguousarray(sorted(set(int(x) for x in ground_truth)), np.int32)
+        n = t.size
+        tpr, fpr = np.empty(n), np.empty(n)
+        kept, steps = np.empty(n, np.int32), np.empty(n, np.int32)
+        auc = C.c_double()
+        pc = prune.c()
+        _check(self.lib.cqg_roc_sweep(self.h, C.byref(pc), _vp(t), n, _vp(gt), gt.size, _vp(tpr),
+                                      _vp(fpr), _vp(kept), _vp(steps), C.byref(auc)))
+        pts = [RocPoint(float(t[i]), float(tpr[i]), float(fpr[i]), int(kept[i]), int(steps[i]))
+               for i in range(n)]
+        return RocCurve(pts, auc.value)
 
     def quantize_matrix(self, idx: int, precision: int, low_mode: int = E4M3) -> np.ndarray:
         shape = self.cfg.matrix_specs()[idx][1]

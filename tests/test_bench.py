@@ -30,3 +30,29 @@ def test_bench_module_imports():
     sys.path.insert(0, ROOT)
     import bench  # noqa: F401
     assert "gpt2s" in bench.CONFIGS and "toy" in bench.CONFIGS
+
+
+@pytest.mark.skipif(not os.path.exists(REF), reason="reference library not built (make -C oracle ref)")
+def test_reference_arm_is_independent_of_libcqg():
+    """The reference arm enumerates edges with the reference's own graph and
+    never maps the product library."""
+    code = ("import sys; sys.argv=['bench.py']; import bench; "
+            "bench.main(['--impl','reference','--config','toy','--steps','1','--warmup','0']); "
+            "print('MAPS', 'libcqg' in open('/proc/self/maps').read())")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                       cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "MAPS False" in r.stdout, r.stdout[-500:]
+
+
+@pytest.mark.skipif(not os.path.exists(REF), reason="reference library not built (make -C oracle ref)")
+def test_gpus_flag_self_launches_ranks():
+    """`bench.py --gpus 2` without torchrun starts 2 ranks (torch.distributed.run
+    on 127.0.0.1); rank 0 prints the one line, and it reports n_gpus 2."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--gpus", "2", "--config", "toy", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    assert json.loads(lines[0])["n_gpus"] == 2

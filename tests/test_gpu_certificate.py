@@ -1,0 +1,146 @@
+"""Robustness of the tensor-core exactness certificate (gemm_tc.h) on
+structured and adversarial data, on the GPU.
+
+The reference sums each dot product sequentially in FP32
+(proj/src/kernels.cpp:44-52) and then rounds to E4M3 / BF16. The tensor cores
+sum in another order; the epilogue flags every element whose rounding the
+margin m = kappa(K) u sqrt(K) max(|acc|, ||a|| ||b|| / sqrt(K)) does not
+certify, and the fixup recomputes it sequentially. These tests feed data
+built to break that margin:
+
+* sign-ordered (cancelling) rows: every product positive over the first half
+  of K and negative over the second, so the partial sums reach ~||a|| ||b|| / 2
+  while the result is ~0 (the sequential sum's rounding error then has
+  std ~ u ||a|| ||b|| sqrt(K/12), far above the iid-data scale);
+* outlier columns of A (a few k with 100x magnitude), heavy-tailed values
+  (Student t, 1.5 degrees of freedom), and iid Gaussian rows.
+
+Bar: the certified + fixed output equals round(sequential FP32 sum) bit for
+bit on every element (BF16 at K = 768 / 3072, E4M3 at K = 768). The raw
+tensor-core error |acc - seq| in units of u sqrt(K) max(|acc|, ||a|| ||b||/sqrt K)
+is recorded in gpurun_out/certificate_kappa.json.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from test_gpu_parity import _bf16_grid, _tc_gemm
+from helpers import bits
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+U = 2.0 ** -24
+
+
+def e4m3_grid(x):
+    """round_f8 (numerics.cpp:41-64): RNE to the E4M3 grid, saturating at 448."""
+    codes = np.arange(127, dtype=np.int64)
+    e, m = codes >> 3, codes & 7
+    vals = np.where(e == 0, m * 2.0 ** -9, (1 + m / 8.0) * 2.0 ** (e - 7))
+    x = np.asarray(x, np.float64)
+    a = np.minimum(np.abs(x), 448.0)
+    i = np.clip(np.searchsorted(vals, a), 1, 126)
+    lo, hi = vals[i - 1], vals[i]
+    pick_hi = (hi - a < a - lo) | ((hi - a == a - lo) & ((i & 1) == 0))
+    return (np.sign(x) * np.where(pick_hi, hi, lo)).astype(np.float32)
+
+
+def seq_dot(A, Bt):
+    """Sequential FP32 sum of exact products, k ascending (dot_col)."""
+    M, K = A.shape
+    s = np.zeros((M, Bt.shape[0]), np.float32)
+    for k in range(K):
+        s = (s + (A[:, k:k + 1] * Bt[:, k][None, :]).astype(np.float32)).astype(np.float32)
+    return s
+
+
+def make_data(kind, M, N, K, grid, rng):
+    if kind == "iid":
+        A = rng.randn(M, K)
+        Bt = rng.randn(N, K) * 0.03
+    elif kind == "cancelling":
+        # products a_k b_nk > 0 for k < K/2, < 0 after (B rows all positive)
+        A = np.abs(rng.randn(M, K))
+        A[:, K // 2:] *= -1.0
+        # exact cancellation for a quarter of the rows: second half mirrors the first
+        A[::4, K // 2:] = -A[::4, :K // 2]
+        Bt = np.abs(rng.randn(N, K)) * 0.03
+        Bt[:, K // 2:] = Bt[:, :K // 2]
+        Bt[1::2] = np.abs(rng.randn(N // 2, K)) * 0.03  # half the columns: inexact mirror
+    elif kind == "outliers":
+        A = rng.randn(M, K)
+        cols = rng.choice(K, 6, replace=False)
+        A[:, cols] *= 100.0
+        Bt = rng.randn(N, K) * 0.03
+    elif kind == "heavy":
+        A = rng.standard_t(1.5, size=(M, K)).clip(-1e4, 1e4)
+        Bt = rng.standard_t(1.5, size=(N, K)).clip(-1e4, 1e4) * 0.01
+    else:
+        raise ValueError(kind)
+    return grid(A.astype(np.float32)), grid(Bt.astype(np.float32))
+
+
+def kappa_units(A, Bt, acc, seq, K):
+    na = np.sqrt((A.astype(np.float64) ** 2).sum(1))
+    nb = np.sqrt((Bt.astype(np.float64) ** 2).sum(1))
+    scale = np.maximum(np.abs(acc.astype(np.float64)), np.outer(na, nb) / np.sqrt(K))
+    with np.errstate(divide="ignore", invalid="ignore"):
+        r = np.abs(acc.astype(np.float64) - seq.astype(np.float64)) / (U * np.sqrt(K) * scale)
+    return float(np.nanmax(np.where(scale > 0, r, 0.0)))
+
+
+RESULTS = {}
+
+
+@pytest.mark.parametrize("elem,K", [(1, 768), (1, 3072), (0, 768)])
+@pytest.mark.parametrize("kind", ["iid", "cancelling", "outliers", "heavy"])
+def test_certificate_on_adversarial_data(elem, K, kind):
+    rng = np.random.RandomState(K + len(kind))
+    M, N = 256, 256
+    grid = _bf16_grid if elem == 1 else e4m3_grid
+    A, Bt = make_data(kind, M, N, K, grid, rng)
+    seq = seq_dot(A, Bt)
+    raw, _, _ = _tc_gemm(elem, 2, 0, A, Bt)  # raw tensor-core accumulators (no rounding)
+    prec = 1 if elem == 1 else 0
+    out, ex, nf = _tc_gemm(elem, prec, 0, A, Bt)
+    want = _bf16_grid(seq) if elem == 1 else e4m3_grid(seq)
+    ku = kappa_units(A, Bt, raw, seq, K)
+    RESULTS[f"{'bf16' if elem else 'e4m3'}_K{K}_{kind}"] = {
+        "max_err_kappa_units": ku, "flagged": int(nf), "elements": M * N}
+    p = os.path.join(ROOT, "gpurun_out", "certificate_kappa.json")
+    os.makedirs(os.path.dirname(p), exist_ok=True)
+    json.dump(RESULTS, open(p, "w"), indent=1)
+    bad = bits(out) != bits(want)
+    assert not bad.any(), (kind, int(bad.sum()), ku)
+    assert np.array_equal(bits(ex), bits(want))
+
+
+def test_e4m3_exact_accumulation_wide_exponent_spread():
+    """cert_all (gemm_tc.cu: E4M3 x E4M3 with ||a|| ||b|| < 2^6 is certified
+    without a margin test) relies on the fp8 tensor-core accumulator returning
+    the exact sum whenever every partial sum is a multiple of 2^-18 below 2^6.
+    Exercise exactly that: one large product next to many 2^-18-scale ones,
+    in every K position, with the sum landing on E4M3 rounding midpoints."""
+    K, M, N = 768, 128, 128
+    rng = np.random.RandomState(7)
+    tiny = 2.0 ** -9  # smallest E4M3 subnormal: tiny*tiny = 2^-18
+    A = np.full((M, K), tiny, np.float32) * rng.choice([-1, 1], (M, K))
+    Bt = np.full((N, K), tiny, np.float32) * rng.choice([-1, 1], (N, K))
+    big_k = rng.randint(0, K, M)
+    A[np.arange(M), big_k] = e4m3_grid(rng.uniform(1, 6, M).astype(np.float32))
+    Bt[:, :] = np.where(rng.rand(N, K) < 0.5, Bt, Bt * 2)
+    for r in range(M):  # large partner values in B at the row's big column
+        Bt[r % N, big_k[r]] = e4m3_grid(np.float32(rng.uniform(0.5, 1.0)))
+    A, Bt = e4m3_grid(A), e4m3_grid(Bt)
+    na = np.sqrt((A.astype(np.float64) ** 2).sum(1)).max()
+    nb = np.sqrt((Bt.astype(np.float64) ** 2).sum(1)).max()
+    assert na * nb < 63.99, na * nb  # inside cert_all's domain
+    seq = seq_dot(A, Bt)
+    exact = (A.astype(np.float64) @ Bt.astype(np.float64).T)
+    assert np.array_equal(seq.astype(np.float64), exact)  # every partial sum exact
+    raw, _, _ = _tc_gemm(0, 2, 0, A, Bt)
+    assert np.array_equal(bits(raw), bits(seq)), "fp8 tensor-core accumulation is not exact"
+    out, _, _ = _tc_gemm(0, 0, 0, A, Bt)
+    assert np.array_equal(bits(out), bits(e4m3_grid(seq)))

@@ -292,16 +292,22 @@ def test_planted_known_answer_aucs_on_gpu(preset):
     gt = set(json.load(open(os.path.join(d, "task.json")))["ground_truth"])
     e = eng.Engine(w)
     e.set_dataset(ds, LOGITDIFF)
+    taus = eng.threshold_grid(0.001, 3.16, 21)
     for mname, mid in (("acdc", 0), ("rtn8", 1), ("pahq", 2)):
         pts = []
-        for tau in eng.threshold_grid(0.001, 3.16, 21):
+        for tau in taus:
             c = eng.method_prune_config(mid)
             c.tau = tau
             r = e.run_acdc(c)
             kept = np.nonzero(r.final_mask)[0]
             tp = sum(1 for x in kept if x in gt)
-            pts.append((tp / len(gt), (len(kept) - tp) / (e.n_edges - len(gt))))
-        assert float(auc_from_points(pts)).hex() == G["planted"][preset][mname]["auc"], mname
+            pts.append((tp / len(gt), (len(kept) - tp) / (e.n_edges - len(gt)), len(kept), r.steps))
+        assert float(auc_from_points([p[:2] for p in pts])).hex() == G["planted"][preset][mname]["auc"], mname
+        # cqg_roc_sweep (iteration 1 shared across thresholds) = independent runs
+        curve = e.roc_sweep(eng.method_prune_config(mid), taus, gt)
+        assert float(curve.auc).hex() == G["planted"][preset][mname]["auc"], mname
+        assert [(p.tpr, p.fpr, p.kept, p.steps) for p in curve.points] == pts, mname
+        assert eng.auc_from_points(curve.points) == curve.auc
     e.close()
 
 

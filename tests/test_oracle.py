@@ -215,3 +215,23 @@ def test_port_run_acdc_equals_reference_small(ref, tmp_path):
     assert a.steps == b.steps and np.array_equal(a.final_mask, b.final_mask)
     assert a.records == b.records
     rm.close()
+
+
+def test_port_targeted_base_per_edge_equals_reference(ref, tmp_path):
+    """Per-edge policies over a base that carries its own target head / MLP
+    (policy_for_edge resets it, pahq.cpp:198-209): the restatement equals the
+    reference library bit for bit (the GPU test compares against the port)."""
+    from helpers import write
+    w, ds = make(SMALL, 5, 3, 9)
+    p = Port(SMALL, w.mats)
+    mask = np.ones(p.n_edges, bool)
+    mask[np.random.RandomState(3).rand(p.n_edges) < 0.3] = False
+    edges = np.nonzero(mask)[0].astype(np.int32)
+    wp, dp = write(str(tmp_path), w, ds)
+    m = ref.open(wp, dp, KL)
+    for base in (Policy.make(th=(0, 1)), Policy.make(tm=2), Policy.make(th=(2, 3), tm=0)):
+        for pe in (True, False):
+            a = p.score_edges(ds, edges, base, per_edge=pe, metric=KL, mask=mask)
+            b = m.score_edges(edges, base, pe, 0, mask)
+            assert np.array_equal(a, b), (pe, base.target_head_layer, base.target_mlp)
+    m.close()
