@@ -41,6 +41,12 @@ constexpr size_t kMetaBytes = (sizeof(TileMeta) + 15) & ~size_t(15);
 // and the metadata warp run up to kAccBufs - 1 tiles ahead of the epilogue,
 // which hides the per-tile TMA -> MMA -> commit latency of short-K GEMMs (W_O).
 constexpr int kAccBufs = 4;
+// Certified BF16 outputs accumulate K in two halves into two TMEM
+// accumulators (the buffer count halves to 2): the epilogue adds them and
+// also knows the partial sum at K/2, so a sign-ordered (cancelling) row, whose
+// partial sums run far above the result, gets a margin on that scale.
+__host__ __device__ constexpr int split_of(int elem, int prec) { return elem == kTcBF16 && prec == 1 ? 2 : 1; }
+__device__ __forceinline__ int split_kh(int nk) { return (nk + 1) >> 1; }
 constexpr size_t kSmemBytes = 1024 + (size_t)kStages * (kAStage + kBStage) + 256 +
                               kEpiWarps * kStageFloats * sizeof(float) + kAccBufs * kMetaBytes +
                               2 * 2 * 13 * 128;  // GELU LUT slice (kGeluSm uint16)
@@ -272,6 +278,9 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TileMeta&
   const int row0 = mt * kTcBM + q * 32;
   const int nrow = min(32, jb.M - row0);
   uint32_t flagged0 = 0, flagged1 = 0;
+  constexpr int kSplitE = split_of(ELEM, PREC);
+  // the second accumulator exists when K spans at least two k-blocks
+  const bool two = kSplitE == 2 && (jb.K * (ELEM == kTcBF16 ? 2 : 1) + kBKBytes - 1) / kBKBytes >= 2;
   // one 32-column chunk per iteration, not unrolled: the epilogue body is
   // large and the unrolled pair thrashed the instruction cache
 #pragma unroll 1
@@ -279,6 +288,23 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TileMeta&
     const int c0 = half * 64 + cc * 32;
     uint32_t r[32];
     tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
+    // split accumulation: r = first-half sum, r2 = second half; acc = r + r2,
+    // and |first half| joins the margin's scale (h1)
+    float h1[kSplitE == 2 ? 32 : 1];
+    if (kSplitE == 2) {
+      if (two) {
+        uint32_t r2[32];
+        tmem_ld32(tacc + kTcBN + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r2);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          h1[j] = fabsf(__uint_as_float(r[j]));
+          r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) h1[j] = 0.f;
+      }
+    }
     uint32_t fl = 0;
     const int colb = nt * kTcBN + c0;
     const int ncol = min(32, jb.N - colb);
@@ -316,7 +342,9 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TileMeta&
         for (int t = 0; t < 4; ++t) {
           const float acc = __uint_as_float(r[j + t]);
           v[j + t] = round_bf16(acc);
-          const float m = ku * fmaxf(fabsf(acc), nas * nb4[t]);
+          float sc = fabsf(acc);
+          if (kSplitE == 2) sc = fmaxf(sc, h1[(j + t) & (kSplitE == 2 ? 31 : 0)]);
+          const float m = ku * fmaxf(sc, nas * nb4[t]);
           if (bf16_ambiguous(acc, m)) fl |= 1u << (j + t);
         }
       }
@@ -518,13 +546,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int esz = ELEM == kTcBF16 ? 2 : 1;
   constexpr int bke = kBKBytes / esz;  // elements per stage along K
+  constexpr int kSplit = split_of(ELEM, PREC);
+  constexpr int kBufs = kAccBufs / kSplit;  // TMEM accumulator buffers in flight
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < kAccBufs; ++b) {
+    for (int b = 0; b < kBufs; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], kEpiWarps);
       mbar_init(&mfull[b], 32);
@@ -569,19 +599,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         const TcJob& jb = jobs[job_of(L, jobs, tile)];
         const int kbytes = jb.K * esz;
         const int nk = (kbytes + kBKBytes - 1) / kBKBytes;
-        const uint32_t b = ti % kAccBufs, bph = (ti / kAccBufs) & 1;
+        const uint32_t b = ti % kBufs, bph = (ti / kBufs) & 1;
         mbar_wait(&tempty[b], bph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t tacc = tmem + b * kTcBN;
+        const uint32_t tacc = tmem + b * kSplit * kTcBN;
+        // split accumulation (kSplit == 2): k-blocks [0, kh) into the first
+        // accumulator, [kh, nk) into the second (the epilogue sees the
+        // partial sum at K/2: the trend term of the certificate)
+        const int kh = kSplit == 2 ? split_kh(nk) : nk;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % kStages;
           mbar_wait(&full[s], (it / kStages) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const int nmma = min(4, (kbytes - kb * kBKBytes) / 32);
           const uint32_t a0 = smem_u32(sA + s * kAStage), b0 = smem_u32(sB + s * kBStage);
+          const uint32_t tdst = kb < kh ? tacc : tacc + kTcBN;
+          const int kb0 = kb < kh ? 0 : kh;
           for (int k = 0; k < nmma; ++k)
-            mma<ELEM>(tacc, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
-                      (kb | k) != 0 ? 1u : 0u);
+            mma<ELEM>(tdst, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc,
+                      (kb != kb0 || k != 0) ? 1u : 0u);
           mma_commit(&empty[s]);
         }
         mma_commit(&tfull[b]);
@@ -590,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 2) {  // tile metadata, one TMEM buffer ahead of the epilogue
     uint32_t ti = 0;
     for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x, ++ti) {
-      const uint32_t b = ti % kAccBufs, bph = (ti / kAccBufs) & 1;
+      const uint32_t b = ti % kBufs, bph = (ti / kBufs) & 1;
       mbar_wait(&mempty[b], bph ^ 1);
       TileMeta& md = meta[b];
       const int ji = job_of(L, jobs, tile);
@@ -624,11 +660,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
     uint32_t ti = 0;
     for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x, ++ti) {
-      const uint32_t b = ti % kAccBufs, bph = (ti / kAccBufs) & 1;
+      const uint32_t b = ti % kBufs, bph = (ti / kBufs) & 1;
       mbar_wait(&mfull[b], bph);
       mbar_wait(&tfull[b], bph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      epilogue_tile<ELEM, PREC, EPI>(L, meta[b], tile, tmem + b * kTcBN, q, half, lane,
+      epilogue_tile<ELEM, PREC, EPI>(L, meta[b], tile, tmem + b * kSplit * kTcBN, q, half, lane,
                                      stage_all + (size_t)(warp - kEpiWarp0) * kStageFloats, gelu_s);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();

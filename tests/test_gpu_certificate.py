@@ -69,6 +69,14 @@ def make_data(kind, M, N, K, grid, rng):
         Bt = np.abs(rng.randn(N, K)) * 0.03
         Bt[:, K // 2:] = Bt[:, :K // 2]
         Bt[1::2] = np.abs(rng.randn(N // 2, K)) * 0.03  # half the columns: inexact mirror
+    elif kind == "cancelling4":
+        # finer sign order (+ - + - over K quarters): the partial sums peak at
+        # K/4 and 3K/4, between the K/2 split point and the end
+        A = np.abs(rng.randn(M, K))
+        q = K // 4
+        A[:, q:2 * q] *= -1.0
+        A[:, 3 * q:] *= -1.0
+        Bt = np.abs(rng.randn(N, K)) * 0.03
     elif kind == "outliers":
         A = rng.randn(M, K)
         cols = rng.choice(K, 6, replace=False)
@@ -95,8 +103,15 @@ RESULTS = {}
 
 
 @pytest.mark.parametrize("elem,K", [(1, 768), (1, 3072), (0, 768)])
-@pytest.mark.parametrize("kind", ["iid", "cancelling", "outliers", "heavy"])
-def test_certificate_on_adversarial_data(elem, K, kind):
+@pytest.mark.parametrize("kind", ["iid", "cancelling", "cancelling4", "outliers", "heavy"])
+def test_certificate_on_adversarial_data(elem, K, kind, request):
+    if kind == "cancelling4" and K == 3072:
+        # Known limit of a statistical certificate: the margin
+        # sees the partial sum at K/2 (split accumulation) but not the peaks
+        # at K/4 and 3K/4 of a + - + - sign-sorted row; the tensor-core error
+        # there reaches ~15 margin units (gpurun_out/certificate_kappa.json).
+        request.applymarker(pytest.mark.xfail(reason="sign-sorted quarters defeat the K/2 trend term",
+                                              strict=False))
     rng = np.random.RandomState(K + len(kind))
     M, N = 256, 256
     grid = _bf16_grid if elem == 1 else e4m3_grid
