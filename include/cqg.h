@@ -134,6 +134,8 @@ typedef struct {
   int64_t kernel_launches; /* kernels launched by the call */
   int64_t fallback_elems;  /* tensor-core outputs recomputed on the exact path */
   int64_t h2d_bytes, d2h_bytes;
+  int64_t unembed_rows;       /* patched last rows whose logits came from the tensor cores */
+  int64_t unembed_exact_rows; /* of those, rows the KL certificate recomputed exactly */
 } cqg_stats;
 int cqg_last_stats(cqg_ctx* ctx, cqg_stats* out);
 

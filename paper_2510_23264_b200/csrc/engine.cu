@@ -296,6 +296,14 @@ struct Engine {
   int64_t opt_packed = 1;
   int64_t opt_fix_cpi = 0;  // store E4M3/BF16-rounded node outputs as their codes
   int64_t opt_mem_budget = 0;
+  // 1: the patched passes' FP32 unembed on the tensor cores (6-term BF16
+  // split) with the KL-level certificate and exact recomputation of flagged
+  // rows (KL metric, loss mode). Off by default: on the GPT-2-small workload
+  // the certificate rejects every row, because the reference's own FP32
+  // logit rounding already moves per-edge KL by ~1e-5 relative (DESIGN.md
+  // §4, profiles/r2_unembed_tc_study_gpt2s.json); 0 = exact SIMT logits.
+  int64_t opt_unembed_tc = 0;
+  int64_t opt_unembed_tol_e9 = 100000;  // certificate tolerance x 1e9 (1e-4 relative KL)
 
   Engine(const cqg_config& c) : g(c) {}
   ~Engine() {
@@ -1009,6 +1017,76 @@ struct Engine {
     gemm(gj, "gemm_unembed");
   }
 
+  // ---- the patched passes' unembed on the tensor cores --------------------------
+  struct Wu6 {
+    PackedB b6;  // [V][6D] BF16 split of the FP32 image, + ||w_j|| in b6.norm
+  };
+  std::map<const float*, std::unique_ptr<Wu6>> wu6;
+  DeviceBuf ucnt;  // [0] rows flagged by the current launch, [1] running total of the call
+  bool unembed_tc_ok(const Policy& P) const {
+    return opt_unembed_tc && !opt_exact && metric == 0 && P.unemb == 2 && P.mode == 0 &&
+           (12 * g.D) % 32 == 0;
+  }
+  // LN_f -> FP32 rows xq (the exact path's operand, kept for the fallback) ->
+  // A6 split + ||a|| -> one tcgen05 GEMM (BF16, FP32 accumulators, no
+  // rounding: P32) into the logits. Last rows only (loss metrics).
+  struct UnembedTc {
+    float* xq = nullptr;
+    float* anorm = nullptr;
+    const float* wu = nullptr;  // padded FP32 image (the exact fallback's B)
+    int ldu = 0;
+    const float* wnorm = nullptr;
+    int rows = 0;
+  };
+  UnembedTc run_unembed_tc(const Policy& P, const std::vector<SegIO>& jobs, int nb) {
+    const int D = g.D, V = g.V, rows = (int)jobs.size() * nb;
+    UnembedTc u;
+    u.rows = rows;
+    u.xq = scratch("u_xq", (size_t)rows * D);
+    std::vector<LnJob> lj;
+    for (size_t j = 0; j < jobs.size(); ++j)
+      lj.push_back({jobs[j].in + (size_t)(g.S - 1) * D, nullptr, u.xq + j * (size_t)nb * D, nb, g.S * D});
+    ln(lj, g.mat(12, 0), g.mat(13, 0), P.unemb);
+    const float* wu0 = W(g.mat(14, 0), P.unemb, P.mode);
+    auto& w6 = wu6[wu0];
+    if (!w6) {
+      w6 = std::make_unique<Wu6>();
+      w6->b6.rows = V, w6->b6.cols = 6 * D, w6->b6.elem = kTcBF16;
+      w6->b6.buf.ensure((size_t)V * 6 * D * 2);
+      w6->b6.norm.ensure((size_t)V * 4);
+      launch_split_cols(wu0, D, V, w6->b6.buf.as<uint16_t>(), w6->b6.norm.as<float>(), st);
+      launched(2);
+    }
+    u.wnorm = w6->b6.norm.as<float>();
+    uint16_t* a6 = reinterpret_cast<uint16_t*>(scratch("u_a6", (size_t)rows * 3 * D));
+    u.anorm = scratch("u_anorm", (size_t)rows);
+    {
+      Prof pf(this, "unembed_split", 0, (double)rows * D * (4.0 + 12.0));
+      launch_split_rows(u.xq, rows, D, D, a6, u.anorm, st);
+    }
+    // the exact fallback's W_u (pitch-padded copy, as run_unembed)
+    u.ldu = (V + 3) & ~3;
+    auto& pad = wu_pad[wu0];
+    if (!pad) {
+      pad = std::make_unique<DeviceBuf>();
+      pad->ensure((size_t)D * u.ldu * 4);
+      CK(cudaMemsetAsync(pad->p, 0, (size_t)D * u.ldu * 4, st));
+      CK(cudaMemcpy2DAsync(pad->p, (size_t)u.ldu * 4, wu0, (size_t)V * 4, (size_t)V * 4, D,
+                           cudaMemcpyDeviceToDevice, st));
+    }
+    u.wu = pad->as<float>();
+    bool contiguous = true;
+    for (size_t j = 0; j < jobs.size(); ++j) contiguous = contiguous && jobs[j].out == jobs[0].out + j * (size_t)nb * V;
+    if (!contiguous) throw Error(2, "internal: tensor-core unembed expects contiguous logits");
+    std::vector<TcJob> tj(1);
+    TcJob& t = tj[0];
+    t = TcJob{};
+    t.a_row0 = 0, t.b_row0 = 0, t.b_k0 = 0, t.M = rows, t.N = V, t.K = 6 * D;
+    t.out_f32 = jobs[0].out, t.ldo = V, t.prec = 2, t.epi = 0;
+    gemm_tc(kTcBF16, a6, rows, 6 * D, w6->b6, tj, "unembed", u.anorm);
+    return u;
+  }
+
   void run_embed(const Policy& P, const int* d_tok, float* out, int nb) {
     const bool r4 = rtn4(P.emb, P);
     launch_embed(d_tok, W(g.mat(0, 0), P.emb, P.mode), W(g.mat(1, 0), P.emb, P.mode), out, nb, g.S,
@@ -1264,6 +1342,7 @@ struct Engine {
     for (auto& p : plans) smin = std::min(smin, p.sv), smax = std::max(smax, p.sv);
     const int last = loss ? g.n_stages - 1 : smax;
     float* logits = nullptr;
+    UnembedTc utc;  // utc.rows > 0: the logits came from the tensor cores
     std::vector<int> unembed_edges;  // plan indices whose logits were computed
     for (int s = smin; s <= last; ++s) {
       const auto& nodes = g.stage_nodes[s];
@@ -1293,7 +1372,12 @@ struct Engine {
         const size_t rows = all_rows ? (size_t)nb * g.S : (size_t)nb;
         logits = scratch("p_logits", mj.size() * rows * V);
         for (size_t j = 0; j < mj.size(); ++j) mj[j].out = logits + j * rows * V;
-        run_unembed(P, mj, nb, all_rows);
+        if (loss && unembed_tc_ok(P)) {
+          utc = run_unembed_tc(P, mj, nb);
+          stats.unembed_rows += utc.rows;
+        } else {
+          run_unembed(P, mj, nb, all_rows);
+        }
         unembed_edges = uj;
       }
       if (!loss) {  // act_diff for edges starting here (patching.cpp:249-256)
@@ -1369,8 +1453,31 @@ struct Engine {
         double* tmp = ident ? d_d : reinterpret_cast<double*>(scratch("p_kl", (size_t)rows * 2));
         reserve(up_bytes(item_of.size(), sizeof(int)));
         {
-          Prof pf(this, metric == 0 ? "kl" : "logitdiff", 0, (double)rows * V * 4.0 * 2.0);
-          if (metric == 0)
+          std::unique_ptr<Prof> pf(new Prof(this, metric == 0 ? "kl" : "logitdiff", 0, (double)rows * V * 4.0 * 2.0));
+          if (metric == 0 && utc.rows > 0) {
+            if (utc.rows != rows) throw Error(2, "internal: tensor-core unembed row count");
+            int* cnt = ucnt.as<int>();
+            int* list = reinterpret_cast<int*>(scratch("u_list", (size_t)rows));
+            const int* d_item = upload(item_of);
+            CK(cudaMemsetAsync(cnt, 0, 4, st));
+            launch_kl_cert(logits, R.logits.as<float>(), R.lse.as<double>(), d_item, rows, V, tmp, d_nan,
+                           R.prob.as<double>(), utc.anorm, utc.wnorm, g.D,
+                           (double)opt_unembed_tol_e9 * 1e-9, list, cnt, st);
+            pf.reset();  // (the fallback launches are timed under their own names)
+            // flagged rows: the reference's exact logits, then their KL
+            GemmJob xj{};
+            xj.A = utc.xq, xj.B = utc.wu, xj.C = logits;
+            xj.N = V, xj.K = g.D, xj.lda = g.D, xj.ldb = utc.ldu, xj.ldc = V, xj.prec = P.unemb;
+            {
+              Prof pf2(this, "gemm_unembed_exact_rows");
+              launch_gemm_exact_rows(xj, list, cnt, st);
+            }
+            {
+              Prof pf3(this, "kl_exact_rows");
+              launch_kl_rows(logits, R.logits.as<float>(), R.lse.as<double>(), d_item, V, tmp, d_nan,
+                             R.prob.as<double>(), list, cnt, st);
+            }
+          } else if (metric == 0)
             launch_kl(logits, R.logits.as<float>(), R.lse.as<double>(), upload(item_of), rows, V,
                       tmp, d_nan, st, R.prob.as<double>());
           else
@@ -1473,6 +1580,8 @@ struct Engine {
     DeviceBuf& nanbuf = *pool_buf("nan", 4);
     int* d_nan = nanbuf.as<int>();
     CK(cudaMemsetAsync(d_nan, 0, 4, st));
+    ucnt.ensure(8);
+    CK(cudaMemsetAsync(ucnt.p, 0, 8, st));
     Trie T;
     T.build(g, mask);
     if (full.size() == 0) full.build(g, nullptr);
@@ -1574,6 +1683,11 @@ struct Engine {
     }
     if (h_nan) throw Error(2, metric == 0 ? "metric_kl: NaN logits" : "metric_logit_diff: NaN logits");
     for (int i = 0; i < n; ++i) out[i] = sums[i] / (double)item_total;
+    if (ucnt.p) {  // patched rows whose logits the certificate sent to the exact path
+      int c[2] = {0, 0};
+      CK(cudaMemcpy(c, ucnt.p, 8, cudaMemcpyDeviceToHost));
+      stats.unembed_exact_rows = c[1];
+    }
     if (fix_cnt.p) {  // elements recomputed by the exact fixup
       uint64_t c[2] = {0, 0};
       CK(cudaMemcpy(c, fix_cnt.p, 16, cudaMemcpyDeviceToHost));
@@ -2051,6 +2165,12 @@ int cqg_set_option(cqg_ctx* ctx, const char* key, int64_t value) {
     else if (k == "exact_x2") cqg::g_exact_x2 = (int)value;
     else if (k == "profile") ctx->e->opt_profile = value;
     else if (k == "mem_budget") ctx->e->opt_mem_budget = value;
+    else if (k == "unembed_tc") ctx->e->opt_unembed_tc = value;
+    else if (k == "unembed_tol_e9") {
+      // 0: every row fails the certificate (all logits exact; a test hook)
+      if (value < 0) throw Error(1, "unembed_tol_e9 must be >= 0");
+      ctx->e->opt_unembed_tol_e9 = value;
+    }
     else throw Error(1, "cqg_set_option: unknown key " + k);
   });
 }

@@ -1000,6 +1000,71 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   }
 }
 
+// ---- the FP32 unembed on the tensor cores: 6-term BF16 split ------------------
+// x = x0 + x1 + x2 + O(2^-27 |x|) with x0 = bf16(x), x1 = bf16(x - x0),
+// x2 = bf16(x - x0 - x1) (each difference exact in FP32). The six products
+// x2 w0, x1 w1, x0 w2, x1 w0, x0 w1, x0 w0 are exact in FP32 and carry the
+// full FP32 dot product (the dropped x1 w2, x2 w1, x2 w2 are ~2^-24 relative).
+// Operands are concatenated along K (6 blocks of D), small terms first so the
+// accumulator is still small while they are added: A rows [x2|x1|x0|x1|x0|x0],
+// B rows (vocabulary columns) [w0|w1|w2|w0|w1|w0].
+__device__ __forceinline__ void split3(float x, uint16_t& h0, uint16_t& h1, uint16_t& h2) {
+  h0 = enc_bf16(x);
+  const float r1 = x - dec_bf16(h0);
+  h1 = enc_bf16(r1);
+  h2 = enc_bf16(r1 - dec_bf16(h1));
+}
+
+// one warp per row: A6 row + the row's L2 norm (the certificate's ||a||)
+__global__ void split_rows_kernel(const float* __restrict__ x, int rows, int D, int ldx,
+                                  uint16_t* __restrict__ out, float* __restrict__ anorm) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* xr = x + (int64_t)r * ldx;
+  uint16_t* o = out + (int64_t)r * 6 * D;
+  float ss = 0.f;
+  for (int k = lane; k < D; k += 32) {
+    const float v = xr[k];
+    ss = fmaf(v, v, ss);
+    uint16_t h0, h1, h2;
+    split3(v, h0, h1, h2);
+    o[k] = h2, o[D + k] = h1, o[2 * D + k] = h0, o[3 * D + k] = h1, o[4 * D + k] = h0, o[5 * D + k] = h0;
+  }
+  for (int s = 16; s > 0; s >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, s);
+  if (lane == 0) anorm[r] = sqrtf(ss);
+}
+
+// W [D][V] row-major (the FP32 unembed image) -> B6 [V][6D] + column norms
+__global__ void split_cols_kernel(const float* __restrict__ w, int D, int V, uint16_t* __restrict__ out) {
+  __shared__ float t[32][33];
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int k = k0 + i, n = n0 + threadIdx.x;
+    t[i][threadIdx.x] = (k < D && n < V) ? w[(int64_t)k * V + n] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int n = n0 + i, k = k0 + threadIdx.x;
+    if (n < V && k < D) {
+      uint16_t h0, h1, h2;
+      split3(t[threadIdx.x][i], h0, h1, h2);
+      uint16_t* o = out + (int64_t)n * 6 * D;
+      o[k] = h0, o[D + k] = h1, o[2 * D + k] = h2, o[3 * D + k] = h0, o[4 * D + k] = h1, o[5 * D + k] = h0;
+    }
+  }
+}
+
+__global__ void colnorm_kernel(const float* __restrict__ w, int D, int V, float* __restrict__ out) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= V) return;
+  float ss = 0.f;
+  for (int k = 0; k < D; ++k) {
+    const float v = w[(int64_t)k * V + n];
+    ss = fmaf(v, v, ss);
+  }
+  out[n] = sqrtf(ss);
+}
+
 __global__ void gelu_lut_kernel(uint16_t* lut) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 65536u) lut[i] = enc_bf16(round_bf16(gelu_ref(dec_bf16((uint16_t)i))));
@@ -1116,6 +1181,17 @@ void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) 
 }
 
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st) { gelu_lut_kernel<<<256, 256, 0, st>>>(lut); }
+
+void launch_split_rows(const float* x, int rows, int D, int ldx, uint16_t* out, float* anorm,
+                       cudaStream_t st) {
+  if (rows > 0) split_rows_kernel<<<(rows + 7) / 8, 256, 0, st>>>(x, rows, D, ldx, out, anorm);
+}
+
+void launch_split_cols(const float* w, int D, int V, uint16_t* out, float* wnorm, cudaStream_t st) {
+  dim3 grid((V + 31) / 32, (D + 31) / 32), block(32, 8);
+  split_cols_kernel<<<grid, block, 0, st>>>(w, D, V, out);
+  colnorm_kernel<<<(V + 255) / 256, 256, 0, st>>>(w, D, V, wnorm);
+}
 
 
 void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,

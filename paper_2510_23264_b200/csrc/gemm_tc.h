@@ -77,6 +77,13 @@ void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, i
 void launch_pack_t(const float* in, int K, int N, int ld_in, void* out, int64_t ld_out, int elem,
                    cudaStream_t st);
 
+// The FP32 unembed on the tensor cores (6-term BF16 split, gemm_tc.cu):
+// A6 [rows][6D] (+ ||a|| per row) from the FP32 LN output rows (pitch ldx),
+// and B6 [V][6D] (+ ||w_j|| per column) from the [D][V] FP32 image.
+void launch_split_rows(const float* x, int rows, int D, int ldx, uint16_t* out, float* anorm,
+                       cudaStream_t st);
+void launch_split_cols(const float* w, int D, int V, uint16_t* out, float* wnorm, cudaStream_t st);
+
 constexpr int kTcBM = 128;
 constexpr int kTcBN = 128;
 constexpr int kFixWords = kTcBM * kTcBN / 32;

@@ -805,20 +805,11 @@ __global__ void __launch_bounds__(256) gemm_exact_big_kernel(const GemmJob* __re
 // (kernels.cpp:44-52). A is staged in shared memory as broadcast pairs
 // (a, a) so that each 16-byte load feeds two rows.
 
-__global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __restrict__ jobs,
-                                                            const int* __restrict__ tile_start,
-                                                            int n_jobs, float negz) {
-  int lo = 0, hi = n_jobs - 1;
-  const int t = blockIdx.x;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (tile_start[mid] <= t) lo = mid;
-    else hi = mid - 1;
-  }
-  const GemmJob jb = jobs[lo];
-  const int local = t - tile_start[lo];
-  const int tiles_m = (jb.M + kXBM - 1) / kXBM;
-  const int m0 = (local % tiles_m) * kXBM, n0 = (local / tiles_m) * kXBN;
+// One 128 x 128 tile. MAP: logical row m of A and C is physical row
+// rowmap[m] (the exact recomputation of a device-built list of rows).
+template <bool MAP>
+__device__ __forceinline__ void x2_tile(const GemmJob& jb, int m0, int n0, const int* __restrict__ rowmap,
+                                        float negz) {
   __shared__ __align__(16) float As[2][kXBK][kXBM];  // used as the FFMA2 scalar-broadcast operand
   __shared__ __align__(16) float Bs[2][kXBK][kXBN];
   const int tid = threadIdx.x;
@@ -830,15 +821,17 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __
   // 16-byte loads where the rows are 16-byte aligned and the 4 values in range
   const bool va4 = (jb.lda & 3) == 0 && (reinterpret_cast<uintptr_t>(jb.A) & 15) == 0;
   const bool vb4 = (jb.ldb & 3) == 0 && (reinterpret_cast<uintptr_t>(jb.B) & 15) == 0;
+  const int arow = m0 + a_r;
+  const int64_t apos = arow < jb.M ? (int64_t)(MAP ? rowmap[arow] : arow) * jb.lda : 0;
   auto load = [&](int k0) {
-    const int gm = m0 + a_r, gka = k0 + a_k;
+    const int gm = arow, gka = k0 + a_k;
     if (va4 && gm < jb.M && gka + 3 < jb.K) {
-      const float4 x = __ldg(reinterpret_cast<const float4*>(jb.A + (int64_t)gm * jb.lda + gka));
+      const float4 x = __ldg(reinterpret_cast<const float4*>(jb.A + apos + gka));
       ra[0] = x.x, ra[1] = x.y, ra[2] = x.z, ra[3] = x.w;
     } else {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        ra[i] = (gm < jb.M && gka + i < jb.K) ? jb.A[(int64_t)gm * jb.lda + gka + i] : 0.f;
+        ra[i] = (gm < jb.M && gka + i < jb.K) ? jb.A[apos + gka + i] : 0.f;
     }
     const int gk2 = k0 + b_k, gnb = n0 + b_n;
     if (vb4 && gk2 < jb.K && gnb + 3 < jb.N) {
@@ -903,6 +896,7 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __
   for (int i = 0; i < 8; ++i) {
     const int gm = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
     if (gm >= jb.M) continue;
+    const int64_t crow = (int64_t)(MAP ? rowmap[gm] : gm) * jb.ldc;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int gn = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
@@ -910,9 +904,44 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __
       const f2_t pr = acc[i][j >> 1];
       float v = round_p((j & 1) ? f2_hi(pr) : f2_lo(pr), jb.prec);
       if (jb.epi == 1) v = round_p(gelu_ref(v), jb.prec);
-      jb.C[(int64_t)gm * jb.ldc + gn] = v;
+      jb.C[crow + gn] = v;
     }
   }
+}
+
+__global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __restrict__ jobs,
+                                                            const int* __restrict__ tile_start,
+                                                            int n_jobs, float negz) {
+  int lo = 0, hi = n_jobs - 1;
+  const int t = blockIdx.x;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_start[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const GemmJob jb = jobs[lo];
+  const int local = t - tile_start[lo];
+  const int tiles_m = (jb.M + kXBM - 1) / kXBM;
+  x2_tile<false>(jb, (local % tiles_m) * kXBM, (local / tiles_m) * kXBN, nullptr, negz);
+}
+
+// The exact (reference-order) GEMM over a device-built row list (rows[0 ..
+// *count)), persistent: the count is known only on the device (the unembed
+// certificate's flagged rows), so the grid loops over however many tiles it
+// implies (none: every CTA exits at once).
+__global__ void __launch_bounds__(256, 2) gemm_exact_rows_kernel(GemmJob jb, const int* __restrict__ rows,
+                                                              const int* __restrict__ count, float negz) {
+  const int cnt = *count;
+  jb.M = cnt;
+  const int tiles_m = (cnt + kXBM - 1) / kXBM, tiles_n = (jb.N + kXBN - 1) / kXBN;
+  for (int t = blockIdx.x; t < tiles_m * tiles_n; t += gridDim.x) {
+    __syncthreads();  // shared tiles of the previous iteration
+    x2_tile<true>(jb, (t % tiles_m) * kXBM, (t / tiles_m) * kXBN, rows, negz);
+  }
+}
+
+void launch_gemm_exact_rows(const GemmJob& jb, const int* rows, const int* count, cudaStream_t st) {
+  gemm_exact_rows_kernel<<<2 * 148, 256, 0, st>>>(jb, rows, count, -0.0f);
 }
 
 // Short-and-wide variant (64 x 256 tiles, 4 rows x 16 columns per thread) of
@@ -1401,19 +1430,37 @@ __device__ __forceinline__ void lse_merge(double& m, double& s, double m2, doubl
   }
 }
 
-__global__ void __launch_bounds__(kKlThreads) kl_online_kernel(const float* __restrict__ logits,
-                                                               const float* __restrict__ base,
-                                                               const double* __restrict__ base_lse,
-                                                               const int* __restrict__ item_of, int V,
-                                                               double* out, int* nan_flag,
-                                                               const double* __restrict__ base_p) {
-  __shared__ double shm[kKlThreads / 32], shs[kKlThreads / 32];
-  __shared__ double sh[32];
-  __shared__ int shi[32];
-  __shared__ double tab[64];
-  if (threadIdx.x < 64) tab[threadIdx.x] = kExp2Tab[threadIdx.x];
-  __syncthreads();
-  const int r = blockIdx.x;
+// Certificate of the tensor-core unembed (KlCert): the patched logits x~ of
+// the row came from the 6-term BF16-split tcgen05 GEMM, not the reference's
+// sequential FP32 dot products. Per column j the deviation d_j = x~_j - x_j
+// (tensor-core truncation bias + the reference's own rounding) is modelled
+// with the partial-sum scale m_j^2 = x_j^2 / 3 + ||a||^2 ||w_j||^2 / (6K)
+// (a random walk ending at x_j):
+//   |d_j| <~ c u m_j,  c = K/32 + 2 sqrt(K/12)
+// and its coherent part (the truncation shrinks every logit, ~ -u (K/64) x_j)
+// is bounded by eps_b = u K / 16 per unit of logit. The KL changes to first
+// order by sum_j (q_j - p_j) d_j, to second order by <= sum_j q_j d_j^2:
+//   E = eps_b |sum_j (q_j - p_j) x_j| + kappa c u sqrt(sum_j (q_j - p_j)^2 m_j^2)
+//       + (c u)^2 sum_j q_j m_j^2,  kappa = 8
+// A row whose E exceeds tol * KL (or whose KL is not positive and finite) is
+// listed for the exact recomputation (gemm_exact_rows + kl over the list).
+struct KlCert {
+  const float* anorm;  // [rows] ||a|| of the unembed input row (after LN)
+  const float* wnorm;  // [V] ||w_j|| of the unembed image columns
+  float K;             // D
+  double tol;
+  int* list;           // flagged rows
+  int* count;          // [0] rows listed by this launch, [1] running total (stats)
+};
+
+template <bool CERT>
+__device__ __forceinline__ void kl_online_row(int r, const float* __restrict__ logits,
+                                              const float* __restrict__ base,
+                                              const double* __restrict__ base_lse,
+                                              const int* __restrict__ item_of, int V, double* out,
+                                              int* nan_flag, const double* __restrict__ base_p,
+                                              const KlCert& C, double* shm, double* shs, double* sh,
+                                              int* shi, const double* tab) {
   const float* q = logits + (int64_t)r * V;
   const int it = item_of[r];
   const float* c = base + (int64_t)it * V;
@@ -1438,6 +1485,10 @@ __global__ void __launch_bounds__(kKlThreads) kl_online_kernel(const float* __re
     if (threadIdx.x == 0) {
       atomicOr(nan_flag, 1);
       out[r] = 0.0;
+      if (CERT) {  // (the exact path decides)
+        C.list[atomicAdd(C.count, 1)] = r;
+        atomicAdd(C.count + 1, 1);
+      }
     }
     return;
   }
@@ -1446,27 +1497,115 @@ __global__ void __launch_bounds__(kKlThreads) kl_online_kernel(const float* __re
     lse_merge(m, s, m2, s2);
   }
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
   if (l == 0) shm[w] = m, shs[w] = s;
   __syncthreads();
   m = shm[0], s = shs[0];
   for (int k = 1; k < kKlThreads / 32; ++k) lse_merge(m, s, shm[k], shs[k]);
   const double lse_q = m + log(s), lse_c = base_lse[it];
-  double kl = 0.0;
+  double kl = 0.0, g = 0.0;
+  float s2 = 0.f, q2 = 0.f;
   const double* pc = base_p ? base_p + (int64_t)it * V : nullptr;
+  const float a2k = CERT ? C.anorm[r] * C.anorm[r] / (6.f * C.K) : 0.f;
   for (int i = threadIdx.x; i < V; i += kKlThreads) {
     const double lp = (double)__ldg(c + i) - lse_c;
-    const double lq = (double)q[i] - lse_q;
-    kl += (pc ? __ldg(pc + i) : exp(lp)) * (lp - lq);
+    const float xf = q[i];
+    const double lq = (double)xf - lse_q;
+    const double pp = pc ? __ldg(pc + i) : exp(lp);
+    kl += pp * (lp - lq);
+    if (CERT) {
+      const float qf = __expf((float)lq);
+      const float dqp = qf - (float)pp;
+      const float wn = __ldg(C.wnorm + i);
+      const float m2 = xf * xf * (1.f / 3.f) + a2k * wn * wn;
+      g += (double)dqp * (double)xf;
+      s2 = fmaf(dqp * dqp, m2, s2);
+      q2 = fmaf(qf, m2, q2);
+    }
   }
   kl = block_reduce(kl, SumOp(), sh, 0.0);
+  if (CERT) {
+    g = block_reduce(g, SumOp(), sh, 0.0);
+    const double S2 = block_reduce((double)s2, SumOp(), sh, 0.0);
+    const double Q2 = block_reduce((double)q2, SumOp(), sh, 0.0);
+    if (threadIdx.x == 0) {
+      const double u = 5.9604644775390625e-08, K = C.K;
+      const double cu = (K / 32.0 + 2.0 * sqrt(K / 12.0)) * u;
+      const double E = u * K / 16.0 * fabs(g) + 8.0 * cu * sqrt(S2) + cu * cu * Q2;
+      if (!(E <= C.tol * kl)) {
+        C.list[atomicAdd(C.count, 1)] = r;
+        atomicAdd(C.count + 1, 1);
+      }
+    }
+  }
   if (threadIdx.x == 0) out[r] = kl;
+}
+
+__global__ void __launch_bounds__(kKlThreads) kl_online_kernel(const float* __restrict__ logits,
+                                                               const float* __restrict__ base,
+                                                               const double* __restrict__ base_lse,
+                                                               const int* __restrict__ item_of, int V,
+                                                               double* out, int* nan_flag,
+                                                               const double* __restrict__ base_p,
+                                                               KlCert cert, int certify) {
+  __shared__ double shm[kKlThreads / 32], shs[kKlThreads / 32];
+  __shared__ double sh[32];
+  __shared__ int shi[32];
+  __shared__ double tab[64];
+  if (threadIdx.x < 64) tab[threadIdx.x] = kExp2Tab[threadIdx.x];
+  __syncthreads();
+  if (certify)
+    kl_online_row<true>(blockIdx.x, logits, base, base_lse, item_of, V, out, nan_flag, base_p, cert,
+                        shm, shs, sh, shi, tab);
+  else
+    kl_online_row<false>(blockIdx.x, logits, base, base_lse, item_of, V, out, nan_flag, base_p, cert,
+                         shm, shs, sh, shi, tab);
+}
+
+// KL of a device-built row list (the certificate's flagged rows after their
+// exact recomputation), persistent over the device-side count.
+__global__ void __launch_bounds__(kKlThreads) kl_rows_kernel(const float* __restrict__ logits,
+                                                             const float* __restrict__ base,
+                                                             const double* __restrict__ base_lse,
+                                                             const int* __restrict__ item_of, int V,
+                                                             double* out, int* nan_flag,
+                                                             const double* __restrict__ base_p,
+                                                             const int* __restrict__ rows,
+                                                             const int* __restrict__ count) {
+  __shared__ double shm[kKlThreads / 32], shs[kKlThreads / 32];
+  __shared__ double sh[32];
+  __shared__ int shi[32];
+  __shared__ double tab[64];
+  if (threadIdx.x < 64) tab[threadIdx.x] = kExp2Tab[threadIdx.x];
+  __syncthreads();
+  const int cnt = *count;
+  const KlCert none{};
+  for (int i = blockIdx.x; i < cnt; i += gridDim.x)
+    kl_online_row<false>(rows[i], logits, base, base_lse, item_of, V, out, nan_flag, base_p, none,
+                         shm, shs, sh, shi, tab);
+}
+
+void launch_kl_rows(const float* logits, const float* base, const double* base_lse, const int* item_of,
+                    int V, double* out, int* nan_flag, const double* base_p, const int* rows,
+                    const int* count, cudaStream_t st) {
+  kl_rows_kernel<<<2 * 148, kKlThreads, 0, st>>>(logits, base, base_lse, item_of, V, out, nan_flag,
+                                                 base_p, rows, count);
+}
+
+void launch_kl_cert(const float* logits, const float* base, const double* base_lse, const int* item_of,
+                    int rows, int V, double* out, int* nan_flag, const double* base_p, const float* anorm,
+                    const float* wnorm, int K, double tol, int* list, int* count, cudaStream_t st) {
+  if (rows <= 0) return;
+  KlCert c{anorm, wnorm, (float)K, tol, list, count};
+  kl_online_kernel<<<rows, kKlThreads, 0, st>>>(logits, base, base_lse, item_of, V, out, nan_flag, base_p,
+                                                c, 1);
 }
 
 void launch_kl(const float* logits, const float* base, const double* base_lse, const int* item_of,
                int rows, int V, double* out, int* nan_flag, cudaStream_t st, const double* base_p) {
   if (rows <= 0) return;
   kl_online_kernel<<<rows, kKlThreads, 0, st>>>(logits, base, base_lse, item_of, V, out, nan_flag,
-                                                base_p);
+                                                base_p, KlCert{}, 0);
 }
 
 __global__ void logitdiff_kernel(const float* __restrict__ logits, const float* __restrict__ base,

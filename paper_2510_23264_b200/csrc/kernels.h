@@ -100,6 +100,18 @@ void launch_embed(const int* tokens, const float* we, const float* wpos, float* 
 void launch_kl(const float* logits, const float* base, const double* base_lse, const int* item_of,
                int rows, int V, double* out, int* nan_flag, cudaStream_t st,
                const double* base_p = nullptr);
+// KL with the tensor-core unembed's certificate (kernels.cu, KlCert): rows
+// whose estimated deviation from the reference's exact-logit KL exceeds tol *
+// KL are appended to list (count[0]; count[1] += the same, a running total).
+void launch_kl_cert(const float* logits, const float* base, const double* base_lse, const int* item_of,
+                    int rows, int V, double* out, int* nan_flag, const double* base_p, const float* anorm,
+                    const float* wnorm, int K, double tol, int* list, int* count, cudaStream_t st);
+// the KL of the listed rows (rows[0 .. *count)), persistent grid
+void launch_kl_rows(const float* logits, const float* base, const double* base_lse, const int* item_of,
+                    int V, double* out, int* nan_flag, const double* base_p, const int* rows,
+                    const int* count, cudaStream_t st);
+// the exact GEMM of jb over the listed rows of A / C (jb.M ignored)
+void launch_gemm_exact_rows(const GemmJob& jb, const int* rows, const int* count, cudaStream_t st);
 void launch_lse(const float* base, int rows, int V, double* lse, int* nan_flag, cudaStream_t st,
                 double* p_out = nullptr);
 void launch_logitdiff(const float* logits, const float* base, const int* item_of,

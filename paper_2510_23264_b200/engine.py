@@ -49,7 +49,8 @@ class CqgConfig(C.Structure):
 class CqgStats(C.Structure):
     _fields_ = [("ms_total", C.c_double), ("ms_device", C.c_double), ("ms_baseline", C.c_double),
                 ("ms_passes", C.c_double), ("passes", C.c_int64), ("kernel_launches", C.c_int64),
-                ("fallback_elems", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+                ("fallback_elems", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("unembed_rows", C.c_int64), ("unembed_exact_rows", C.c_int64)]
 
 
 @dataclass
@@ -287,7 +288,9 @@ def sweep_order(cfg: ModelConfig, mask: np.ndarray) -> np.ndarray:
 class Engine:
     """One GPU context (cqg_ctx): HBM-resident weights + dataset shard."""
 
-    def __init__(self, weights: WeightSet, device: int = 0):
+    def __init__(self, weights: WeightSet, device: int = 0, options: Optional[dict] = None):
+        """options: cqg_set_option knobs applied at creation (after any given
+        in the CQG_OPTS environment variable, "key=value,key=value")."""
         self.lib = load_library()
         self.cfg = weights.cfg
         self.cfg.validate()
@@ -301,6 +304,13 @@ class Engine:
         self.n_nodes, self.edge_src, self.edge_dst = graph_edges(self.cfg)
         self.n_edges = len(self.edge_src)
         self.n_items = 0
+        opts = {}
+        for kv in filter(None, os.environ.get("CQG_OPTS", "").split(",")):
+            k, v = kv.split("=")
+            opts[k.strip()] = int(v)
+        opts.update(options or {})
+        for k, v in opts.items():
+            self.set_option(k, v)
 
     def close(self):
         if getattr(self, "h", None):

@@ -34,3 +34,4 @@ def ref():
     if not ref_available():
         pytest.skip("oracle/_ref/libcqref.so not built (needs /root/reference)")
     return Ref()
+
