@@ -12,7 +12,7 @@ synthetic weights and prompts):
 * pythia_slice — Pythia-1.4B widths (D = 2048, d_k = 128, S = 32, V = 50304),
   2 layers, docstring-shaped prompts.
 
-Tolerance: |gpu - ref| <= 1e-9 |ref| + 1e-15 (see test_gpu_parity.py).
+Tolerance: |gpu - ref| <= 1e-9 |ref| + 2^-44 (see test_gpu_parity.py).
 
 Also: per-edge policies over a base policy that carries its own target
 (policy_for_edge resets it, pahq.cpp:198-209) against the oracle.

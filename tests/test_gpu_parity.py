@@ -2,10 +2,15 @@
 
 Tolerances (written here, per BASELINE.json north star):
 * quantized tensors and every FP32 activation: bit-exact (uint32 compare);
-* per-edge scores: |gpu - ref| <= 1e-9 * |ref| + 1e-15. The only
+* per-edge scores: |gpu - ref| <= 1e-9 * |ref| + 2^-44. The only
   non-bitwise step is the FP64 log-softmax/KL reduction order over the
-  vocabulary (parallel tree vs the reference's sequential sum), whose
-  relative effect is ~1e-15; the north-star bar is 1e-4 relative.
+  vocabulary (parallel tree vs the reference's sequential sum). Its effect
+  is relative to the TERMS of the sum, not to the KL: every term carries
+  lq_v = x_v - lse, and one ulp of lse (2^-49 at lse ~ log V ~ 10.8) moves
+  the KL by ~2^-49 absolute. Measured: exactly 2^-48 on the Pythia-width
+  slice (V = 50304, KL ~ 6e-8), with every node output bitwise equal
+  (tools/debug_slice.py). 2^-44 = 32 such ulps; the north-star bar is 1e-4
+  relative.
 * pruned edge sets: identical.
 """
 import concurrent.futures as cf
@@ -23,7 +28,7 @@ from helpers import GOLDEN, SMALL, TINY, TOY, bits, make, random_mask
 
 pytestmark = pytest.mark.gpu
 G = json.load(open(os.path.join(GOLDEN, "golden.json")))
-RTOL, ATOL = 1e-9, 1e-15
+RTOL, ATOL = 1e-9, 2.0 ** -44
 
 
 def close(a, b):
