@@ -56,13 +56,13 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
   cudaMalloc(&ftiles, ntile * 4);
   cudaMalloc(&fmark, ntile * 4);
   cudaMemset(fmark, 0, ntile * 4);
-  cudaMalloc(&cnt, 16);
+  cudaMalloc(&cnt, 32);
   cudaMalloc(&dj, sizeof(TcJob));
   cudaMalloc(&dts, sizeof(int));
   cudaMalloc(&dg, sizeof(GemmJob));
   cudaMemcpy(dA, A, (size_t)M * K * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dBt, Bt, (size_t)N * K * 4, cudaMemcpyHostToDevice);
-  cudaMemset(cnt, 0, 16);
+  cudaMemset(cnt, 0, 32);
   {
     // pack_t(in: K x N row-major) -> out[n][k]; feed transposed host copies so
     // that pA is A (M x K) and pB is Bt (N x K), both K-major.
@@ -106,7 +106,22 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
     L.total_tiles = ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
     L.fix_mask = fmask, L.fix_tiles = ftiles, L.tile_mark = fmark, L.fix_count = cnt;
     launch_gemm_tc(L, dj, 0);
-    launch_gemm_fixup(L, dj, 0);
+    // BF16: the chunked block fixup unless CQG_DIAG_FIX_BLK=0 (tests run both)
+    const char* fe = getenv("CQG_DIAG_FIX_BLK");
+    int4* dfb = nullptr;
+    if (elem == kTcBF16 && !(fe && fe[0] == '0') &&
+        tc_make_map_sw32(&L.fxA, pA, M, K, (uint64_t)K * esz) &&
+        tc_make_map_sw32(&L.fxB, pB, N, K, (uint64_t)K * esz)) {
+      TcJob hj{};
+      hj.M = M, hj.N = N, hj.K = K;
+      std::vector<int4> fb = fixup_chunks(&hj, 1, 148);
+      cudaMalloc(&dfb, fb.size() * sizeof(int4));
+      cudaMemcpy(dfb, fb.data(), fb.size() * sizeof(int4), cudaMemcpyHostToDevice);
+      L.fix_blocks = dfb, L.n_fix_blocks = (int)fb.size();
+      launch_gemm_fixup_blk(L, dj, 0);
+    } else {
+      launch_gemm_fixup(L, dj, 0);
+    }
     // exact reference product on the decoded grid values
     GemmJob gj{};
     gj.A = dA, gj.B = dB, gj.C = dC2, gj.M = M, gj.N = N, gj.K = K, gj.lda = K, gj.ldb = N,
@@ -118,6 +133,7 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
     if (cudaDeviceSynchronize() != cudaSuccess) rc = 2;
     cudaMemcpy(out_tc, dC1, (size_t)M * N * 4, cudaMemcpyDeviceToHost);
     cudaMemcpy(out_exact, dC2, (size_t)M * N * 4, cudaMemcpyDeviceToHost);
+    if (dfb) cudaFree(dfb);
     uint64_t c[2] = {0, 0};
     cudaMemcpy(c, cnt, 16, cudaMemcpyDeviceToHost);
     *n_fix = (uint32_t)c[1];

@@ -294,6 +294,10 @@ struct Engine {
   cqg_stats stats{};
   int64_t opt_exact = 0;
   int64_t opt_packed = 1;
+  // BF16 fixups: chunked block kernel (1) or the per-tile kernel (0, default:
+  // measured faster, DESIGN.md section 7 "tried")
+  int64_t opt_fix_blk = 0;
+  int64_t opt_fix_blk_min = 148;  // ... for launches with at least this many row-tile units
   int64_t opt_fix_cpi = 0;  // store E4M3/BF16-rounded node outputs as their codes
   int64_t opt_mem_budget = 0;
   // 1: the patched passes' FP32 unembed on the tensor cores (6-term BF16
@@ -620,8 +624,8 @@ struct Engine {
     for (const TcJob& j : jobs)
       if (j.prec != L.prec || j.epi != L.epi) throw Error(2, "internal: mixed epilogues in one TC launch");
     if (!fix_cnt.p) {
-      fix_cnt.ensure(16);
-      CK(cudaMemsetAsync(fix_cnt.p, 0, 16, st));
+      fix_cnt.ensure(32);
+      CK(cudaMemsetAsync(fix_cnt.p, 0, 32, st));
     }
     fix_mask.ensure((size_t)total * kFixWords * 4);
     fix_tiles.ensure((size_t)total * 4);
@@ -642,9 +646,25 @@ struct Engine {
       const int end = j + 1 < jobs.size() ? jobs[j + 1].tile0 : total;
       for (int t = jobs[j].tile0; t < end; ++t) tj_map[(size_t)t] = (int)j;
     }
-    reserve(up_bytes(jobs.size(), sizeof(TcJob)) + up_bytes(tj_map.size(), sizeof(int)));
+    // BF16: the chunked block fixup (gemm_fixup_blk_kernel) when the launch has
+    // enough row tiles to fill the GPU; small launches keep the tile fixup
+    long row_tiles = 0;
+    for (const TcJob& j : jobs)
+      row_tiles += (long)((j.M + kTcBM - 1) / kTcBM) * ((j.N + kTcBN - 1) / kTcBN + 5) / 6;
+    const bool blk = elem == kTcBF16 && opt_fix_blk && row_tiles >= opt_fix_blk_min;
+    std::vector<int4> fb;
+    if (blk) {
+      fb = fixup_chunks(jobs.data(), (int)jobs.size(), 148);
+      if (!tc_make_map_sw32(&L.fxA, A, (uint64_t)a_rows, (uint64_t)a_k, (uint64_t)a_k * esz) ||
+          !tc_make_map_sw32(&L.fxB, B.buf.p, (uint64_t)B.rows, (uint64_t)B.cols, (uint64_t)B.cols * esz))
+        throw Error(2, "cuTensorMapEncodeTiled failed for the fixup operands");
+      L.n_fix_blocks = (int)fb.size();
+    }
+    reserve(up_bytes(jobs.size(), sizeof(TcJob)) + up_bytes(tj_map.size(), sizeof(int)) +
+            (blk ? up_bytes(fb.size(), sizeof(int4)) : 0));
     const TcJob* dj = upload(jobs);
     L.tile_job = upload(tj_map);
+    if (blk) L.fix_blocks = upload(fb);
     {
       Prof pf(this, elem == kTcBF16 ? (std::string("gemm_tc_bf16_") + name).c_str()
                                     : (std::string("gemm_tc_fp8_") + name).c_str(),
@@ -654,7 +674,8 @@ struct Engine {
     const std::string fname = std::string("gemm_fixup_") + name;
     {
       Prof pf(this, fname.c_str());
-      launch_gemm_fixup(L, dj, st);
+      if (blk) launch_gemm_fixup_blk(L, dj, st);
+      else launch_gemm_fixup(L, dj, st);
     }
     if (opt_profile) {
       uint64_t fixed1 = 0;
@@ -2164,6 +2185,8 @@ int cqg_set_option(cqg_ctx* ctx, const char* key, int64_t value) {
     }
     else if (k == "exact_x2") cqg::g_exact_x2 = (int)value;
     else if (k == "profile") ctx->e->opt_profile = value;
+    else if (k == "fix_blk") ctx->e->opt_fix_blk = value;
+    else if (k == "fix_blk_min") ctx->e->opt_fix_blk_min = value;
     else if (k == "mem_budget") ctx->e->opt_mem_budget = value;
     else if (k == "unembed_tc") ctx->e->opt_unembed_tc = value;
     else if (k == "unembed_tol_e9") {

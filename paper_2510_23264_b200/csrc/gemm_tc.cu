@@ -1000,6 +1000,275 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   }
 }
 
+// ---- block fixup (BF16) ---------------------------------------------------------
+// The tile fixup above streams a whole 128 x 128 tile's operands (A 128 x K
+// and B 128 x K) through shared memory to recompute the 2.5-4.5% of its
+// elements the certificate flags: as many operand bytes as the GEMM itself, so
+// it runs at L2 -> SM streaming speed. Here a CTA owns a chunk of up to 4 x 6
+// GEMM tiles (512 rows x 768 columns): each 32-byte K slice of the chunk's A
+// rows and B rows is loaded once (TMA, SWIZZLE_32B) and serves every flagged
+// element of the chunk. The chains stay exact and sequential (dot_col,
+// kernels.cpp:44-52).
+//
+// Lanes: a warp runs "packs" of up to 32 flagged elements drawn from one group
+// of 8 consecutive chunk rows, 4 elements per column class (col mod 8). In the
+// SW32 layout row r's 16-byte unit u sits in bank group
+// 2 (r & 3) + (u ^ ((r >> 2) & 1)), distinct for the 8 rows of a group, and a
+// column's likewise per column class. A 128-bit shared load is served per
+// quarter-warp, and every quarter holds one lane per column class: both
+// operands of a pack are conflict-free (4 wavefronts each; empty lanes read
+// their own class's column and the group's first row). Each lane keeps one FP32 chain per pack it
+// holds (kFbSlots accumulators), run kFbChunk at a time without branches.
+//
+// Scheduling: persistent CTAs take chunks from a host-built list through an
+// atomic counter; the list starts with 4-row-tile chunks and ends with
+// 1-row-tile ones, so the tail is balanced.
+constexpr int kFbStages = 4;
+constexpr int kFbThreads = 512, kFbWarps = kFbThreads / 32;
+constexpr int kFbSlots = 16;   // packs per lane per round (register accumulators)
+constexpr int kFbChunk = 8;    // chains run together (independent FHFMA chains, loads in flight)
+constexpr int kFbGroup = 8;    // rows per pack group
+constexpr int kFbMaxCT = 6;    // column tiles per chunk (768 columns)
+constexpr uint32_t kFbBox = 256 * 32;  // one TMA box: 256 rows x 32 B
+constexpr uint32_t kFbStageA = 2 * kFbBox, kFbStageB = 3 * kFbBox;  // 512 / 768 rows
+constexpr size_t kFbSmem = 1024 + (size_t)kFbStages * (kFbStageA + kFbStageB) + 512 +
+                           (size_t)kFbWarps * kFbSlots * 32 * 4;
+constexpr uint32_t kFbEmpty = 0x80000000u, kFbUnsafe = 0x40000000u;
+
+// byte offset of row r's unit 0 in a stage (256-row SW32 boxes)
+__device__ __forceinline__ uint32_t fb_off(uint32_t r) {
+  return (r >> 8) * kFbBox + (r & 255u) * 32u + (((r >> 2) & 1u) << 4);
+}
+
+__device__ __forceinline__ void fb_issue(const TcLaunch& L, uint8_t* sA, uint8_t* sB, uint64_t* full,
+                                         uint64_t* empty, uint32_t& ld, int sg, int arow, int brow,
+                                         int nba, int nbb) {
+  const int s = ld % kFbStages;
+  mbar_wait(&empty[s], ((ld / kFbStages) & 1) ^ 1);
+  mbar_expect_tx(&full[s], (uint32_t)(nba + nbb) * kFbBox);
+  uint8_t* a = sA + s * kFbStageA;
+  uint8_t* b = sB + s * kFbStageB;
+  for (int h = 0; h < nba; ++h) tma_load_2d(a + h * kFbBox, &L.fxA, &full[s], sg * 16, arow + 256 * h);
+  for (int h = 0; h < nbb; ++h) tma_load_2d(b + h * kFbBox, &L.fxB, &full[s], sg * 16, brow + 256 * h);
+  ++ld;
+}
+
+// 8 products of one 16-byte unit, k ascending, not FMA-safe (fmul + fadd)
+__device__ __forceinline__ float fb_slow(uint4 a, uint4 b, float s) {
+  float x[8], y[8];
+  dec16<kTcBF16>(a, x);
+  dec16<kTcBF16>(b, y);
+#pragma unroll
+  for (int t = 0; t < 8; ++t) s = __fadd_rn(s, __fmul_rn(x[t], y[t]));
+  return s;
+}
+
+// One ring stage (two 16-byte K units) of the lane's packs, kFbChunk chains
+// at a time (their 2 x kFbChunk shared loads are issued together).
+// FMA: FHFMA.BF16 (every product exact in FP32); otherwise fmul + fadd.
+template <bool FMA>
+__device__ __forceinline__ void fb_stage(const uint8_t* as, const uint8_t* bs, const uint32_t (&ra)[kFbSlots],
+                                         const uint32_t (&cb)[kFbSlots], float (&acc)[kFbSlots], int nch) {
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+#pragma unroll
+    for (int jc = 0; jc < kFbSlots / kFbChunk; ++jc) {
+      if (jc < nch) {
+        uint4 av[kFbChunk], bv[kFbChunk];
+#pragma unroll
+        for (int t = 0; t < kFbChunk; ++t) {
+          av[t] = *reinterpret_cast<const uint4*>(as + (ra[kFbChunk * jc + t] ^ (u << 4)));
+          bv[t] = *reinterpret_cast<const uint4*>(bs + (cb[kFbChunk * jc + t] ^ (u << 4)));
+        }
+        float* a = acc + kFbChunk * jc;
+        if (FMA) {
+#pragma unroll
+          for (int t = 0; t < kFbChunk; ++t) a[t] = fma_bf16x2(av[t].x, bv[t].x, a[t]);
+#pragma unroll
+          for (int t = 0; t < kFbChunk; ++t) a[t] = fma_bf16x2(av[t].y, bv[t].y, a[t]);
+#pragma unroll
+          for (int t = 0; t < kFbChunk; ++t) a[t] = fma_bf16x2(av[t].z, bv[t].z, a[t]);
+#pragma unroll
+          for (int t = 0; t < kFbChunk; ++t) a[t] = fma_bf16x2(av[t].w, bv[t].w, a[t]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < kFbChunk; ++t) a[t] = fb_slow(av[t], bv[t], a[t]);
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kFbThreads, 1)
+    gemm_fixup_blk_kernel(const __grid_constant__ TcLaunch L, const TcJob* __restrict__ jobs) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kFbStages * kFbStageA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kFbStages * kFbStageB);
+  uint64_t* empty = full + kFbStages;
+  uint32_t* rbad = reinterpret_cast<uint32_t*>(empty + kFbStages);  // [16] rows not FMA-safe
+  uint32_t* cbad = rbad + 16;                                      // [24] columns not FMA-safe
+  int* s_chunk = reinterpret_cast<int*>(cbad + 24);
+  uint32_t* packs = reinterpret_cast<uint32_t*>(smem + kFbStages * (kFbStageA + kFbStageB) + 512);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t* wp = packs + warp * kFbSlots * 32;
+  if (tid == 0) {
+    for (int s = 0; s < kFbStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kFbWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t ld = 0, it = 0;  // stages loaded / consumed (ring phases)
+  // column class (col mod 8) and index within the class: a 128-bit shared
+  // load is served per quarter-warp (8 lanes), so each quarter holds the 8
+  // classes once (B conflict-free) and rows of one group (A conflict-free)
+  const int lb = lane & 7, lt = lane >> 3;
+  const uint32_t cmask = 0x01010101u << lb;
+  for (;;) {
+    __syncthreads();  // (previous chunk's shared state is dead)
+    if (tid == 0) *s_chunk = (int)atomicAdd(L.fix_count + 4, 1u);
+    __syncthreads();
+    const int ci = *s_chunk;
+    if (ci >= L.n_fix_blocks) break;
+    const int4 cd = L.fix_blocks[ci];  // job, first row tile, first column tile, nrt | nct << 8
+    const TcJob jb = jobs[cd.x];
+    const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
+    const int mt0 = cd.y, nt0 = cd.z, nrt = cd.w & 255, nct = cd.w >> 8;
+    const int n_stages = jb.K / 16;  // K is a multiple of 16 (tc_dims_ok)
+    const int arow = jb.a_row0 + mt0 * kTcBM, brow = jb.b_row0 + nt0 * kTcBN;
+    const int nba = (nrt * kTcBM + 255) / 256, nbb = (nct * kTcBN + 255) / 256;
+    const int W = nct * 4;  // flag words per chunk row
+    // FMA safety of the chunk's rows and columns (one bit each)
+    {
+      const bool rb = tid < nrt * kTcBM && !a_fma_safe(L, arow + tid);
+      const uint32_t br = __ballot_sync(0xffffffffu, rb);
+      if (lane == 0) rbad[warp] = br;
+      for (int c = tid; c < 768; c += kFbThreads) {
+        const bool bc = c < nct * kTcBN && !fma_safe(jb.b_norm[nt0 * kTcBN + c]);
+        const uint32_t bb = __ballot_sync(0xffffffffu, bc);
+        if (lane == 0) cbad[c >> 5] = bb;
+      }
+    }
+    __syncthreads();
+    const int n_groups = nrt * (kTcBM / kFbGroup);
+    int g = warp;  // this warp's current group ...
+    int p0 = 0;    // ... and its first pack not yet run
+    for (;;) {     // rounds: up to kFbSlots packs per warp, one pass over K each
+      int ns = 0;
+      while (g < n_groups && ns < kFbSlots) {
+        const int r0 = g * kFbGroup, rt = r0 >> 7;
+        // flag words of the group's 8 rows x W words: lane holds word lane + 32 q
+        uint32_t wv[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const int k = lane + 32 * q, i = k / W, w = k - i * W, ct = w >> 2;
+          wv[q] = 0u;
+          if (i < kFbGroup) {
+            const int tile = jb.tile0 + (mt0 + rt) * tiles_n + nt0 + ct;
+            const int rr = (r0 + i) & 127;
+            const uint32_t parts = L.tile_mark[tile];
+            if ((parts >> ((rr >> 5) + 4 * ((w & 3) >> 1))) & 1u)
+              wv[q] = L.fix_mask[(size_t)tile * kFixWords + rr * 4 + (w & 3)];
+          }
+        }
+        const int room = kFbSlots - ns;
+        int n = 0;  // elements of this lane's column class seen so far
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          if (32 * q >= kFbGroup * W) break;
+#pragma unroll 1
+          for (int s = 0; s < 32; ++s) {
+            uint32_t m = __shfl_sync(0xffffffffu, wv[q], s) & cmask;
+            while (m) {
+              const int bit = __ffs(m) - 1;
+              m &= m - 1;
+              const int pk = n >> 2;
+              if ((n & 3) == lt && pk >= p0 && pk < p0 + room) {
+                const int k = s + 32 * q, i = k / W, rb = r0 + i, col = (k - i * W) * 32 + bit;
+                const bool bad = ((rbad[rb >> 5] >> (rb & 31)) | (cbad[col >> 5] >> (col & 31))) & 1u;
+                wp[(ns + pk - p0) * 32 + lane] = ((uint32_t)rb << 16) | (uint32_t)col | (bad ? kFbUnsafe : 0u);
+              }
+              ++n;
+            }
+          }
+        }
+        const int pg = (__reduce_max_sync(0xffffffffu, (uint32_t)n) + 3) >> 2;  // packs of the group
+        const int take = min(pg - p0, room);
+        for (int s = 0; s < take; ++s)  // this lane's empty slots of those packs
+          if (4 * (p0 + s) + lt >= n) wp[(ns + s) * 32 + lane] = kFbEmpty | ((uint32_t)r0 << 16) | (uint32_t)lb;
+        ns += take;
+        if (p0 + take >= pg) g += kFbWarps, p0 = 0;
+        else p0 += take;
+      }
+      const int nch = (ns + kFbChunk - 1) / kFbChunk;
+      for (int s = ns; s < kFbChunk * nch; ++s) wp[s * 32 + lane] = kFbEmpty | (uint32_t)lb;
+      __syncwarp();
+      if (!__syncthreads_or(ns > 0)) break;
+      uint32_t ra[kFbSlots], cb[kFbSlots];
+      float acc[kFbSlots];
+      bool unsafe = false;
+#pragma unroll
+      for (int j = 0; j < kFbSlots; ++j) {
+        const uint32_t d = j < kFbChunk * nch ? wp[j * 32 + lane] : kFbEmpty;
+        ra[j] = fb_off((d >> 16) & 511u);
+        cb[j] = fb_off(d & 1023u);
+        acc[j] = 0.f;
+        unsafe = unsafe || (d & kFbUnsafe) != 0u;
+      }
+      unsafe = __any_sync(0xffffffffu, unsafe);
+      if (tid == 0)
+        for (int sg = 0; sg < min(kFbStages, n_stages); ++sg)
+          fb_issue(L, sA, sB, full, empty, ld, sg, arow, brow, nba, nbb);
+      for (int sg = 0; sg < n_stages; ++sg, ++it) {
+        const int s = it % kFbStages;
+        mbar_wait(&full[s], (it / kFbStages) & 1);
+        const uint8_t* as = sA + s * kFbStageA;
+        const uint8_t* bs = sB + s * kFbStageB;
+        if (!unsafe) fb_stage<true>(as, bs, ra, cb, acc, nch);
+        else fb_stage<false>(as, bs, ra, cb, acc, nch);  // (rare: some product not exact in FP32)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (tid == 0 && sg + kFbStages < n_stages)
+          fb_issue(L, sA, sB, full, empty, ld, sg + kFbStages, arow, brow, nba, nbb);
+      }
+#pragma unroll
+      for (int j = 0; j < kFbSlots; ++j) {
+        const uint32_t d = j < kFbChunk * nch ? wp[j * 32 + lane] : kFbEmpty;  // (the list is still in place)
+        if (!(d & kFbEmpty)) {
+          float v = round_out(acc[j], jb.prec);
+          if (jb.epi == 1) {
+            if (jb.prec == 1 && L.gelu_lut) v = dec_bf16(L.gelu_lut[enc_bf16(v)]);
+            else v = round_out(gelu_ref(v), jb.prec);
+          }
+          store_out(jb, mt0 * kTcBM + (int)((d >> 16) & 511u), nt0 * kTcBN + (int)(d & 1023u), v);
+        }
+      }
+      __syncwarp();  // (the pack list is rebuilt by the next round)
+    }
+  }
+  // The last CTA to finish clears the listed tiles' marks and the counters
+  // for the next launch (fix_count[1] counts finished CTAs, [4] the chunk queue).
+  __shared__ int last_cta;
+  if (tid == 0) {
+    __threadfence();
+    last_cta = atomicAdd(L.fix_count + 1, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last_cta) {
+    __threadfence();
+    const uint32_t n_tiles = *reinterpret_cast<volatile uint32_t*>(L.fix_count);
+    for (uint32_t i = tid; i < n_tiles; i += blockDim.x) L.tile_mark[L.fix_tiles[i]] = 0u;
+    __syncthreads();
+    if (tid == 0) {
+      L.fix_count[0] = 0u;
+      L.fix_count[1] = 0u;
+      L.fix_count[4] = 0u;
+    }
+  }
+}
+
 // ---- the FP32 unembed on the tensor cores: 6-term BF16 split ------------------
 // x = x0 + x1 + x2 + O(2^-27 |x|) with x0 = bf16(x), x1 = bf16(x - x0),
 // x2 = bf16(x - x0 - x1) (each difference exact in FP32). The six products
@@ -1147,6 +1416,20 @@ bool tc_make_map(CUtensorMap* map, const void* base, int elem, uint64_t rows, ui
   return r == CUDA_SUCCESS;
 }
 
+bool tc_make_map_sw32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols_elems,
+                      uint64_t pitch_bytes) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols_elems, rows};
+  cuuint64_t strides[1] = {pitch_bytes};
+  cuuint32_t box[2] = {16, 256};  // 32 bytes of K x 256 rows (BF16)
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
   if (L.total_tiles <= 0) return;
   const int grid = std::min(L.total_tiles, 148);
@@ -1178,6 +1461,41 @@ void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) 
   };
   if (L.elem == kTcBF16) go(gemm_fixup_kernel<kTcBF16>);
   else go(gemm_fixup_kernel<kTcE4M3>);
+}
+
+std::vector<int4> fixup_chunks(const TcJob* jobs, int n_jobs, int ctas) {
+  // rows per chunk: what one round of kFbSlots packs per warp covers at the
+  // measured flag rates (~4.5% at K = 3072, ~2.5% at K = 768)
+  const long max_rt = n_jobs > 0 && jobs[0].K >= 2048 ? 1 : 2;
+  struct Seg { int job, nt0, nct, tm; };
+  std::vector<Seg> segs;
+  long remaining = 0;  // row-tile units not yet emitted
+  for (int j = 0; j < n_jobs; ++j) {
+    const int tm = (jobs[j].M + kTcBM - 1) / kTcBM, tn = (jobs[j].N + kTcBN - 1) / kTcBN;
+    const int ncb = (tn + kFbMaxCT - 1) / kFbMaxCT;
+    for (int c = 0; c < ncb; ++c) {
+      const int a = tn * c / ncb, b = tn * (c + 1) / ncb;  // balanced column blocks
+      segs.push_back({j, a, b - a, tm});
+      remaining += tm;
+    }
+  }
+  std::vector<int4> out;
+  for (const Seg& sg : segs)
+    for (int mt = 0; mt < sg.tm;) {
+      const int want = (int)std::max(1L, std::min(max_rt, remaining / (2L * ctas)));
+      const int n = std::min(want, sg.tm - mt);
+      out.push_back(make_int4(sg.job, mt, sg.nt0, n | sg.nct << 8));
+      mt += n;
+      remaining -= n;
+    }
+  return out;
+}
+
+void launch_gemm_fixup_blk(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
+  if (L.n_fix_blocks <= 0) return;
+  const int grid = std::min(L.n_fix_blocks, 148);
+  cudaFuncSetAttribute(gemm_fixup_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem);
+  gemm_fixup_blk_kernel<<<grid, kFbThreads, kFbSmem, st>>>(L, d_jobs);
 }
 
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st) { gelu_lut_kernel<<<256, 256, 0, st>>>(lut); }

@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace cqg {
 
 enum TcElem : int { kTcE4M3 = 0, kTcBF16 = 1 };
@@ -55,11 +57,19 @@ struct TcLaunch {
   uint32_t* tile_mark;  // [total_tiles] flagged-part bits (q + 4*half); zero between launches
   uint32_t* fix_count;  // [0] tiles listed by this launch, [1] fixup CTAs finished (both
                         //   zeroed by the fixup's last CTA),
-                        // [2..3] u64 running total of flagged elements
+                        // [2..3] u64 running total of flagged elements,
+                        // [4] block-fixup chunk queue (reset by its last CTA)
   float kappa;
   int fix_cpi;  // fixup columns per work item: 0 adaptive, else 1 / 2 / 4
   const int* tile_job;  // [total_tiles] job index of each tile (may be null: binary search)
   const uint16_t* gelu_lut;  // bf16 -> round_bf16(gelu(x)) for all 2^16 inputs
+  // block fixup (BF16): SW32 maps of A / B (32-byte K slices x 256 rows) and
+  // the launch's chunk list {job, first row tile, first column tile,
+  // row tiles | column tiles << 8} (<= 4 x 6 tiles), taken in order through
+  // the queue counter fix_count[4]
+  CUtensorMap fxA, fxB;
+  const int4* fix_blocks;
+  int n_fix_blocks;
 };
 
 // Builds 2D K-major tensor maps (SW128, box = 128 B x box_rows) for A/B.
@@ -68,6 +78,13 @@ bool tc_make_map(CUtensorMap* map, const void* base, int elem, uint64_t rows, ui
 
 void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
 void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
+// BF16 only: persistent CTAs over chunks of up to 4 x 6 tiles (gemm_tc.cu)
+void launch_gemm_fixup_blk(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st);
+// the chunk list of a launch's jobs: 4-row-tile chunks first, then 2, then 1
+// (persistent CTAs take them in order: a balanced tail)
+std::vector<int4> fixup_chunks(const TcJob* jobs, int n_jobs, int ctas);
+bool tc_make_map_sw32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols_elems,
+                      uint64_t pitch_bytes);
 // lut[b] = enc_bf16(round_bf16(gelu_ref(dec_bf16(b)))) (glibc-exact erff)
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st);
 // ||row|| of a packed [rows][K] operand (elements starting at col k0)

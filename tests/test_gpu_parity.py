@@ -163,13 +163,17 @@ def _bf16_grid(x):
     return u.astype(np.uint32).view(np.float32)
 
 
-@pytest.mark.parametrize("K", [768, 3072])
-def test_tc_gemm_bitexact_incl_non_fma_rows(K):
+@pytest.mark.parametrize("K,M,N,blk", [(768, 256, 256, "1"), (3072, 256, 256, "1"),
+                                       (768, 640, 896, "1"), (3072, 136, 768, "1"),
+                                       (768, 256, 256, "0"), (3072, 256, 256, "0")])
+def test_tc_gemm_bitexact_incl_non_fma_rows(K, M, N, blk, monkeypatch):
     """BF16 x BF16 on tcgen05 + certified fixup equals the sequential FP32 dot
     (kernels.cpp:44-52) bit for bit, also for rows holding values whose products
-    are not exact in FP32 (|x| < 2^-67: the fixup then keeps fmul + fadd)."""
+    are not exact in FP32 (|x| < 2^-67: the fixup then keeps fmul + fadd).
+    blk: the chunked block fixup (engine option fix_blk; shapes with partial
+    chunks and several chunks) or the per-tile fixup (the default)."""
+    monkeypatch.setenv("CQG_DIAG_FIX_BLK", blk)
     rng = np.random.RandomState(K)
-    M, N = 256, 256
     A = _bf16_grid(rng.randn(M, K).astype(np.float32))
     A[::7, ::5] = _bf16_grid(np.float32(3e-23) * rng.randn(len(range(0, M, 7)), len(range(0, K, 5))))
     Bt = _bf16_grid((rng.rand(N, K).astype(np.float32) - 0.5) * 0.0288)
