@@ -45,6 +45,10 @@ CONFIGS = {
     # configs[3]: GPT-2-medium shape, batch 256
     "gpt2m": dict(cfg=formats.ModelConfig(24, 16, 1024, 64, 50257, 16, 1, 1), items=256,
                   data="ioi"),
+    # configs[4]: Pythia-1.4B shape (d_k = 128, V = 50304), docstring-shaped prompts
+    # (S = 32); batch 512 over 8 GPUs, i.e. 64 items per GPU
+    "pythia": dict(cfg=formats.ModelConfig(24, 16, 2048, 128, 50304, 32, 1, 1), items=512,
+                   data="docstring"),
 }
 METRIC = "patched forward passes/sec and ACDC end-to-end s (1/2/4/8 B200 vs host CPU)"
 
@@ -67,6 +71,8 @@ def make_inputs(name):
         ds = synth.ioi_dataset(cfg, c["items"], 1)
     elif c["data"] == "greater_than":
         ds = synth.greater_than_dataset(cfg, c["items"], 1)
+    elif c["data"] == "docstring":
+        ds = synth.docstring_dataset(cfg, c["items"], 1)
     else:
         ds = synth.random_dataset(cfg, c["items"], 2)
     return cfg, w, ds
@@ -254,16 +260,25 @@ def run_reference(args):
     print(json.dumps(out))
 
 
-def config_block(args):
+def config_block(args, n_edges_all=None, n_scored=None):
     c = CONFIGS[args.config]
     cfg = c["cfg"]
-    return {"workload": f"{args.config}: L{cfg.n_layers} H{cfg.n_heads} d{cfg.d_model} "
-                        f"V{cfg.vocab} S{cfg.seq_len}, {c['data']}-shaped prompts batch "
-                        f"{c['items']}, PAHQ (E4M3 heads, BF16 MLP, FP32 source/unembed), "
-                        f"KL, ACDC iteration-1 scoring of every edge",
-            "items": c["items"], "parallelism": f"items sharded over {args.gpus} GPU(s)",
+    items = min(args.items, c["items"]) if getattr(args, "items", 0) else c["items"]
+    sampled = n_scored is not None and n_edges_all is not None and n_scored < n_edges_all
+    out = {"workload": f"{args.config}: L{cfg.n_layers} H{cfg.n_heads} d{cfg.d_model} "
+                       f"V{cfg.vocab} S{cfg.seq_len}, {c['data']}-shaped prompts batch "
+                       f"{items}, PAHQ (E4M3 heads, BF16 MLP, FP32 source/unembed), "
+                       f"KL, ACDC iteration-1 scoring of "
+                       + (f"a strided sample of {n_scored} of the {n_edges_all} edges" if sampled
+                          else "every edge"),
+           "items": items, "parallelism": f"items sharded over {args.gpus} GPU(s)",
             "low_precision": "e4m3 (reference-pinned; INT8 per-channel not implemented)",
-            "l2": "inputs >> L2 (activations per step ~GBs)"}
+           "l2": "inputs >> L2 (activations per step ~GBs)"}
+    if sampled:
+        out["edges_sampled"] = {"scored": n_scored, "of": n_edges_all}
+    if items != c["items"]:
+        out["items_note"] = f"{items} of the config's {c['items']} items (one GPU's shard)"
+    return out
 
 
 # ------------------------------------------------------------------------------
@@ -283,6 +298,12 @@ def main(argv=None):
     ap.add_argument("--ncu", action="store_true",
                     help="profiling mode: one untimed scoring step, no JSON line (for ncu "
                          "launch lists; no number from it is a bench value)")
+    ap.add_argument("--items", type=int, default=0,
+                    help="prompt batch (default: the config's; e.g. the per-GPU shard of an "
+                         "8-GPU config on one GPU)")
+    ap.add_argument("--max-edges", type=int, default=0,
+                    help="score an evenly strided sample of at most this many iteration-1 edges "
+                         "(configs 4-5 on one GPU; reported in config.edges_sampled)")
     ap.add_argument("--acdc-quantile", type=float, default=0.99,
                     help="ACDC end-to-end threshold = this quantile of the iteration-1 scores "
                          "(a non-trivial circuit survives); tau=0.01 is timed as well")
@@ -303,6 +324,8 @@ def main(argv=None):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     cfg, w, ds = make_inputs(args.config)
+    if args.items:
+        ds = ds.subset(list(range(min(args.items, len(ds)))))
     items = len(ds)
     lo, hi = shard_mod.item_block(rank, world, items)
     shard = ds.subset(list(range(lo, hi)))
@@ -318,6 +341,9 @@ def main(argv=None):
         e.init_comm(obj[0], rank, world)
     mask = np.ones(e.n_edges, bool)
     edges = eng.sweep_order(cfg, mask)
+    n_edges_all = len(edges)
+    if args.max_edges and len(edges) > args.max_edges:  # strided: every source depth is sampled
+        edges = edges[::-(-len(edges) // args.max_edges)]
     pol = eng.PrecisionPolicy.head_quantized()
     passes_per_step = len(edges) * items
 
@@ -452,8 +478,9 @@ def main(argv=None):
                "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": dev_s / args.steps * 1e3, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "e4m3/bf16/fp32 (exact)",
-               "data": "synthetic (random-init weights per support.hpp, IOI-shaped prompts)",
-               "config": config_block(args), "clocks": clk.summary(),
+               "data": f"synthetic (random-init weights per support.hpp, "
+                       f"{CONFIGS[args.config]['data']}-shaped prompts)",
+               "config": config_block(args, n_edges_all, len(edges)), "clocks": clk.summary(),
                "e2e": {"value": passes_per_step * args.steps / e2e_s, "unit": "passes/s",
                        "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                        "parts": e2e_parts},

@@ -31,7 +31,9 @@ typedef struct {
 } cqg_config;
 
 /* PrecisionPolicy (proj/include/circuitquant/precision_policy.hpp:36-58).
- * Precision: 0=P8 1=P16 2=P32; low_mode: 0=E4m3 1=Rtn4; targets -1 = none. */
+ * Precision: 0=P8 1=P16 2=P32; low_mode: 0=E4m3 1=Rtn4 2=INT8 (extension: per-channel
+ * weights, per-token activations, RTN conventions of numerics.cpp:105-120 with q <= 127;
+ * no reference counterpart, restated in oracle/cq_oracle.c); targets -1 = none. */
 typedef struct {
   int8_t attention_default, mlp_default, embed_precision, unembed_precision, low_mode;
   int32_t target_head_layer, target_head_head, target_mlp;

@@ -110,8 +110,33 @@ int cqo_quantize_rtn(float* x, int64_t n, int bits, double* delta_out) {
   return 0;
 }
 
-/* quantize_span, kernels.cpp:236-251 */
-static void quantize(float* x, int64_t n, int p, int mode) {
+/* INT8 RTN of one strided group — EXTENSION (BASELINE config 2), parity
+ * unpinned: the reference has no INT8 caller. It follows quantize_rtn's
+ * conventions (numerics.cpp:105-120): delta = max|x| / 2^(8-1) in double
+ * (all-zero group: unchanged), q = round_half_even(x / delta), value =
+ * float(delta * q); plus the INT8 range: q is clamped to 127, so the one
+ * value quantize_rtn maps to +128 (a group's positive maximum, cf. the
+ * frozen example test_numerics.cpp:221-229 where -2 -> -128) saturates to
+ * 127 * delta. -128 is representable and kept. NaN passes through. */
+static void rtn8_group(float* x, int64_t n, int64_t stride) {
+  double mx = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double a = fabs((double)x[i * stride]);
+    if (a > mx) mx = a;
+  }
+  if (mx == 0.0) return;
+  double d = mx / 128.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double q = rhe((double)x[i * stride] / d);
+    if (q > 127.0) q = 127.0;
+    x[i * stride] = (float)(d * q);
+  }
+}
+
+/* quantize_span, kernels.cpp:236-251, on a [n / cols][cols] tensor. P8 +
+ * INT8 (extension): one group per row (per token: the last dimension of the
+ * tensor the reference quantizes, i.e. dynamic per-token activation scales). */
+static void quantize(float* x, int64_t n, int64_t cols, int p, int mode) {
   if (p == CQO_P32) return;
   if (p == CQO_P16) {
     for (int64_t i = 0; i < n; ++i) x[i] = cqo_round_bf16(x[i]);
@@ -119,6 +144,8 @@ static void quantize(float* x, int64_t n, int p, int mode) {
   }
   if (mode == CQO_E4M3) {
     for (int64_t i = 0; i < n; ++i) x[i] = cqo_round_f8(x[i]);
+  } else if (mode == CQO_INT8) {
+    for (int64_t r = 0; r < n / cols; ++r) rtn8_group(x + r * cols, cols, 1);
   } else {
     cqo_quantize_rtn(x, n, 4, NULL);
   }
@@ -140,7 +167,7 @@ struct cqo_model {
   float** master;
   int64_t* msize;
   int* mkind;  /* MK_* per matrix */
-  float** img[3]; /* [0]=P8/E4M3, [1]=P16, [2]=P8/Rtn4; NULL until first use */
+  float** img[4]; /* [0]=P8/E4M3, [1]=P16, [2]=P8/Rtn4, [3]=P8/INT8; NULL until first use */
 };
 
 static int mat_index(const cqo_model* m, int mk, int layer) {
@@ -249,7 +276,7 @@ void cqo_model_free(cqo_model* m) {
   if (!m) return;
   for (int i = 0; i < m->n_nodes; ++i) free(m->in_edges[i]);
   for (int i = 0; i < m->n_mats; ++i) free(m->master[i]);
-  for (int q = 0; q < 3; ++q) {
+  for (int q = 0; q < 4; ++q) {
     if (!m->img[q]) continue;
     for (int i = 0; i < m->n_mats; ++i) free(m->img[q][i]);
     free(m->img[q]);
@@ -300,18 +327,39 @@ static void rtn4_matrix(const cqo_model* m, int mk, float* t, int64_t size) {
   cqo_quantize_rtn(t, size, 4, NULL);
 }
 
+/* INT8 per-channel weight image (extension): one group per output channel
+ * of the [in][out] matrix, i.e. per column; W_O per (head, column), its
+ * d_k rows of that head (per-head quantization, as Rtn4's W_O head blocks,
+ * model.cpp:445-469); vectors (LN parameters, never multiplied) as one group. */
+static void int8_matrix(const cqo_model* m, int mk, float* t, int64_t size) {
+  int64_t D = m->D, dk = m->dk;
+  if (mk == MK_LN1G || mk == MK_LN1B || mk == MK_LN2G || mk == MK_LN2B || mk == MK_LNFG ||
+      mk == MK_LNFB) {
+    rtn8_group(t, size, 1);
+    return;
+  }
+  if (mk == MK_WO) {
+    for (int64_t h = 0; h < m->H; ++h)
+      for (int64_t c = 0; c < D; ++c) rtn8_group(t + h * dk * D + c, dk, D);
+    return;
+  }
+  int64_t C = mk == MK_WIN ? 4 * D : (mk == MK_WU ? m->V : D);
+  for (int64_t c = 0; c < C; ++c) rtn8_group(t + c, size / C, C);
+}
+
 /* ImageBank::get (model.cpp:505-519) with eager per-(precision,mode)
  * materialisation (model.cpp:473-491). */
 static const float* image(cqo_model* m, int idx, int p, int mode) {
   if (p == CQO_P32) return m->master[idx];
-  int q = p == CQO_P16 ? 1 : (mode == CQO_E4M3 ? 0 : 2);
+  int q = p == CQO_P16 ? 1 : (mode == CQO_E4M3 ? 0 : mode == CQO_INT8 ? 3 : 2);
   if (!m->img[q]) {
     m->img[q] = calloc((size_t)m->n_mats, sizeof(float*));
     for (int i = 0; i < m->n_mats; ++i) {
       float* t = malloc(sizeof(float) * (size_t)m->msize[i]);
       memcpy(t, m->master[i], sizeof(float) * (size_t)m->msize[i]);
       if (q == 2) rtn4_matrix(m, m->mkind[i], t, m->msize[i]);
-      else quantize(t, m->msize[i], p, CQO_E4M3);
+      else if (q == 3) int8_matrix(m, m->mkind[i], t, m->msize[i]);
+      else quantize(t, m->msize[i], m->msize[i], p, CQO_E4M3);
       m->img[q][i] = t;
     }
   }
@@ -495,7 +543,7 @@ int cqo_forward(const cqo_model* mc, const int* tok, const uint8_t* mask, const 
       float* out = outs + node_off(m, vi);
       for (int64_t i = 0; i < S; ++i)
         for (int64_t j = 0; j < D; ++j) out[i * D + j] = we[(int64_t)tok[i] * D + j] + wp[i * D + j];
-      quantize(out, S * D, p, mode);
+      quantize(out, S * D, D, p, mode);
       ++vi;
       continue;
     }
@@ -509,7 +557,7 @@ int cqo_forward(const cqo_model* mc, const int* tok, const uint8_t* mask, const 
         sum_inputs(m, mask, outs, patch_edge, patch_value, first + h, in);
         layer_norm(in, S, D, g1, b1, xln + h * S * D);
         memcpy(xq + h * S * D, xln + h * S * D, sizeof(float) * (size_t)(S * D));
-        quantize(xq + h * S * D, S * D, p_low, mode);
+        quantize(xq + h * S * D, S * D, D, p_low, mode);
       }
       const float* wimg[3];
       for (int c = 0; c < 3; ++c) wimg[c] = image(m, mat_index(m, MK_WQ + c, l), p_low, mode);
@@ -517,7 +565,7 @@ int cqo_forward(const cqo_model* mc, const int* tok, const uint8_t* mask, const 
       for (int c = 0; c < 3; ++c) /* low_comp, model.cpp:655-664 */
         for (int h = 0; h < H; ++h) {
           matmul_cols(xq + h * S * D, S, D, wimg[c], D, h * dk, (h + 1) * dk, tmp);
-          quantize(tmp, S * dk, p_low, mode);
+          quantize(tmp, S * dk, dk, p_low, mode);
           for (int64_t i = 0; i < S; ++i)
             memcpy(low + ((c * S + i) * H + h) * dk, tmp + i * dk, sizeof(float) * (size_t)dk);
         }
@@ -534,10 +582,10 @@ int cqo_forward(const cqo_model* mc, const int* tok, const uint8_t* mask, const 
         const float* v = low + (2 * S * H + h) * dk;
         causal_attention(q, k, v, H * dk, S, dk, z);
         int p_h = (h == target) ? CQO_P32 : p_low;
-        quantize(z, S * dk, p_h, mode);
+        quantize(z, S * dk, dk, p_h, mode);
         float* out = outs + node_off(m, first + h);
         matmul_cols(z, S, dk, wo + (int64_t)h * dk * D, D, 0, D, out); /* matmul_rows */
-        quantize(out, S * D, p_h, mode);
+        quantize(out, S * D, D, p_h, mode);
       }
       vi += (int)H;
       continue;
@@ -548,14 +596,14 @@ int cqo_forward(const cqo_model* mc, const int* tok, const uint8_t* mask, const 
       sum_inputs(m, mask, outs, patch_edge, patch_value, vi, in);
       layer_norm(in, S, D, m->master[mat_index(m, MK_LN2G, l)], m->master[mat_index(m, MK_LN2B, l)],
                  xln);
-      quantize(xln, S * D, p, mode);
+      quantize(xln, S * D, D, p, mode);
       matmul_cols(xln, S, D, image(m, mat_index(m, MK_WIN, l), p, mode), 4 * D, 0, 4 * D, hid);
-      quantize(hid, S * 4 * D, p, mode);
+      quantize(hid, S * 4 * D, 4 * D, p, mode);
       gelu(hid, S * 4 * D);
-      quantize(hid, S * 4 * D, p, mode);
+      quantize(hid, S * 4 * D, 4 * D, p, mode);
       float* out = outs + node_off(m, vi);
       matmul_cols(hid, S, 4 * D, image(m, mat_index(m, MK_WOUT, l), p, mode), D, 0, D, out);
-      quantize(out, S * D, p, mode);
+      quantize(out, S * D, D, p, mode);
       ++vi;
       continue;
     }
@@ -564,10 +612,10 @@ int cqo_forward(const cqo_model* mc, const int* tok, const uint8_t* mask, const 
       sum_inputs(m, mask, outs, patch_edge, patch_value, vi, in);
       layer_norm(in, S, D, m->master[mat_index(m, MK_LNFG, 0)], m->master[mat_index(m, MK_LNFB, 0)],
                  xln);
-      quantize(xln, S * D, p, mode);
+      quantize(xln, S * D, D, p, mode);
       float* out = outs + node_off(m, vi);
       matmul_cols(xln, S, D, image(m, mat_index(m, MK_WU, 0), p, mode), V, 0, V, out);
-      quantize(out, S * V, p, mode);
+      quantize(out, S * V, V, p, mode);
       ++vi;
     }
   }

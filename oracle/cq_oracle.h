@@ -20,7 +20,7 @@ extern "C" {
 
 /* Precision (numerics.hpp:19) and LowMode (numerics.hpp:25). */
 enum { CQO_P8 = 0, CQO_P16 = 1, CQO_P32 = 2 };
-enum { CQO_E4M3 = 0, CQO_RTN4 = 1 };
+enum { CQO_E4M3 = 0, CQO_RTN4 = 1, CQO_INT8 = 2 /* extension: INT8 per-channel RTN */ };
 /* NodeKind (precision_policy.hpp:25). */
 enum { CQO_EMBED = 0, CQO_HEAD = 1, CQO_MLP = 2, CQO_UNEMBED = 3 };
 

@@ -20,7 +20,7 @@ REF_SO = os.path.join(HERE, "_ref", "libcqref.so")
 PORT_SO = os.path.join(HERE, "libcqoracle.so")
 
 P8, P16, P32 = 0, 1, 2
-E4M3, RTN4 = 0, 1
+E4M3, RTN4, INT8 = 0, 1, 2  # INT8: extension (per-channel weights, per-token activations)
 KL, LOGITDIFF = 0, 1
 
 

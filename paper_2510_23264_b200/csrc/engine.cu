@@ -147,7 +147,8 @@ Policy Policy::from(const cqg_policy& p) {
   q.tm = p.target_mlp;
   for (int v : {q.att, q.mlp, q.emb, q.unemb})
     if (v < 0 || v > 2) throw Error(1, "policy: precision must be 0 (P8), 1 (P16) or 2 (P32)");
-  if (q.mode < 0 || q.mode > 1) throw Error(1, "policy: low_mode must be 0 (E4m3) or 1 (Rtn4)");
+  if (q.mode < 0 || q.mode > 2)
+    throw Error(1, "policy: low_mode must be 0 (E4m3), 1 (Rtn4) or 2 (INT8, extension)");
   return q;
 }
 
@@ -235,6 +236,8 @@ struct Run {  // one evaluation context (a baseline) over nb items
   int nb = 0;
   size_t seg = 0;  // floats per node activation
   DeviceBuf out, trie, logits, lse, prob;  // prob: [nb][V] exp(lp) of the last rows (KL)
+  DeviceBuf psum;                           // [nb] sum_v exp(lp_v) (fused unembed + KL)
+  DeviceBuf xbp, ebp;                       // logits / exp(lp) zero-padded to 128-column pitch
   std::vector<int8_t> otype;                // OutType of each node's output in `out`
   float* o(int n) const { return out.as<float>() + (size_t)n * seg; }
   float* t(int n) const { return trie.as<float>() + (size_t)n * seg; }
@@ -258,7 +261,7 @@ struct Engine {
   cudaStream_t st = nullptr;
   std::vector<std::unique_ptr<DeviceBuf>> master;
   std::vector<int64_t> msize;
-  std::map<int, std::vector<std::unique_ptr<DeviceBuf>>> img;  // 0 e4m3, 1 bf16, 2 rtn4
+  std::map<int, std::vector<std::unique_ptr<DeviceBuf>>> img;  // 0 e4m3, 1 bf16, 2 rtn4, 3 int8
   // dataset
   int B = 0, item_off = 0, item_total = 0, metric = 0;
   DeviceBuf d_clean, d_corrupt, d_ans, d_dis;
@@ -297,7 +300,8 @@ struct Engine {
   // BF16 fixups: chunked block kernel (1) or the per-tile kernel (0, default:
   // measured faster, DESIGN.md section 7 "tried")
   int64_t opt_fix_blk = 0;
-  int64_t opt_fix_blk_min = 148;  // ... for launches with at least this many row-tile units
+  int64_t opt_fix_blk_min = 148;
+  int64_t opt_kl_fused = 1;  // patched rows: unembed with the KL in its epilogue (no logits)  // ... for launches with at least this many row-tile units
   int64_t opt_fix_cpi = 0;  // store E4M3/BF16-rounded node outputs as their codes
   int64_t opt_mem_budget = 0;
   // 1: the patched passes' FP32 unembed on the tensor cores (6-term BF16
@@ -418,7 +422,7 @@ struct Engine {
   // ---- weights -------------------------------------------------------------
   const float* W(int m, int prec, int mode) {
     if (prec == 2) return master[m]->as<float>();
-    const int key = prec == 1 ? 1 : (mode == 0 ? 0 : 2);
+    const int key = prec == 1 ? 1 : (mode == 0 ? 0 : mode == 1 ? 2 : 3);
     auto& v = img[key];
     if (v.empty()) v.resize(master.size());
     if (!v[m]) {
@@ -444,7 +448,23 @@ struct Engine {
     const float* in = master[m]->as<float>();
     if (key == 0) launch_quantize(in, out, msize[m], 0, st);
     else if (key == 1) launch_quantize(in, out, msize[m], 1, st);
-    else {
+    else if (key == 3) {
+      // INT8 per-channel (extension, oracle/cq_oracle.c int8_matrix): one group
+      // per output column; W_O per (head, column) over the head's d_k rows;
+      // vectors as one group
+      const int w = mat_kind(m);
+      const int64_t D = g.D;
+      if (w == 7) {
+        for (int h = 0; h < g.H; ++h)
+          launch_rtn_groups(in + h * g.dk * D, out + h * g.dk * D, g.D, 1, g.dk, 1, g.D, 8, st, 127);
+      } else if (w == 2 || w == 3 || w == 8 || w == 9 || w == 12 || w == 13) {
+        launch_rtn_groups(in, out, 1, 0, 1, (int)msize[m], (int)msize[m], 8, st, 127);
+      } else {
+        const int C = w == 10 ? 4 * g.D : (w == 14 ? g.V : g.D);
+        const int R = (int)(msize[m] / C);
+        launch_rtn_groups(in, out, C, 1, R, 1, C, 8, st, 127);
+      }
+    } else {
       // quantize_rtn4_matrix (model.cpp:445-469)
       const int w = mat_kind(m);
       if (w == 4 || w == 5 || w == 6)
@@ -502,10 +522,26 @@ struct Engine {
     else launch_gemm_exact(upload(jobs), upload(ts), (int)jobs.size(), total, st);
   }
   // Rtn4 activation groups (one per item), in place
-  static bool rtn4(int prec, const Policy& P) { return prec == 0 && P.mode == 1; }
-  void rtn_act(const std::vector<RtnJob>& jobs, int nb) {
+  // P8 under an RTN low mode: Rtn4 (reference) or INT8 (extension). Both run
+  // the exact SIMT GEMMs on the FP32 grid values, with an RTN pass over every
+  // tensor the reference quantizes (quantize_tensor, kernels.cpp:236-253).
+  static bool rtn4(int prec, const Policy& P) { return prec == 0 && P.mode != 0; }
+  // Jobs describe one item's [S][cols] tensor (group_off = the item stride).
+  // Rtn4: one group per item tensor (the reference's quantize_span of the
+  // whole tensor). INT8: one group per row (per-token scales), 8 bits, q <= 127.
+  void rtn_act(const std::vector<RtnJob>& jobs, int nb, const Policy& P) {
     if (jobs.empty()) return;
     reserve(up_bytes(jobs.size(), sizeof(RtnJob)));
+    if (P.mode == 2) {
+      std::vector<RtnJob> rows(jobs);
+      for (RtnJob& j : rows) {
+        if (j.group_off != (int64_t)j.rows * j.ld) throw Error(2, "internal: INT8 row groups need item-major rows");
+        j.group_off = j.ld, j.rows = 1;
+      }
+      Prof pf(this, "int8_act");
+      launch_rtn_act(upload(rows), (int)rows.size(), nb * g.S, 8, st, 127);
+      return;
+    }
     Prof pf(this, "rtn4_act");
     launch_rtn_act(upload(jobs), (int)jobs.size(), nb, 4, st);
   }
@@ -756,7 +792,7 @@ struct Engine {
     std::vector<RtnJob> rq;
     if (r4)
       for (size_t u = 0; u < nu; ++u) rq.push_back({xq + u * SEG, (int64_t)g.S * D, g.S, D, D, 0});
-    rtn_act(rq, nb);
+    rtn_act(rq, nb, P);
     rq.clear();
 
     // Q/K/V: per unique input a [RB][3D] block (q | k | v, head-major columns)
@@ -819,7 +855,7 @@ struct Engine {
     }
     if (tc) gemm_tc(kTcE4M3, xq8, (int64_t)nu * RB, D, *bq, tj, "qkv", xnorm);
     gemm(gj, "gemm_qkv");
-    rtn_act(rq, nb);
+    rtn_act(rq, nb, P);
     rq.clear();
 
     // attention + z (FP32 for the exact W_O, E4M3 bytes for the tensor cores)
@@ -850,7 +886,7 @@ struct Engine {
       aj.push_back(a);
     }
     attn(aj, nb);
-    rtn_act(rq, nb);
+    rtn_act(rq, nb, P);
     rq.clear();
     gj.clear();
     tj.clear();
@@ -881,7 +917,7 @@ struct Engine {
         if (r4 && !target) rq.push_back({o.C, (int64_t)g.S * D, g.S, D, D, 0});
       }
       gemm(gj, "gemm_wo");
-      rtn_act(rq, nb);
+      rtn_act(rq, nb, P);
     }
   }
 
@@ -954,7 +990,7 @@ struct Engine {
       r2.push_back({hid + j * SEG * 4, S * 4 * D, g.S, 4 * D, 4 * D, 1});
       r3.push_back({jobs[j].out, S * D, g.S, D, D, 0});
     }
-    rtn_act(r0, nb);
+    rtn_act(r0, nb, P);
     const float* win = W(g.mat(10, l), p, P.mode);
     const float* wout = W(g.mat(11, l), p, P.mode);
     std::vector<GemmJob> g1, g2;
@@ -970,10 +1006,10 @@ struct Engine {
       g2.push_back(b);
     }
     gemm(g1, "gemm_mlp_in");
-    rtn_act(r1, nb);  // round -> GELU -> round (model.cpp:727-731)
-    rtn_act(r2, nb);
+    rtn_act(r1, nb, P);  // round -> GELU -> round (model.cpp:727-731)
+    rtn_act(r2, nb, P);
     gemm(g2, "gemm_mlp_out");
-    rtn_act(r3, nb);
+    rtn_act(r3, nb, P);
   }
 
   // unembed (model.cpp:741-753): all_rows=false computes only row S-1 of
@@ -987,12 +1023,12 @@ struct Engine {
         float* xq = scratch("u_xq", (size_t)nb * g.S * D);
         float* lg = all_rows ? jb.out : scratch("u_lg", (size_t)nb * g.S * V);
         ln({{jb.in, nullptr, xq, nb * g.S, D}}, g.mat(12, 0), g.mat(13, 0), 2);
-        rtn_act({{xq, (int64_t)g.S * D, g.S, D, D, 0}}, nb);
+        rtn_act({{xq, (int64_t)g.S * D, g.S, D, D, 0}}, nb, P);
         GemmJob a{};
         a.A = xq, a.B = W(g.mat(14, 0), p, P.mode), a.C = lg;
         a.M = nb * g.S, a.N = V, a.K = D, a.lda = D, a.ldb = V, a.ldc = V, a.prec = 2;
         gemm({a}, "gemm_unembed");
-        rtn_act({{lg, (int64_t)g.S * V, g.S, V, V, 0}}, nb);
+        rtn_act({{lg, (int64_t)g.S * V, g.S, V, V, 0}}, nb, P);
         if (!all_rows)
           CK(cudaMemcpy2DAsync(jb.out, (size_t)V * 4, lg + (size_t)(g.S - 1) * V, (size_t)g.S * V * 4,
                                (size_t)V * 4, nb, cudaMemcpyDeviceToDevice, st));
@@ -1044,6 +1080,43 @@ struct Engine {
   };
   std::map<const float*, std::unique_ptr<Wu6>> wu6;
   DeviceBuf ucnt;  // [0] rows flagged by the current launch, [1] running total of the call
+  // K7 + K8 fused (gemm_unembed_kl_kernel): the patched rows' exact unembed
+  // writes per-tile KL partials instead of logits; kl_reduce forms the KL.
+  bool kl_fused_ok(const Policy& P, bool loss) const {
+    return opt_kl_fused && loss && metric == 0 && !unembed_tc_ok(P) && !rtn4(P.unemb, P);
+  }
+  const double2* run_unembed_kl(const Policy& P, const Run& R, const std::vector<SegIO>& jobs, int nb) {
+    const int D = g.D, V = g.V;
+    const size_t rows = jobs.size() * (size_t)nb;
+    float* xq = scratch("u_xq", rows * D);
+    std::vector<LnJob> lj;
+    for (size_t j = 0; j < jobs.size(); ++j)
+      lj.push_back({jobs[j].in + (size_t)(g.S - 1) * D, nullptr, xq + j * (size_t)nb * D, nb, g.S * D});
+    ln(lj, g.mat(12, 0), g.mat(13, 0), P.unemb);
+    const int ldu = (V + 3) & ~3;
+    const float* wu = wu_padded(W(g.mat(14, 0), P.unemb, P.mode), ldu);
+    const int n_ct = unembed_kl_col_tiles(V);
+    double2* part = reinterpret_cast<double2*>(scratch("u_klpart", rows * n_ct * 4));
+    GemmJob a{};
+    a.A = xq, a.B = wu, a.C = nullptr;
+    a.M = (int)rows, a.N = V, a.K = D, a.lda = D, a.ldb = ldu, a.ldc = V, a.prec = P.unemb;
+    if (!R.xbp.p) throw Error(2, "internal: fused KL without padded baselines");
+    KlFuse kf{R.xbp.as<float>(), R.ebp.as<double>(), part, nb, n_ct, n_ct * 128};
+    Prof pf(this, "gemm_unembed", 2.0 * (double)rows * V * D, 0);
+    launch_gemm_unembed_kl(a, kf, st);
+    return part;
+  }
+  const float* wu_padded(const float* wu0, int ldu) {
+    auto& pad = wu_pad[wu0];
+    if (!pad) {
+      pad = std::make_unique<DeviceBuf>();
+      pad->ensure((size_t)g.D * ldu * 4);
+      CK(cudaMemsetAsync(pad->p, 0, (size_t)g.D * ldu * 4, st));
+      CK(cudaMemcpy2DAsync(pad->p, (size_t)ldu * 4, wu0, (size_t)g.V * 4, (size_t)g.V * 4, g.D,
+                           cudaMemcpyDeviceToDevice, st));
+    }
+    return pad->as<float>();
+  }
   bool unembed_tc_ok(const Policy& P) const {
     return opt_unembed_tc && !opt_exact && metric == 0 && P.unemb == 2 && P.mode == 0 &&
            (12 * g.D) % 32 == 0;
@@ -1113,7 +1186,7 @@ struct Engine {
     launch_embed(d_tok, W(g.mat(0, 0), P.emb, P.mode), W(g.mat(1, 0), P.emb, P.mode), out, nb, g.S,
                  g.D, r4 ? 2 : P.emb, st);
     launched();
-    if (r4) rtn_act({{out, (int64_t)g.S * g.D, g.S, g.D, g.D, 0}}, nb);
+    if (r4) rtn_act({{out, (int64_t)g.S * g.D, g.S, g.D, g.D, 0}}, nb, P);
   }
 
   // ---- a full (or suffix) forward over a trie: the baseline runs ----------
@@ -1168,9 +1241,19 @@ struct Engine {
         run_unembed(P, {{input_of(T, R, g.unembed), R.logits.as<float>()}}, R.nb, all_rows);
         if (!all_rows) {
           const bool kl = metric == 0;
-          if (kl) R.prob.ensure((size_t)R.nb * g.V * 8);
+          if (kl) R.prob.ensure((size_t)R.nb * g.V * 8), R.psum.ensure((size_t)R.nb * 8);
           launch_lse(R.logits.as<float>(), R.nb, g.V, R.lse.as<double>(), d_nan, st,
-                     kl ? R.prob.as<double>() : nullptr);
+                     kl ? R.prob.as<double>() : nullptr, kl ? R.psum.as<double>() : nullptr);
+          if (kl && opt_kl_fused) {  // the fused KL's 16-byte-aligned baseline rows
+            const int ld = unembed_kl_col_tiles(g.V) * 128;
+            R.xbp.ensure((size_t)R.nb * ld * 4), R.ebp.ensure((size_t)R.nb * ld * 8);
+            CK(cudaMemsetAsync(R.xbp.p, 0, (size_t)R.nb * ld * 4, st));
+            CK(cudaMemsetAsync(R.ebp.p, 0, (size_t)R.nb * ld * 8, st));
+            CK(cudaMemcpy2DAsync(R.xbp.p, (size_t)ld * 4, R.logits.p, (size_t)g.V * 4, (size_t)g.V * 4, R.nb,
+                                 cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpy2DAsync(R.ebp.p, (size_t)ld * 8, R.prob.p, (size_t)g.V * 8, (size_t)g.V * 8, R.nb,
+                                 cudaMemcpyDeviceToDevice, st));
+          }
           launched();
         }
       }
@@ -1363,6 +1446,7 @@ struct Engine {
     for (auto& p : plans) smin = std::min(smin, p.sv), smax = std::max(smax, p.sv);
     const int last = loss ? g.n_stages - 1 : smax;
     float* logits = nullptr;
+    const double2* klpart = nullptr;  // fused unembed + KL: per-tile partials (no logits)
     UnembedTc utc;  // utc.rows > 0: the logits came from the tensor cores
     std::vector<int> unembed_edges;  // plan indices whose logits were computed
     for (int s = smin; s <= last; ++s) {
@@ -1391,13 +1475,17 @@ struct Engine {
       else if (k == kUnembed && !mj.empty()) {
         const bool all_rows = !loss;
         const size_t rows = all_rows ? (size_t)nb * g.S : (size_t)nb;
-        logits = scratch("p_logits", mj.size() * rows * V);
-        for (size_t j = 0; j < mj.size(); ++j) mj[j].out = logits + j * rows * V;
-        if (loss && unembed_tc_ok(P)) {
-          utc = run_unembed_tc(P, mj, nb);
-          stats.unembed_rows += utc.rows;
+        if (kl_fused_ok(P, loss)) {
+          klpart = run_unembed_kl(P, R, mj, nb);
         } else {
-          run_unembed(P, mj, nb, all_rows);
+          logits = scratch("p_logits", mj.size() * rows * V);
+          for (size_t j = 0; j < mj.size(); ++j) mj[j].out = logits + j * rows * V;
+          if (loss && unembed_tc_ok(P)) {
+            utc = run_unembed_tc(P, mj, nb);
+            stats.unembed_rows += utc.rows;
+          } else {
+            run_unembed(P, mj, nb, all_rows);
+          }
         }
         unembed_edges = uj;
       }
@@ -1475,7 +1563,11 @@ struct Engine {
         reserve(up_bytes(item_of.size(), sizeof(int)));
         {
           std::unique_ptr<Prof> pf(new Prof(this, metric == 0 ? "kl" : "logitdiff", 0, (double)rows * V * 4.0 * 2.0));
-          if (metric == 0 && utc.rows > 0) {
+          if (klpart) {
+            pf.reset();
+            Prof pf2(this, "kl_reduce", 0, (double)rows * unembed_kl_col_tiles(V) * 16.0);
+            launch_kl_reduce(klpart, rows, unembed_kl_col_tiles(V), R.psum.as<double>(), nb, tmp, d_nan, st);
+          } else if (metric == 0 && utc.rows > 0) {
             if (utc.rows != rows) throw Error(2, "internal: tensor-core unembed row count");
             int* cnt = ucnt.as<int>();
             int* list = reinterpret_cast<int*>(scratch("u_list", (size_t)rows));
@@ -1523,8 +1615,10 @@ struct Engine {
     const size_t SEG = segf(nb);
     // arena + per-edge scratch of the widest step (heads: xq + qkv + z; mlp: xq + hid; logits:
     // the last row only under loss metrics, patching.cpp:155-157)
-    size_t scratch_b = std::max({SEG + (size_t)g.H * 4 * nb * g.S * g.dk, 5 * SEG,
-                                 (size_t)nb * (loss ? 1 : g.S) * g.V});
+    // (fused unembed + KL: per-tile partials, 4 floats per 128 columns)
+    const bool fused = loss && opt_kl_fused && metric == 0 && !opt_unembed_tc;
+    const size_t lg = fused ? (size_t)nb * unembed_kl_col_tiles(g.V) * 4 : (size_t)nb * (loss ? 1 : g.S) * g.V;
+    size_t scratch_b = std::max({SEG + (size_t)g.H * 4 * nb * g.S * g.dk, 5 * SEG, lg});
     return ((size_t)(1 + p.n_slots) * SEG + scratch_b) * 4;
   }
 
@@ -2110,7 +2204,7 @@ int cqg_quantize_matrix(cqg_ctx* ctx, int matrix_index, int precision, int low_m
     if (!ctx) throw Error(1, "null context");
     auto& E = *ctx->e;
     if (matrix_index < 0 || matrix_index >= E.g.n_mats()) throw Error(1, "cqg_quantize_matrix: bad matrix index");
-    if (precision < 0 || precision > 2 || low_mode < 0 || low_mode > 1)
+    if (precision < 0 || precision > 2 || low_mode < 0 || low_mode > 2)
       throw Error(1, "cqg_quantize_matrix: bad precision/mode");
     CK(cudaSetDevice(E.device));
     const float* d = E.W(matrix_index, precision, low_mode);
@@ -2187,6 +2281,7 @@ int cqg_set_option(cqg_ctx* ctx, const char* key, int64_t value) {
     else if (k == "profile") ctx->e->opt_profile = value;
     else if (k == "fix_blk") ctx->e->opt_fix_blk = value;
     else if (k == "fix_blk_min") ctx->e->opt_fix_blk_min = value;
+    else if (k == "kl_fused") ctx->e->opt_kl_fused = value;
     else if (k == "mem_budget") ctx->e->opt_mem_budget = value;
     else if (k == "unembed_tc") ctx->e->opt_unembed_tc = value;
     else if (k == "unembed_tol_e9") {

@@ -807,9 +807,34 @@ __global__ void __launch_bounds__(256) gemm_exact_big_kernel(const GemmJob* __re
 
 // One 128 x 128 tile. MAP: logical row m of A and C is physical row
 // rowmap[m] (the exact recomputation of a device-built list of rows).
-template <bool MAP>
+// expm1 in double: Taylor polynomials for |d| < 2^-10 (degree 6) and
+// |d| < 2^-7 (degree 9), truncation < 2^-70 |d|; libdevice expm1 otherwise
+__device__ __forceinline__ double expm1_small(double d) {
+  if (fabs(d) < 0.0009765625) {  // |d| < 2^-10: degree 6 (truncation < 2^-72 |d|)
+    double p = fma(d, 1.0 / 720.0, 1.0 / 120.0);
+    p = fma(p, d, 1.0 / 24.0);
+    p = fma(p, d, 1.0 / 6.0);
+    p = fma(p, d, 0.5);
+    p = fma(p, d, 1.0);
+    return p * d;
+  }
+  if (fabs(d) < 0.0078125) {
+    double p = fma(d, 1.0 / 362880.0, 1.0 / 40320.0);
+    p = fma(p, d, 1.0 / 5040.0);
+    p = fma(p, d, 1.0 / 720.0);
+    p = fma(p, d, 1.0 / 120.0);
+    p = fma(p, d, 1.0 / 24.0);
+    p = fma(p, d, 1.0 / 6.0);
+    p = fma(p, d, 0.5);
+    p = fma(p, d, 1.0);
+    return p * d;
+  }
+  return expm1(d);
+}
+
+template <bool MAP, bool FUSE = false>
 __device__ __forceinline__ void x2_tile(const GemmJob& jb, int m0, int n0, const int* __restrict__ rowmap,
-                                        float negz) {
+                                        float negz, const KlFuse* kf = nullptr) {
   __shared__ __align__(16) float As[2][kXBK][kXBM];  // used as the FFMA2 scalar-broadcast operand
   __shared__ __align__(16) float Bs[2][kXBK][kXBN];
   const int tid = threadIdx.x;
@@ -892,6 +917,50 @@ __device__ __forceinline__ void x2_tile(const GemmJob& jb, int m0, int n0, const
       buf ^= 1;
     }
   }
+  if (FUSE) {
+    // KL partials of this tile's 128 vocabulary columns per row (see
+    // gemm_unembed_kl_kernel): T = sum e_v expm1(d_v), S = sum e_v d_v with
+    // d_v = x_v - xb_v (exact in double), e_v = exp(lp_v) of the baseline.
+    // A NaN logit makes both NaN (the reduce kernel raises the flag).
+    // baselines are zero-padded to a multiple of 128 columns (kf->ld): the
+    // padded columns have e = 0 and x = 0 (zero B columns), adding nothing
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int gm = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+      double T = 0.0, S = 0.0;
+      if (gm < jb.M) {
+        const int it = gm % kf->nb;
+        const float* xb = kf->xb + (int64_t)it * kf->ld + n0 + tx * 4;
+        const double* eb = kf->eb + (int64_t)it * kf->ld + n0 + tx * 4;
+        const float4 xa = __ldg(reinterpret_cast<const float4*>(xb));
+        const float4 xc = __ldg(reinterpret_cast<const float4*>(xb + 64));
+        const double2 e0 = __ldg(reinterpret_cast<const double2*>(eb));
+        const double2 e1 = __ldg(reinterpret_cast<const double2*>(eb + 2));
+        const double2 e2 = __ldg(reinterpret_cast<const double2*>(eb + 64));
+        const double2 e3 = __ldg(reinterpret_cast<const double2*>(eb + 66));
+        const float xbv[8] = {xa.x, xa.y, xa.z, xa.w, xc.x, xc.y, xc.z, xc.w};
+        const double ebv[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
+        double t2[2] = {0.0, 0.0}, s2[2] = {0.0, 0.0};  // two independent chains
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const f2_t pr = acc[i][j >> 1];
+          const float x = round_p((j & 1) ? f2_hi(pr) : f2_lo(pr), jb.prec);
+          const double d = (double)x - (double)xbv[j];
+          s2[j & 1] = fma(ebv[j], d, s2[j & 1]);
+          t2[j & 1] = fma(ebv[j], expm1_small(d), t2[j & 1]);
+        }
+        T = t2[0] + t2[1], S = s2[0] + s2[1];
+      }
+      // the 16 threads of a row are one half-warp (tid = ty * 16 + tx)
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        T += __shfl_xor_sync(0xffffffffu, T, o);
+        S += __shfl_xor_sync(0xffffffffu, S, o);
+      }
+      if (tx == 0 && gm < jb.M) kf->part[(int64_t)gm * kf->n_ct + n0 / kXBN] = make_double2(T, S);
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int gm = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
@@ -923,6 +992,65 @@ __global__ void __launch_bounds__(256, 2) gemm_exact_x2_kernel(const GemmJob* __
   const int local = t - tile_start[lo];
   const int tiles_m = (jb.M + kXBM - 1) / kXBM;
   x2_tile<false>(jb, (local % tiles_m) * kXBM, (local / tiles_m) * kXBN, nullptr, negz);
+}
+
+// ---- K7 + K8 fused: the patched rows' exact unembed with the KL in its
+// epilogue (logits are never stored). The reference's per-row
+//   KL = sum_v e_v (lp_v - lq_v),  lp_v = xb_v - lse_b,  lq_v = x_v - lse_q
+// (patching.cpp:127-161) equals, with d_v = x_v - xb_v and E = sum_v e_v,
+//   KL = E (lse_q - lse_b) - sum_v e_v d_v,
+//   lse_q - lse_b = log sum_v e_v exp(d_v) = log1p((E - 1) + sum_v e_v expm1(d_v)),
+// an identity of the same real numbers. Each 128 x 128 tile writes its
+// per-row (T, S) partials; kl_reduce_kernel sums a row's partials and forms
+// the KL. Every term is O(|d|) and the final subtraction is of two O(|d|)
+// numbers, so the result is accurate to ~1e-16 |d| absolute, below the
+// reference's own rounding of lse_q (one ulp of ~log V, i.e. ~2^-49).
+__global__ void __launch_bounds__(256, 2) gemm_unembed_kl_kernel(GemmJob jb, KlFuse kf, float negz) {
+  const int tiles_m = (jb.M + kXBM - 1) / kXBM;
+  const int t = blockIdx.x;
+  x2_tile<false, true>(jb, (t % tiles_m) * kXBM, (t / tiles_m) * kXBN, nullptr, negz, &kf);
+}
+
+void launch_gemm_unembed_kl(const GemmJob& jb, const KlFuse& kf, cudaStream_t st) {
+  if (jb.M <= 0) return;
+  const int tiles = ((jb.M + kXBM - 1) / kXBM) * ((jb.N + kXBN - 1) / kXBN);
+  gemm_unembed_kl_kernel<<<tiles, 256, 0, st>>>(jb, kf, -0.0f);
+}
+
+int unembed_kl_col_tiles(int V) { return (V + kXBN - 1) / kXBN; }
+
+// one warp per row: sum the row's tile partials, then the KL (above)
+__global__ void kl_reduce_kernel(const double2* __restrict__ part, int rows, int n_ct,
+                                 const double* __restrict__ esum, int nb, double* out, int* nan_flag) {
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  double T = 0.0, S = 0.0;
+  for (int c = lane; c < n_ct; c += 32) {
+    const double2 p = part[(int64_t)r * n_ct + c];
+    T += p.x, S += p.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T += __shfl_xor_sync(0xffffffffu, T, o);
+    S += __shfl_xor_sync(0xffffffffu, S, o);
+  }
+  if (lane == 0) {
+    if (T != T || S != S) {  // NaN logits: the score is rejected by the host (patching.cpp:120-123)
+      atomicOr(nan_flag, 1);
+      out[r] = 0.0;
+      return;
+    }
+    // every d_v = 0: the patched logits are the baseline's bit for bit, so
+    // lse_q == lse_b and the reference's KL is exactly 0 (test_patching.cpp:115-130)
+    const double E = esum[r % nb];
+    out[r] = (T == 0.0 && S == 0.0) ? 0.0 : E * log1p((E - 1.0) + T) - S;
+  }
+}
+
+void launch_kl_reduce(const double2* part, int rows, int n_ct, const double* esum, int nb, double* out,
+                      int* nan_flag, cudaStream_t st) {
+  if (rows > 0) kl_reduce_kernel<<<(rows + 7) / 8, 256, 0, st>>>(part, rows, n_ct, esum, nb, out, nan_flag);
 }
 
 // The exact (reference-order) GEMM over a device-built row list (rows[0 ..
@@ -1336,20 +1464,27 @@ __device__ double row_lse(const float* x, int V, int* nan_flag, double* sh, int*
 }
 
 __global__ void lse_kernel(const float* __restrict__ base, int V, double* lse, int* nan_flag,
-                           double* p_out) {
+                           double* p_out, double* p_sum) {
   __shared__ double sh[32];
   __shared__ int shi[32];
   const float* x = base + (int64_t)blockIdx.x * V;
   const double l = row_lse(x, V, nan_flag, sh, shi);
   if (threadIdx.x == 0) lse[blockIdx.x] = l;
-  if (p_out)  // the baseline distribution exp(lp), reused by every patched row
-    for (int i = threadIdx.x; i < V; i += blockDim.x)
-      p_out[(int64_t)blockIdx.x * V + i] = exp((double)x[i] - l);
+  if (p_out) {  // the baseline distribution exp(lp), reused by every patched row
+    double e = 0.0;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+      const double p = exp((double)x[i] - l);
+      p_out[(int64_t)blockIdx.x * V + i] = p;
+      e += p;
+    }
+    e = block_reduce(e, SumOp(), sh, 0.0);
+    if (p_sum && threadIdx.x == 0) p_sum[blockIdx.x] = e;  // E = sum_v exp(lp_v) (fused KL)
+  }
 }
 
 void launch_lse(const float* base, int rows, int V, double* lse, int* nan_flag, cudaStream_t st,
-                double* p_out) {
-  if (rows > 0) lse_kernel<<<rows, 256, 0, st>>>(base, V, lse, nan_flag, p_out);
+                double* p_out, double* p_sum) {
+  if (rows > 0) lse_kernel<<<rows, 256, 0, st>>>(base, V, lse, nan_flag, p_out, p_sum);
 }
 
 __global__ void kl_kernel(const float* __restrict__ logits, const float* __restrict__ base,
@@ -1696,7 +1831,7 @@ void launch_pack_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st
 }
 
 __global__ void rtn_groups_kernel(const float* __restrict__ in, float* __restrict__ out,
-                                  int64_t group_off, int rows, int cols, int ld, int bits) {
+                                  int64_t group_off, int rows, int cols, int ld, int bits, int qmax) {
   __shared__ double sh[32];
   const int64_t g0 = (int64_t)blockIdx.x * group_off;
   const int64_t n = (int64_t)rows * cols;
@@ -1710,17 +1845,18 @@ __global__ void rtn_groups_kernel(const float* __restrict__ in, float* __restric
   const double delta = (mx == 0.0) ? 0.0 : __ddiv_rn(mx, ldexp(1.0, bits - 1));
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const int64_t off = g0 + (i / cols) * ld + (i % cols);
-    out[off] = rtn_apply(in[off], delta);
+    out[off] = rtn_apply(in[off], delta, qmax);
   }
 }
 
 void launch_rtn_groups(const float* in, float* out, int n_groups, int64_t group_off, int rows,
-                       int cols, int ld, int bits, cudaStream_t st) {
-  if (n_groups > 0)
-    rtn_groups_kernel<<<n_groups, 256, 0, st>>>(in, out, group_off, rows, cols, ld, bits);
+                       int cols, int ld, int bits, cudaStream_t st, int qmax) {
+  for (int g0 = 0; g0 < n_groups; g0 += 65535)
+    rtn_groups_kernel<<<std::min(65535, n_groups - g0), 256, 0, st>>>(
+        in + (int64_t)g0 * group_off, out + (int64_t)g0 * group_off, group_off, rows, cols, ld, bits, qmax);
 }
 
-__global__ void rtn_act_kernel(const RtnJob* __restrict__ jobs, int bits) {
+__global__ void rtn_act_kernel(const RtnJob* __restrict__ jobs, int bits, int qmax) {
   __shared__ double sh[32];
   const RtnJob jb = jobs[blockIdx.y];
   float* base = jb.p + (int64_t)blockIdx.x * jb.group_off;
@@ -1737,14 +1873,14 @@ __global__ void rtn_act_kernel(const RtnJob* __restrict__ jobs, int bits) {
   const double delta = (mx == 0.0) ? 0.0 : __ddiv_rn(mx, ldexp(1.0, bits - 1));
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const int64_t off = (i / jb.cols) * jb.ld + (i % jb.cols);
-    base[off] = rtn_apply(base[off], delta);
+    base[off] = rtn_apply(base[off], delta, qmax);
   }
 }
 
-void launch_rtn_act(const RtnJob* d_jobs, int n_jobs, int n_groups, int bits, cudaStream_t st) {
+void launch_rtn_act(const RtnJob* d_jobs, int n_jobs, int n_groups, int bits, cudaStream_t st, int qmax) {
   for (int y0 = 0; y0 < n_jobs; y0 += 65535)
     if (n_groups > 0)
-      rtn_act_kernel<<<dim3(n_groups, std::min(65535, n_jobs - y0)), 256, 0, st>>>(d_jobs + y0, bits);
+      rtn_act_kernel<<<dim3(n_groups, std::min(65535, n_jobs - y0)), 256, 0, st>>>(d_jobs + y0, bits, qmax);
 }
 
 // ---------------------------------------------------------------------------

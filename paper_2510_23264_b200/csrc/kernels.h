@@ -113,7 +113,22 @@ void launch_kl_rows(const float* logits, const float* base, const double* base_l
 // the exact GEMM of jb over the listed rows of A / C (jb.M ignored)
 void launch_gemm_exact_rows(const GemmJob& jb, const int* rows, const int* count, cudaStream_t st);
 void launch_lse(const float* base, int rows, int V, double* lse, int* nan_flag, cudaStream_t st,
-                double* p_out = nullptr);
+                double* p_out = nullptr, double* p_sum = nullptr);
+// Fused unembed + KL (kernels.cu, gemm_unembed_kl_kernel): per 128-column
+// tile partials (T, S) of the patched rows against the baseline item
+// (row % nb): xb [nb][ld] baseline logits, eb [nb][ld] exp(lp), both
+// zero-padded to ld = V rounded up to 128.
+struct KlFuse {
+  const float* xb;
+  const double* eb;
+  double2* part;  // [rows][n_ct]
+  int nb, n_ct, ld;
+};
+void launch_gemm_unembed_kl(const GemmJob& jb, const KlFuse& kf, cudaStream_t st);
+int unembed_kl_col_tiles(int V);
+// KL per row = E log1p((E - 1) + T) - S from the row's partials (NaN -> flag)
+void launch_kl_reduce(const double2* part, int rows, int n_ct, const double* esum, int nb, double* out,
+                      int* nan_flag, cudaStream_t st);
 void launch_logitdiff(const float* logits, const float* base, const int* item_of,
                       const int* answer, const int* distractor, int rows, int V, double* out,
                       int* nan_flag, cudaStream_t st);
@@ -136,7 +151,7 @@ void launch_pack_bf16(const float* in, uint16_t* out, int64_t n, cudaStream_t st
 // Rtn4 per group: groups are `n_groups` blocks of rows x cols taken with a
 // row stride `ld` starting at base + g*group_off (model.cpp:445-469).
 void launch_rtn_groups(const float* in, float* out, int n_groups, int64_t group_off, int rows,
-                       int cols, int ld, int bits, cudaStream_t st);
+                       int cols, int ld, int bits, cudaStream_t st, int qmax = 0);
 
 // ---- Rtn4 activations (quantize_span P8/Rtn4, kernels.cpp:236-251) ---------
 // In place: each of n_groups groups (one per item) is a rows x cols block
@@ -148,7 +163,8 @@ struct RtnJob {
   int64_t group_off;
   int rows, cols, ld, gelu;
 };
-void launch_rtn_act(const RtnJob* d_jobs, int n_jobs, int n_groups, int bits, cudaStream_t st);
+// qmax: INT8 extension clamp (127), 0 = none
+void launch_rtn_act(const RtnJob* d_jobs, int n_jobs, int n_groups, int bits, cudaStream_t st, int qmax = 0);
 
 // ---- tests: exhaustive scalar checks on the device --------------------------
 void launch_e4m3_all(uint8_t* out, uint32_t lo, uint64_t count, cudaStream_t st);

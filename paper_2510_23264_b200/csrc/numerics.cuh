@@ -69,10 +69,14 @@ __device__ __forceinline__ long long rhe(double q) {
 }
 
 // One element of quantize_rtn with a known delta (numerics.cpp:115-118).
-__device__ __forceinline__ float rtn_apply(float v, double delta) {
+// qmax: the INT8 extension's clamp (127: the +128 endpoint saturates; see
+// oracle/cq_oracle.c rtn8_group); 0 = none.
+__device__ __forceinline__ float rtn_apply(float v, double delta, int qmax = 0) {
   if (delta == 0.0) return v;
   double q = __ddiv_rn((double)v, delta);
-  return (float)__dmul_rn(delta, (double)rhe(q));
+  long long k = rhe(q);
+  if (qmax && k > qmax) k = qmax;
+  return (float)__dmul_rn(delta, (double)k);
 }
 
 // ---------------------------------------------------------------------------

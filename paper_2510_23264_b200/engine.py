@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(HERE, "libcqg.so")
 
 # Precision (numerics.hpp:19), LowMode (numerics.hpp:25), Metric, ScoreMode, Method
 P8, P16, P32 = 0, 1, 2
-E4M3, RTN4 = 0, 1
+E4M3, RTN4, INT8 = 0, 1, 2  # INT8: extension (per-channel weights, per-token activations)
 KL, LOGITDIFF = 0, 1
 LOSS, ACT = 0, 1
 ACDC, RTN8, PAHQ = 0, 1, 2

@@ -21,7 +21,7 @@ import os
 import numpy as np
 import pytest
 
-from oracle.oracle import KL, LOGITDIFF, P8, RTN4, Policy, Port
+from oracle.oracle import INT8, KL, LOGITDIFF, P8, RTN4, Policy, Port
 from paper_2510_23264_b200 import engine as eng
 from paper_2510_23264_b200 import formats
 from helpers import GOLDEN, SMALL, TINY, TOY, bits, make, random_mask
@@ -115,6 +115,20 @@ def test_weight_images_bitexact(ref, cfg, tmp_path):
     e.close()
 
 
+@pytest.mark.parametrize("cfg", [SMALL, TOY])
+def test_int8_images_bitexact(cfg):
+    """INT8 per-channel weight images (extension; the reference has no INT8
+    image) equal the oracle restatement bit for bit, every matrix."""
+    w, _ = make(cfg, 2, 2, 3)
+    p = Port(cfg, w.mats)
+    e = eng.Engine(w)
+    for idx, (name, shape) in enumerate(cfg.matrix_specs()):
+        got = e.quantize_matrix(idx, 0, INT8).ravel()
+        want = p.image(idx, P8, INT8)
+        assert np.array_equal(bits(got), bits(want)), name
+    e.close()
+
+
 # --- forward (model.cpp:556-757), bitwise --------------------------------------
 @pytest.mark.parametrize("cfg", [TINY, SMALL, TOY])
 def test_forward_bitexact(cfg):
@@ -129,6 +143,9 @@ def test_forward_bitexact(cfg):
     # Rtn4 activations (quantize_span P8/Rtn4, kernels.cpp:236-251): one delta per tensor
     pols += [Policy.all_low(RTN4), Policy.make(mode=RTN4, th=(L - 1, 0)),
              Policy.make(att=P8, mlp=P8, mode=RTN4, tm=0 if cfg.has_mlp else None)]
+    # INT8 per-channel (extension, oracle/cq_oracle.c): per-token activation groups
+    pols += [Policy.all_low(INT8), Policy.make(mode=INT8, th=(L - 1, 0)),
+             Policy.make(att=P8, mlp=P8, mode=INT8, tm=0 if cfg.has_mlp else None)]
     SD = cfg.seq_len * cfg.d_model
     rng = np.random.RandomState(0)
     for i, pol in enumerate(pols):
@@ -255,16 +272,19 @@ def test_small_scores_match_oracle(per_edge, metric, mode):
 
 
 @pytest.mark.parametrize("cfg", [SMALL, TOY])
-def test_rtn4_scores_match_oracle(cfg):
+@pytest.mark.parametrize("mode", [RTN4, INT8])
+def test_rtn4_scores_match_oracle(cfg, mode):
     """PAHQ at 4 bits (ablation_policy(4) = head_quantized(P8, Rtn4), eval.cpp:1045)
-    and all-low Rtn4 (every activation tensor quantized with its own delta)."""
+    and all-low Rtn4 (every activation tensor quantized with its own delta);
+    the same for the INT8 extension (per-channel weight images, per-token
+    activation scales; oracle/cq_oracle.c rtn8_group)."""
     w, ds = make(cfg, 6, 3, 8)
     p = Port(cfg, w.mats)
     e = eng.Engine(w)
     for metric in (KL, LOGITDIFF):
         e.set_dataset(ds, metric)
-        for pol, per_edge, seed in ((Policy.head_quantized(mode=RTN4), True, None),
-                                    (Policy.all_low(RTN4), False, 13)):
+        for pol, per_edge, seed in ((Policy.head_quantized(mode=mode), True, None),
+                                    (Policy.all_low(mode), False, 13)):
             mask = np.ones(p.n_edges, bool) if seed is None else random_mask(p.n_edges, seed, 0.6)
             edges = np.nonzero(mask)[0]
             want = p.score_edges(ds, edges, pol, per_edge=per_edge, metric=metric, mask=mask)
@@ -327,7 +347,8 @@ MID = formats.ModelConfig(2, 4, 128, 32, 300, 16, 1, 1)
 
 
 @pytest.mark.parametrize("opts", [{}, {"packed": 0}, {"exact_x2": 0}, {"fix_cpi": 1},
-                                  {"fix_cpi": 2}, {"fix_cpi": 4}, {"exact": 1}])
+                                  {"fix_cpi": 2}, {"fix_cpi": 4}, {"exact": 1},
+                                  {"kl_fused": 0}, {"fix_blk": 1, "fix_blk_min": 1}])
 def test_engine_options_match_oracle(opts):
     w, ds = make(MID, 3, 10, 4)
     p = Port(MID, w.mats)
@@ -423,4 +444,35 @@ def test_faithfulness_and_accuracy_match_reference(preset):
         f, a = float.fromhex(g["faithfulness"]), float.fromhex(g["task_accuracy"])
         assert abs(eng.faithfulness(e, mask) - f) <= RTOL * abs(f) + 1e-12, (name, f)
         assert eng.task_accuracy(e, mask) == a, name
+    e.close()
+
+
+@pytest.mark.parametrize("opts", [{}, {"kl_fused": 0}])
+def test_nan_logits_raise_runtime_error(opts):
+    """NaN logits in a patched pass are a runtime_error (patching.cpp:120-123),
+    code 2, on the fused unembed + KL path and on the stored-logit path. The
+    NaN enters only through the corrupt prompts: W_e's last row (a token only
+    the corrupt prompts use) is NaN, so the clean baseline stays finite and
+    every patch from the embedding carries NaN into the logits."""
+    w, ds = make(MID, 3, 4, 4)
+    V = MID.vocab
+    ds.clean[ds.clean == V - 1] = 0
+    ds.corrupt[:, 2] = V - 1
+    w.mats[0] = w.mats[0].copy()
+    w.mats[0][V - 1, :] = np.nan
+    p = Port(MID, w.mats)
+    edges = np.array([0], np.int32)  # embed -> first head
+    with pytest.raises(RuntimeError):
+        p.score_edges(ds, edges, Policy.head_quantized(), per_edge=True, metric=KL)
+    e = eng.Engine(w, options=opts)
+    e.set_dataset(ds, KL)
+    mask = np.ones(p.n_edges, bool)
+    with pytest.raises(eng.CqgError):  # (return code 2; 1 -> ValueError, 3 -> MemoryError)
+        e.score_edges(mask, edges, eng.PrecisionPolicy.head_quantized(), True, 0)
+    # the context stays usable: the same call on a NaN-free dataset (corrupt
+    # prompts = clean prompts: every score is exactly 0, test_patching.cpp:115-130)
+    ds2 = formats.Dataset(ds.clean.copy(), ds.clean.copy(), ds.answer, ds.distractor)
+    e.set_dataset(ds2, KL)
+    ok = e.score_edges(mask, edges, eng.PrecisionPolicy.head_quantized(), True, 0)
+    assert np.array_equal(ok, np.zeros_like(ok))
     e.close()

@@ -235,3 +235,79 @@ def test_port_targeted_base_per_edge_equals_reference(ref, tmp_path):
             b = m.score_edges(edges, base, pe, 0, mask)
             assert np.array_equal(a, b), (pe, base.target_head_layer, base.target_mlp)
     m.close()
+
+
+# --- INT8 per-channel RTN (extension, BASELINE config 2; parity unpinned) ------
+def _int8_col(col):
+    """quantize_rtn conventions (numerics.cpp:105-120) with N = 8 on one
+    group, plus the INT8 clamp q <= 127 (restated independently here)."""
+    col = np.asarray(col, np.float32)
+    mx = float(np.max(np.abs(col.astype(np.float64)))) if col.size else 0.0
+    if mx == 0.0:
+        return col.copy()
+    d = mx / 128.0
+    # numpy rounds half to even; int64 as round_half_even's return type (a
+    # zero quotient gives +0, numerics.cpp:21-28)
+    q = np.minimum(np.round(col.astype(np.float64) / d).astype(np.int64), 127)
+    return (d * q).astype(np.float32)
+
+
+def test_int8_rtn_conventions():
+    """Frozen values: quantize_rtn's N = 8 example (test_numerics.cpp:221-229:
+    {1, -2, 0.3} -> delta 2/128, 0.3 -> 0.296875, -2 -> -128 delta kept), the
+    +128 endpoint (a positive group maximum saturates to 127 delta) and an
+    all-zero group (unchanged), through the oracle's W_Q image columns."""
+    from oracle.oracle import INT8, P8
+    cfg = formats.ModelConfig(1, 1, 3, 3, 5, 2, 1, 0)
+    w = synth.random_weights(cfg, 1)
+    wq = np.zeros((3, 3), np.float32)
+    wq[:, 0] = [1.0, -2.0, 0.3]
+    wq[:, 1] = [2.0, -1.0, 0.3]
+    w.mats[4] = wq.ravel().copy()
+    p = Port(cfg, w.mats)
+    img = p.image(4, P8, INT8).reshape(3, 3)
+    assert img[:, 0].tolist() == [1.0, -2.0, 0.296875]
+    assert img[:, 1].tolist() == [np.float32(127 / 64), -1.0, 0.296875]
+    assert img[:, 2].tolist() == [0.0, 0.0, 0.0]
+
+
+@pytest.mark.parametrize("cfg", [SMALL, TOY])
+def test_int8_images_per_channel(cfg):
+    """Every INT8 image equals the independent restatement: W_Q/K/V/W_in/
+    W_out/W_u/W_e/W_pos per output column, W_O per (head, column) block of
+    d_k rows, LN vectors as one group."""
+    from oracle.oracle import INT8, P8
+    w, _ = make(cfg, 2, 1, 1)
+    p = Port(cfg, w.mats)
+    D, dk, H, V = cfg.d_model, cfg.d_k, cfg.n_heads, cfg.vocab
+    for idx, (name, shape) in enumerate(cfg.matrix_specs()):
+        m = np.asarray(w.mats[idx], np.float32).reshape(shape)
+        got = p.image(idx, P8, INT8).reshape(shape)
+        if len(shape) == 1:
+            want = _int8_col(m)
+        elif name.endswith("w_o"):
+            want = np.empty_like(m)
+            for h in range(H):
+                for c in range(D):
+                    want[h * dk:(h + 1) * dk, c] = _int8_col(m[h * dk:(h + 1) * dk, c])
+        else:
+            want = np.stack([_int8_col(m[:, c]) for c in range(shape[1])], axis=1)
+        assert np.array_equal(bits(got), bits(want)), name
+
+
+def test_int8_forward_per_token_grids():
+    """Under an INT8 policy every low-precision head output row (one token,
+    D values) is an INT8 grid: at most 256 distinct values, all multiples of
+    one step (per-token dynamic activation scales)."""
+    from oracle.oracle import INT8
+    w, ds = make(SMALL, 3, 2, 4)
+    p = Port(SMALL, w.mats)
+    out = p.forward(ds.clean[0], Policy.make(mode=INT8))
+    S, D = SMALL.seq_len, SMALL.d_model
+    for n in range(1, 1 + SMALL.n_heads):  # layer-0 heads (nodes 1..H)
+        rows = out[n * S * D:(n + 1) * S * D].reshape(S, D).astype(np.float64)
+        for r in rows:
+            mx = np.max(np.abs(r))
+            q = r / (mx / 127.0) if np.any(r == mx) and mx > 0 else r / (mx / 128.0)
+            assert len(np.unique(r)) <= 256
+            assert np.allclose(q, np.round(q), atol=1e-4), (n, q[:4])
