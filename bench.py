@@ -221,6 +221,51 @@ def toy_acdc_pair(eng):
             "same_steps": r.steps == rr.steps}
 
 
+def timed_roc_sweep(eng, e, scores, edges, barrier, max_over_ranks, iter1_s):
+    """BASELINE config 5's 'full ACDC threshold sweep' (roc_sweep,
+    eval.cpp:1193-1226) over threshold_grid(0.001, 3.16, 21) (acdc.cpp:90-102)
+    through cqg_roc_sweep, which scores iteration 1 once and shares it across
+    the 21 thresholds. Ground truth: the 16 top-scored iteration-1 edges (a
+    synthetic model has no planted circuit; the AUC is not the point here,
+    the time is). 21 independent run_acdc calls would each score iteration 1
+    again: at least 21 x the iteration-1 time."""
+    taus = eng.threshold_grid(0.001, 3.16, 21)
+    gt = [int(x) for x in np.asarray(edges)[np.argsort(-np.asarray(scores))[:16]]]
+    c = eng.method_prune_config(eng.PAHQ)
+    barrier()
+    t0 = time.perf_counter()
+    curve = e.roc_sweep(c, taus, gt)
+    barrier()
+    sweep_s = max_over_ranks(time.perf_counter() - t0)
+    return {"seconds": sweep_s, "thresholds": len(taus), "grid": "threshold_grid(0.001, 3.16, 21)",
+            "iteration1_s": iter1_s, "independent_runs_lower_bound_s": 21 * iter1_s,
+            "kept": [p.kept for p in curve.points], "auc_vs_synthetic_gt": curve.auc}
+
+
+def toy_roc_pair(eng):
+    """Config 1: the 21-threshold sweep with iteration 1 shared vs 21
+    independent run_acdc calls, wall seconds each, same kept counts."""
+    cfg, w, ds = make_inputs("toy")
+    e = eng.Engine(w, device=int(os.environ.get("LOCAL_RANK", 0)))
+    e.set_dataset(ds, eng.KL)
+    c = eng.method_prune_config(eng.PAHQ)
+    taus = eng.threshold_grid(0.001, 3.16, 21)
+    gt = list(range(8))
+    e.roc_sweep(c, taus, gt)  # warm-up
+    t0 = time.perf_counter()
+    curve = e.roc_sweep(c, taus, gt)
+    shared_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    kept = []
+    for t in taus:
+        c.tau = float(t)
+        kept.append(int(e.run_acdc(c).final_mask.sum()))
+    indep_s = time.perf_counter() - t0
+    e.close()
+    return {"shared_s": shared_s, "independent_s": indep_s,
+            "same_kept": kept == [p.kept for p in curve.points]}
+
+
 def write_ref_inputs(ref, cfg, ds, wp, dp):
     """weights.bin by the reference's own generator and writer (support.hpp
     random_weights(seed 1) -> save_weights, byte-identical to synth.random_weights,
@@ -460,6 +505,8 @@ def main(argv=None):
         acdc = timed_acdc(tau_q)
         acdc["tau_rule"] = f"quantile {args.acdc_quantile} of the iteration-1 scores"
         acdc["tau_0.01"] = timed_acdc(0.01)
+        acdc["roc_sweep"] = timed_roc_sweep(eng, e, scores, edges, barrier, max_over_ranks,
+                                            dev_s / args.steps)
 
     if rank == 0:
         cb = None
@@ -472,6 +519,7 @@ def main(argv=None):
             if world == 1 and args.acdc:
                 try:
                     toy = toy_acdc_pair(eng)
+                    toy["roc_sweep"] = toy_roc_pair(eng)
                 except Exception as ex:
                     toy = {"unavailable": f"{type(ex).__name__}: {ex}"}
         out = {"metric": METRIC, "value": value, "unit": "passes/s", "n_gpus": world,

@@ -317,7 +317,33 @@ struct Engine {
   ~Engine() {
     if (comm) nccl().CommDestroy(comm);
     if (h_stage) cudaFreeHost(h_stage);
+    if (st_pf) cudaStreamSynchronize(st_pf), cudaStreamDestroy(st_pf);
     if (st) cudaStreamDestroy(st);
+  }
+
+  // ---- the next group's FP32 slices into L2 on the side stream (a6) ---------
+  // HeadBundle (pahq.cpp:21-24, 93-165): the elevated head's W_Q/W_K/W_V
+  // column slices (D rows x d_k) and its layer's W_O; an elevated MLP's
+  // W_in / W_out. The embed's policy is the base: nothing to fetch.
+  cudaStream_t st_pf = nullptr;
+  int64_t opt_prefetch = 0;  // measured slower (a6): off by default
+  void prefetch_source(int src) {
+    if (!opt_prefetch || src < 0 || g.kind[src] == kEmbed || g.kind[src] == kUnembed) return;
+    if (!st_pf) CK(cudaStreamCreateWithFlags(&st_pf, cudaStreamNonBlocking));
+    PfJob j{};
+    const int l = g.layer[src];
+    if (g.kind[src] == kHead) {
+      const int h = g.head[src];
+      if ((g.dk * 4) % 16 == 0 && (g.D * 4) % 16 == 0)
+        for (int c = 0; c < 3; ++c) j.col[c] = master[g.mat(4 + c, l)]->as<float>() + h * g.dk;
+      j.rows = g.D, j.ld = g.D, j.cols = g.dk;
+      j.blk[0] = master[g.mat(7, l)]->p, j.blk_bytes[0] = msize[g.mat(7, l)] * 4;
+    } else {
+      j.blk[0] = master[g.mat(10, l)]->p, j.blk_bytes[0] = msize[g.mat(10, l)] * 4;
+      j.blk[1] = master[g.mat(11, l)]->p, j.blk_bytes[1] = msize[g.mat(11, l)] * 4;
+    }
+    launch_prefetch_l2(j, st_pf);
+    launched();
   }
 
   size_t segf(int nb) const { return (size_t)nb * g.S * g.D; }
@@ -1726,9 +1752,11 @@ struct Engine {
     DeviceBuf& dd = *pool_buf("d_scores", sizeof(double) * (size_t)std::max(n, 1) * B);
     std::vector<int> row_edge;  // row -> index into edge_ids
     row_edge.reserve(n);
-    for (int src : order) {
+    for (size_t oi = 0; oi < order.size(); ++oi) {
+      const int src = order[oi];
       const auto& idx = by_src[src];
       const Policy P = per_edge ? policy_for_edge(g, edge_ids[idx[0]], base) : base;
+      if (per_edge && oi + 1 < order.size()) prefetch_source(order[oi + 1]);
       check_policy(P);
       if (per_edge && !(P == base)) {
         tb = std::chrono::steady_clock::now();
@@ -2282,6 +2310,7 @@ int cqg_set_option(cqg_ctx* ctx, const char* key, int64_t value) {
     else if (k == "fix_blk") ctx->e->opt_fix_blk = value;
     else if (k == "fix_blk_min") ctx->e->opt_fix_blk_min = value;
     else if (k == "kl_fused") ctx->e->opt_kl_fused = value;
+    else if (k == "prefetch") ctx->e->opt_prefetch = value;
     else if (k == "mem_budget") ctx->e->opt_mem_budget = value;
     else if (k == "unembed_tc") ctx->e->opt_unembed_tc = value;
     else if (k == "unembed_tol_e9") {

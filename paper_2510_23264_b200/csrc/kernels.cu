@@ -1019,6 +1019,35 @@ void launch_gemm_unembed_kl(const GemmJob& jb, const KlFuse& kf, cudaStream_t st
 
 int unembed_kl_col_tiles(int V) { return (V + kXBN - 1) / kXBN; }
 
+// ---- HeadBundle prefetch (pahq.cpp:93-165, 211-238), B200 form --------------
+// The FP32 masters are resident in HBM; what the next source group's
+// baseline needs (the elevated head's W_Q/W_K/W_V column slices and its
+// layer's W_O, or the elevated MLP's W_in/W_out) is pulled into L2 on a side
+// stream while the current group runs (cp.async.bulk.prefetch.L2: no
+// registers, no shared memory, no completion to wait for).
+__global__ void prefetch_l2_kernel(const PfJob j) {
+  const int n_rows = j.col[0] ? 3 * j.rows : 0;
+  const int64_t n_blk0 = (int64_t)((j.blk_bytes[0] + 65535) >> 16), n_blk1 = (int64_t)((j.blk_bytes[1] + 65535) >> 16);
+  const int64_t n = n_rows + n_blk0 + n_blk1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const void* p;
+    uint32_t bytes;
+    if (i < n_rows) {  // one row of a column slice (d_k floats)
+      p = j.col[i / j.rows] + (i % j.rows) * (int64_t)j.ld;
+      bytes = (uint32_t)j.cols * 4u;
+    } else {  // a 64 KB piece of a whole matrix
+      const int64_t k = i - n_rows, b = k < n_blk0 ? 0 : 1, o = (b ? k - n_blk0 : k) << 16;
+      p = reinterpret_cast<const uint8_t*>(j.blk[b]) + o;
+      bytes = (uint32_t)min((uint64_t)65536, j.blk_bytes[b] - (uint64_t)o);
+    }
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+  }
+}
+
+void launch_prefetch_l2(const PfJob& j, cudaStream_t st) {
+  prefetch_l2_kernel<<<16, 256, 0, st>>>(j);
+}
+
 // one warp per row: sum the row's tile partials, then the KL (above)
 __global__ void kl_reduce_kernel(const double2* __restrict__ part, int rows, int n_ct,
                                  const double* __restrict__ esum, int nb, double* out, int* nan_flag) {

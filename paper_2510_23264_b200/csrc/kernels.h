@@ -126,6 +126,17 @@ struct KlFuse {
 };
 void launch_gemm_unembed_kl(const GemmJob& jb, const KlFuse& kf, cudaStream_t st);
 int unembed_kl_col_tiles(int V);
+// L2 prefetch (cp.async.bulk.prefetch.L2) of up to three column slices
+// (rows x cols floats at pitch ld floats; null: none) and two whole matrices;
+// addresses 16-byte aligned, sizes multiples of 16. Passed by value: no
+// device-side list, nothing for the host to wait on.
+struct PfJob {
+  const float* col[3];
+  int rows, ld, cols;
+  const void* blk[2];
+  uint64_t blk_bytes[2];
+};
+void launch_prefetch_l2(const PfJob& j, cudaStream_t st);
 // KL per row = E log1p((E - 1) + T) - S from the row's partials (NaN -> flag)
 void launch_kl_reduce(const double2* part, int rows, int n_ct, const double* esum, int nb, double* out,
                       int* nan_flag, cudaStream_t st);

@@ -348,7 +348,8 @@ MID = formats.ModelConfig(2, 4, 128, 32, 300, 16, 1, 1)
 
 @pytest.mark.parametrize("opts", [{}, {"packed": 0}, {"exact_x2": 0}, {"fix_cpi": 1},
                                   {"fix_cpi": 2}, {"fix_cpi": 4}, {"exact": 1},
-                                  {"kl_fused": 0}, {"fix_blk": 1, "fix_blk_min": 1}])
+                                  {"kl_fused": 0}, {"fix_blk": 1, "fix_blk_min": 1},
+                                  {"prefetch": 1}])
 def test_engine_options_match_oracle(opts):
     w, ds = make(MID, 3, 10, 4)
     p = Port(MID, w.mats)
