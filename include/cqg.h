@@ -25,9 +25,17 @@
 extern "C" {
 #endif
 
-/* ModelConfig minus `batch` (proj/include/circuitquant/model.hpp:31-48). */
+/* ModelConfig minus `batch` (proj/include/circuitquant/model.hpp:31-48),
+ * plus qkv_split (EXTENSION, BASELINE config 3's ~32k edges; SPEC.md:166
+ * "finer Q/K/V-input edges are a config flag left off by default"): 0 = the
+ * reference's graph; 1 = each head has three input receivers (q, k, v
+ * inputs, each its own sum and LN), edges numbered for node j asc, then
+ * component q, k, v, then source i < j asc (model.cpp:192-201 with the
+ * receiver in place of the node). Zero-initialise it in callers that predate
+ * the field. */
 typedef struct {
   uint32_t n_layers, n_heads, d_model, d_k, vocab, seq_len, has_mlp;
+  uint32_t qkv_split;
 } cqg_config;
 
 /* PrecisionPolicy (proj/include/circuitquant/precision_policy.hpp:36-58).
@@ -126,6 +134,9 @@ int cqg_circuit_stats(cqg_ctx* ctx, const uint8_t* mask, double* clean_ld, doubl
 /* Graph facts (model.cpp:166-246). */
 int cqg_graph_info(const cqg_config* cfg, int* n_nodes, int* n_edges);
 int cqg_graph_edges(const cqg_config* cfg, int32_t* edge_src, int32_t* edge_dst);
+/* receiver component of each edge: 0/1/2 = q/k/v input of a head under
+ * qkv_split, 0 otherwise */
+int cqg_graph_edge_comp(const cqg_config* cfg, int32_t* edge_comp);
 
 /* Timing/diagnostic counters of the last cqg_score_edges call. */
 typedef struct {

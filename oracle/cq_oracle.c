@@ -163,7 +163,14 @@ struct cqo_model {
   int n_nodes, n_edges, n_mats;
   int *kind, *layer, *head, *stage;
   int *esrc, *edst;
-  int **in_edges, *n_in;
+  /* receivers (EXTENSION: Q/K/V-split edges, BASELINE config 3's ~32k edges;
+   * SPEC.md:166 "finer Q/K/V-input edges are a config flag left off"): a head
+   * has 3 input receivers (q, k, v inputs, each its own sum and LN), other
+   * nodes 1. Unsplit (the reference's graph): every node 1 receiver. */
+  int split, n_recv;
+  int *recv_node, *recv_comp, *node_recv; /* node_recv: first receiver of a node (-1: embed) */
+  int* erecv;                             /* receiver of each edge */
+  int **in_edges, *n_in;                  /* per receiver */
   float** master;
   int64_t* msize;
   int* mkind;  /* MK_* per matrix */
@@ -194,7 +201,12 @@ static int node_stage(const cqo_model* m, int kind, int layer) {
   }
 }
 
+cqo_model* cqo_model_new_split(const uint32_t* c, const float* const* mats, int split);
 cqo_model* cqo_model_new(const uint32_t* c, const float* const* mats) {
+  return cqo_model_new_split(c, mats, 0);
+}
+
+cqo_model* cqo_model_new_split(const uint32_t* c, const float* const* mats, int split) {
   /* ModelConfig::validate, model.cpp:144-155 */
   if (c[0] < 1 || c[1] < 1 || c[2] < 1 || c[3] < 1 || c[1] * c[3] != c[2] || c[4] < 2 ||
       c[5] < 1 || c[6] > 1) {
@@ -223,20 +235,35 @@ cqo_model* cqo_model_new(const uint32_t* c, const float* const* mats) {
   }
   m->kind[k] = CQO_UNEMBED, m->layer[k] = -1, m->head[k] = -1, ++k;
   for (int i = 0; i < m->n_nodes; ++i) m->stage[i] = node_stage(m, m->kind[i], m->layer[i]);
-  /* edges: for j asc, for i < j asc, iff stage(i) < stage(j) (model.cpp:192-201) */
-  int cap = m->n_nodes * m->n_nodes / 2 + 1;
+  /* receivers: node order, then component (q, k, v for split heads) */
+  m->split = split ? 1 : 0;
+  m->node_recv = malloc(sizeof(int) * m->n_nodes);
+  m->recv_node = malloc(sizeof(int) * 3 * m->n_nodes);
+  m->recv_comp = malloc(sizeof(int) * 3 * m->n_nodes);
+  m->n_recv = 0;
+  for (int j = 0; j < m->n_nodes; ++j) {
+    m->node_recv[j] = j == 0 ? -1 : m->n_recv;
+    int nc = j == 0 ? 0 : (m->split && m->kind[j] == CQO_HEAD ? 3 : 1);
+    for (int q = 0; q < nc; ++q) m->recv_node[m->n_recv] = j, m->recv_comp[m->n_recv] = q, ++m->n_recv;
+  }
+  /* edges: for j asc, for i < j asc, iff stage(i) < stage(j) (model.cpp:192-201);
+   * split graph: for receiver r asc (node j asc, component asc), for i < j asc */
+  int cap = 3 * m->n_nodes * m->n_nodes / 2 + 1;
   m->esrc = malloc(sizeof(int) * cap);
   m->edst = malloc(sizeof(int) * cap);
-  m->in_edges = calloc((size_t)m->n_nodes, sizeof(int*));
-  m->n_in = calloc((size_t)m->n_nodes, sizeof(int));
+  m->erecv = malloc(sizeof(int) * cap);
+  m->in_edges = calloc((size_t)m->n_recv, sizeof(int*));
+  m->n_in = calloc((size_t)m->n_recv, sizeof(int));
   int ne = 0;
-  for (int j = 0; j < m->n_nodes; ++j) {
-    m->in_edges[j] = malloc(sizeof(int) * (size_t)(j + 1));
+  for (int r = 0; r < m->n_recv; ++r) {
+    int j = m->recv_node[r];
+    m->in_edges[r] = malloc(sizeof(int) * (size_t)(j + 1));
     for (int i = 0; i < j; ++i) {
       if (m->stage[i] >= m->stage[j]) continue;
       m->esrc[ne] = i;
       m->edst[ne] = j;
-      m->in_edges[j][m->n_in[j]++] = ne;
+      m->erecv[ne] = r;
+      m->in_edges[r][m->n_in[r]++] = ne;
       ++ne;
     }
   }
@@ -274,7 +301,8 @@ cqo_model* cqo_model_new(const uint32_t* c, const float* const* mats) {
 
 void cqo_model_free(cqo_model* m) {
   if (!m) return;
-  for (int i = 0; i < m->n_nodes; ++i) free(m->in_edges[i]);
+  for (int i = 0; i < m->n_recv; ++i) free(m->in_edges[i]);
+  free(m->node_recv), free(m->recv_node), free(m->recv_comp), free(m->erecv);
   for (int i = 0; i < m->n_mats; ++i) free(m->master[i]);
   for (int q = 0; q < 4; ++q) {
     if (!m->img[q]) continue;
@@ -294,10 +322,17 @@ void cqo_graph(const cqo_model* m, int* nk, int* nl, int* nh, int* es, int* ed) 
   for (int e = 0; e < m->n_edges; ++e) es[e] = m->esrc[e], ed[e] = m->edst[e];
 }
 
+/* component of each edge's receiver: 0 / 1 / 2 = q / k / v input of a head
+ * in the split graph, 0 otherwise */
+void cqo_graph_comp(const cqo_model* m, int* comp) {
+  for (int e = 0; e < m->n_edges; ++e) comp[e] = m->recv_comp[m->erecv[e]];
+}
+int cqo_split(const cqo_model* m) { return m->split; }
+
 /* sweep_order, model.cpp:238-246 */
 int cqo_sweep_order(const cqo_model* m, const uint8_t* mask, int* out) {
   int n = 0;
-  for (int j = m->n_nodes - 1; j >= 0; --j)
+  for (int j = m->n_recv - 1; j >= 0; --j) /* receivers desc (= dst desc unsplit) */
     for (int t = m->n_in[j] - 1; t >= 0; --t) {
       int e = m->in_edges[j][t];
       if (!mask || mask[e]) out[n++] = e;
@@ -496,7 +531,8 @@ static int64_t outs_size(const cqo_model* m) {
   return (int64_t)(m->n_nodes - 1) * m->S * m->D + (int64_t)m->S * m->V;
 }
 
-/* sum_inputs, model.cpp:537-552 */
+/* sum_inputs, model.cpp:537-552, for receiver v (= the node's one receiver
+ * unsplit; a head's q / k / v input in the split graph) */
 static void sum_inputs(const cqo_model* m, const uint8_t* mask, const float* outs, int patch_edge,
                        const float* patch_value, int v, float* in) {
   int64_t n = (int64_t)m->S * m->D;
@@ -526,8 +562,9 @@ int cqo_forward(const cqo_model* mc, const int* tok, const uint8_t* mask, const 
     if (mask && !mask[patch_edge]) return fail(1, "forward: patch references masked edge");
   }
   float* in = malloc(sizeof(float) * (size_t)(S * D));
-  float* xln = malloc(sizeof(float) * (size_t)(H * S * D));
-  float* xq = malloc(sizeof(float) * (size_t)(H * S * D));
+  const int NC = m->split ? 3 : 1; /* input receivers per head */
+  float* xln = malloc(sizeof(float) * (size_t)(NC * H * S * D)); /* [c][h] */
+  float* xq = malloc(sizeof(float) * (size_t)(NC * H * S * D));
   float* low = malloc(sizeof(float) * (size_t)(3 * S * H * dk)); /* [3][S][H][dk] */
   float* tmp = malloc(sizeof(float) * (size_t)(S * (4 * D > V ? 4 * D : V)));
   float* z = malloc(sizeof(float) * (size_t)(S * dk));
@@ -553,18 +590,20 @@ int cqo_forward(const cqo_model* mc, const int* tok, const uint8_t* mask, const 
       int target = (pol->target_head_layer == l) ? pol->target_head_head : -1;
       const float* g1 = m->master[mat_index(m, MK_LN1G, l)];
       const float* b1 = m->master[mat_index(m, MK_LN1B, l)];
-      for (int h = 0; h < H; ++h) {
-        sum_inputs(m, mask, outs, patch_edge, patch_value, first + h, in);
-        layer_norm(in, S, D, g1, b1, xln + h * S * D);
-        memcpy(xq + h * S * D, xln + h * S * D, sizeof(float) * (size_t)(S * D));
-        quantize(xq + h * S * D, S * D, D, p_low, mode);
-      }
+      for (int q = 0; q < NC; ++q)
+        for (int h = 0; h < H; ++h) {
+          float* xl = xln + (q * H + h) * S * D;
+          sum_inputs(m, mask, outs, patch_edge, patch_value, m->node_recv[first + h] + q, in);
+          layer_norm(in, S, D, g1, b1, xl);
+          memcpy(xq + (q * H + h) * S * D, xl, sizeof(float) * (size_t)(S * D));
+          quantize(xq + (q * H + h) * S * D, S * D, D, p_low, mode);
+        }
       const float* wimg[3];
       for (int c = 0; c < 3; ++c) wimg[c] = image(m, mat_index(m, MK_WQ + c, l), p_low, mode);
       const float* wo = image(m, mat_index(m, MK_WO, l), wo_precision(pol, l), mode);
-      for (int c = 0; c < 3; ++c) /* low_comp, model.cpp:655-664 */
+      for (int c = 0; c < 3; ++c) /* low_comp, model.cpp:655-664 (split: component c's own input) */
         for (int h = 0; h < H; ++h) {
-          matmul_cols(xq + h * S * D, S, D, wimg[c], D, h * dk, (h + 1) * dk, tmp);
+          matmul_cols(xq + ((m->split ? c : 0) * H + h) * S * D, S, D, wimg[c], D, h * dk, (h + 1) * dk, tmp);
           quantize(tmp, S * dk, dk, p_low, mode);
           for (int64_t i = 0; i < S; ++i)
             memcpy(low + ((c * S + i) * H + h) * dk, tmp + i * dk, sizeof(float) * (size_t)dk);
@@ -572,7 +611,8 @@ int cqo_forward(const cqo_model* mc, const int* tok, const uint8_t* mask, const 
       if (target >= 0) /* high_comp + assemble_comp, model.cpp:665-675, 708-713 */
         for (int c = 0; c < 3; ++c) {
           const float* wm = m->master[mat_index(m, MK_WQ + c, l)];
-          matmul_cols(xln + target * S * D, S, D, wm, D, target * dk, (target + 1) * dk, tmp);
+          matmul_cols(xln + ((m->split ? c : 0) * H + target) * S * D, S, D, wm, D, target * dk,
+                      (target + 1) * dk, tmp);
           for (int64_t i = 0; i < S; ++i)
             memcpy(low + ((c * S + i) * H + target) * dk, tmp + i * dk, sizeof(float) * (size_t)dk);
         }
@@ -593,7 +633,7 @@ int cqo_forward(const cqo_model* mc, const int* tok, const uint8_t* mask, const 
     if (kind == CQO_MLP) { /* model.cpp:720-739 */
       int l = m->layer[vi];
       int p = precision_of(pol, kind, l, -1);
-      sum_inputs(m, mask, outs, patch_edge, patch_value, vi, in);
+      sum_inputs(m, mask, outs, patch_edge, patch_value, m->node_recv[vi], in);
       layer_norm(in, S, D, m->master[mat_index(m, MK_LN2G, l)], m->master[mat_index(m, MK_LN2B, l)],
                  xln);
       quantize(xln, S * D, D, p, mode);
@@ -609,7 +649,7 @@ int cqo_forward(const cqo_model* mc, const int* tok, const uint8_t* mask, const 
     }
     { /* unembed, model.cpp:741-753 */
       int p = precision_of(pol, kind, -1, -1);
-      sum_inputs(m, mask, outs, patch_edge, patch_value, vi, in);
+      sum_inputs(m, mask, outs, patch_edge, patch_value, m->node_recv[vi], in);
       layer_norm(in, S, D, m->master[mat_index(m, MK_LNFG, 0)], m->master[mat_index(m, MK_LNFB, 0)],
                  xln);
       quantize(xln, S * D, D, p, mode);

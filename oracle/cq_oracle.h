@@ -55,6 +55,11 @@ int cqo_quantize_rtn(float* x, int64_t n, int bits, double* delta);
 /* cfg7 = {n_layers, n_heads, d_model, d_k, vocab, seq_len, has_mlp};
  * mats = canonical for_each_matrix order (model.cpp:285-308). Copies. */
 cqo_model* cqo_model_new(const uint32_t* cfg7, const float* const* mats);
+/* split != 0: the Q/K/V-split edge graph (extension; each head has q / k / v
+ * input receivers, edges numbered for receiver asc, then source asc) */
+cqo_model* cqo_model_new_split(const uint32_t* cfg7, const float* const* mats, int split);
+void cqo_graph_comp(const cqo_model* m, int* comp);
+int cqo_split(const cqo_model* m);
 void cqo_model_free(cqo_model* m);
 int cqo_n_nodes(const cqo_model* m);
 int cqo_n_edges(const cqo_model* m);

@@ -300,13 +300,14 @@ class Port:
 
     _lib = None
 
-    def __init__(self, cfg, mats):
+    def __init__(self, cfg, mats, qkv_split=False):
         if Port._lib is None:
             if not os.path.exists(PORT_SO):
                 raise RuntimeError(f"{PORT_SO} missing: run `make -C oracle port`")
             lib = C.CDLL(PORT_SO)
             lib.cqo_last_error.restype = C.c_char_p
             lib.cqo_model_new.restype = C.c_void_p
+            lib.cqo_model_new_split.restype = C.c_void_p
             lib.cqo_model_free.argtypes = [C.c_void_p]
             lib.cqo_encode_f8.restype = C.c_uint8
             lib.cqo_encode_f8.argtypes = [C.c_double]
@@ -324,7 +325,8 @@ class Port:
         ptrs = (C.c_void_p * len(self._mats))(*[m.ctypes.data_as(C.c_void_p) for m in self._mats])
         c7 = np.asarray([cfg.n_layers, cfg.n_heads, cfg.d_model, cfg.d_k, cfg.vocab, cfg.seq_len,
                          cfg.has_mlp], np.uint32)
-        self.h = self.lib.cqo_model_new(c7.ctypes.data_as(C.c_void_p), ptrs)
+        self.qkv_split = bool(qkv_split)
+        self.h = self.lib.cqo_model_new_split(c7.ctypes.data_as(C.c_void_p), ptrs, int(self.qkv_split))
         if not self.h:
             raise ValueError(self.lib.cqo_last_error().decode())
         self.h = C.c_void_p(self.h)
@@ -352,6 +354,13 @@ class Port:
                            h.ctypes.data_as(C.c_void_p), s.ctypes.data_as(C.c_void_p),
                            d.ctypes.data_as(C.c_void_p))
         return k, l, h, s, d
+
+    def edge_comp(self):
+        """Receiver component per edge: 0/1/2 = q/k/v input of a head (split
+        graph), 0 otherwise."""
+        c = np.empty(self.n_edges, np.int32)
+        self.lib.cqo_graph_comp(self.h, c.ctypes.data_as(C.c_void_p))
+        return c
 
     def sweep_order(self, mask=None):
         out = np.empty(self.n_edges, np.int32)

@@ -11,6 +11,7 @@
 #include "gemm_tc.h"
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -106,15 +107,27 @@ Graph::Graph(const cqg_config& c) {
   n_stages = 2 + 2 * L;
   stage_nodes.resize(n_stages);
   for (int i = 0; i < N; ++i) stage_nodes[stage[i]].push_back(i);
-  // edges (model.cpp:192-201)
-  in_edges.resize(N);
-  for (int j = 0; j < N; ++j)
+  // receivers: node order, then component (q, k, v of a split head)
+  if (c.qkv_split > 1) throw Error(1, "ModelConfig: qkv_split must be 0 or 1");
+  split = (int)c.qkv_split;
+  node_recv.assign(N, -1);
+  for (int j = 1; j < N; ++j) {
+    node_recv[j] = (int)recv_node.size();
+    for (int q = 0; q < n_recv(j); ++q) recv_node.push_back(j), recv_comp.push_back(q);
+  }
+  NR = (int)recv_node.size();
+  // edges (model.cpp:192-201): for receiver r asc, for i < node(r) asc
+  in_edges.resize(NR);
+  for (int r = 0; r < NR; ++r) {
+    const int j = recv_node[r];
     for (int i = 0; i < j; ++i) {
       if (stage[i] >= stage[j]) continue;
-      in_edges[j].push_back((int)esrc.size());
+      in_edges[r].push_back((int)esrc.size());
       esrc.push_back(i);
       edst.push_back(j);
+      erecv.push_back(r);
     }
+  }
   E = (int)esrc.size();
 }
 
@@ -133,7 +146,7 @@ int Graph::mat(int which, int l) const {
 std::vector<int> Graph::sweep_order(const std::vector<uint8_t>& mask) const {
   // model.cpp:238-246
   std::vector<int> o;
-  for (int j = N - 1; j >= 0; --j)
+  for (int j = NR - 1; j >= 0; --j)  // receivers desc (= dst desc on the reference's graph)
     for (auto it = in_edges[j].rbegin(); it != in_edges[j].rend(); ++it)
       if (mask[*it]) o.push_back(*it);
   return o;
@@ -184,9 +197,9 @@ Policy policy_for_edge(const Graph& g, int e, const Policy& base) {
 void Trie::build(const Graph& g, const uint8_t* mask) {
   parent.assign(1, -1);
   src.assign(1, -1);
-  rec_in.assign(g.N, 0);
+  rec_in.assign(g.NR, 0);
   std::map<std::pair<int, int>, int> child;
-  for (int w = 1; w < g.N; ++w) {
+  for (int w = 0; w < g.NR; ++w) {
     int cur = 0;
     for (int e : g.in_edges[w]) {
       if (mask && !mask[e]) continue;
@@ -244,10 +257,12 @@ struct Run {  // one evaluation context (a baseline) over nb items
 };
 
 struct HeadIO {
-  const float* in;
+  const float* in;  // the head's input (its q input under qkv_split)
   int head;
   float* out;
   int otype;  // OutType the output is stored as
+  const float* in_k = nullptr, *in_v = nullptr;  // qkv_split: k / v inputs (null: = in)
+  const float* input(int c) const { return c == 1 && in_k ? in_k : (c == 2 && in_v ? in_v : in); }
 };
 struct SegIO {
   const float* in;
@@ -785,20 +800,25 @@ struct Engine {
     // tensor cores for the E4M3 projections of non-target heads
     const bool tc = !opt_exact && p_low == 0 && P.mode == 0 && tc_dims_ok(D, kTcE4M3) &&
                     tc_dims_ok(dk, kTcE4M3);
+    // unique inputs over every (head, component): a split head reads its q,
+    // k and v projections from (possibly) different inputs
     std::map<const float*, int> uidx;
     std::vector<const float*> uin;
-    std::vector<int> u_of(jobs.size()), xln_of;
+    std::vector<std::array<int, 3>> u_of(jobs.size());
+    std::vector<int> xln_of;
     std::vector<char> need_xln;
-    for (size_t j = 0; j < jobs.size(); ++j) {
-      auto it = uidx.find(jobs[j].in);
-      if (it == uidx.end()) {
-        it = uidx.emplace(jobs[j].in, (int)uin.size()).first;
-        uin.push_back(jobs[j].in);
-        need_xln.push_back(0);
+    for (size_t j = 0; j < jobs.size(); ++j)
+      for (int c = 0; c < 3; ++c) {
+        const float* in = jobs[j].input(c);
+        auto it = uidx.find(in);
+        if (it == uidx.end()) {
+          it = uidx.emplace(in, (int)uin.size()).first;
+          uin.push_back(in);
+          need_xln.push_back(0);
+        }
+        u_of[j][c] = it->second;
+        if (P.th_l == l && P.th_h == jobs[j].head) need_xln[it->second] = 1;
       }
-      u_of[j] = it->second;
-      if (P.th_l == l && P.th_h == jobs[j].head) need_xln[it->second] = 1;
-    }
     const size_t nu = uin.size();
     xln_of.assign(nu, -1);
     int n_xln = 0;
@@ -832,14 +852,15 @@ struct Engine {
     std::vector<TcJob> tj;
     const PackedB* bq = tc ? &packedB(0, l, kTcE4M3, p_low, P.mode) : nullptr;
     for (size_t u = 0; u < nu; ++u) {
-      std::vector<int> hs;  // non-target heads reading input u
+      std::vector<std::pair<int, int>> hc;  // (component, non-target head) projections of input u
       for (size_t j = 0; j < jobs.size(); ++j)
-        if (u_of[j] == (int)u && !(P.th_l == l && P.th_h == jobs[j].head)) hs.push_back(jobs[j].head);
-      std::sort(hs.begin(), hs.end());
-      hs.erase(std::unique(hs.begin(), hs.end()), hs.end());
+        for (int c = 0; c < 3; ++c)
+          if (u_of[j][c] == (int)u && !(P.th_l == l && P.th_h == jobs[j].head)) hc.push_back({c, jobs[j].head});
+      std::sort(hc.begin(), hc.end());
+      hc.erase(std::unique(hc.begin(), hc.end()), hc.end());
       float* blk = qkv8 ? nullptr : qkv + u * QKV;
       uint8_t* blk8 = qkv8 ? qkvb + u * QKV : nullptr;
-      if (tc && (int)hs.size() == H) {
+      if (tc && (int)hc.size() == 3 * H) {
         TcJob t{};
         t.a_row0 = (int)u * RB, t.b_row0 = 0, t.b_k0 = 0, t.M = RB, t.N = 3 * D, t.K = D;
         if (qkv8) t.out_pack = blk8;
@@ -848,8 +869,8 @@ struct Engine {
         tj.push_back(t);
         continue;
       }
-      for (int h : hs)
-        for (int c = 0; c < 3; ++c) {
+      for (const auto& ch : hc) {
+          const int c = ch.first, h = ch.second;
           if (tc) {
             TcJob t{};
             t.a_row0 = (int)u * RB, t.b_row0 = c * D + h * dk, t.b_k0 = 0, t.M = RB, t.N = dk, t.K = D;
@@ -873,8 +894,8 @@ struct Engine {
       if (!(P.th_l == l && P.th_h == h)) continue;
       for (int c = 0; c < 3; ++c) {
         GemmJob q{};
-        q.A = xln + xln_of[u_of[j]] * SEG, q.B = master[g.mat(4 + c, l)]->as<float>() + h * dk;
-        q.C = qkv + u_of[j] * QKV + c * D + h * dk;
+        q.A = xln + xln_of[u_of[j][c]] * SEG, q.B = master[g.mat(4 + c, l)]->as<float>() + h * dk;
+        q.C = qkv + u_of[j][c] * QKV + c * D + h * dk;
         q.M = RB, q.N = dk, q.K = D, q.lda = D, q.ldb = D, q.ldc = 3 * D, q.prec = 2;
         gj.push_back(q);
       }
@@ -897,11 +918,13 @@ struct Engine {
       const bool target = P.th_l == l && P.th_h == h;
       AttnJob a{};
       if (qkv8) {
-        const uint8_t* b8 = qkvb + u_of[j] * QKV;
-        a.q8 = b8 + h * dk, a.k8 = b8 + D + h * dk, a.v8 = b8 + 2 * D + h * dk;
+        a.q8 = qkvb + u_of[j][0] * QKV + h * dk;
+        a.k8 = qkvb + u_of[j][1] * QKV + D + h * dk;
+        a.v8 = qkvb + u_of[j][2] * QKV + 2 * D + h * dk;
       } else {
-        float* blk = qkv + u_of[j] * QKV;
-        a.q = blk + h * dk, a.k = blk + D + h * dk, a.v = blk + 2 * D + h * dk;
+        a.q = qkv + u_of[j][0] * QKV + h * dk;
+        a.k = qkv + u_of[j][1] * QKV + D + h * dk;
+        a.v = qkv + u_of[j][2] * QKV + 2 * D + h * dk;
       }
       a.ld = 3 * D;
       a.prec = (target || r4) ? 2 : p_low, a.ldz = dk, a.q0 = last_only ? g.S - 1 : 0;
@@ -1226,8 +1249,15 @@ struct Engine {
     R.otype.assign(g.N, kOutF32);
   }
 
-  const float* input_of(const Trie& T, const Run& R, int w) {
-    return T.rec_in[w] == 0 ? zeros(R.seg) : R.t(T.rec_in[w]);
+  // node w's input (component c of a split head)
+  const float* input_of(const Trie& T, const Run& R, int w, int c = 0) {
+    const int r = T.rec_in[g.recv(w, c)];
+    return r == 0 ? zeros(R.seg) : R.t(r);
+  }
+  HeadIO head_io(const Trie& T, const Run& R, int w, float* out, int otype) {
+    HeadIO h{input_of(T, R, w), g.head[w], out, otype};
+    if (g.split) h.in_k = input_of(T, R, w, 1), h.in_v = input_of(T, R, w, 2);
+    return h;
   }
 
   // loss metrics read only the last position of the logits: the final
@@ -1256,7 +1286,7 @@ struct Engine {
         std::vector<HeadIO> hj;
         for (int w : nodes) {
           R.otype[w] = (int8_t)out_type(P, w);
-          hj.push_back({input_of(T, R, w), g.head[w], R.o(w), R.otype[w]});
+          hj.push_back(head_io(T, R, w, R.o(w), R.otype[w]));
         }
         run_heads(g.layer[nodes[0]], P, hj, R.nb, last_rows(g.layer[nodes[0]], P, loss_only));
       } else if (k == kMlp) {
@@ -1322,7 +1352,7 @@ struct Engine {
     c.buf.ensure(patch_run.seg * 4);
     c.gen = target_gen;
     const float* in = input_of(full, patch_run, s);
-    if (g.kind[s] == kHead) run_heads(g.layer[s], ps, {{in, g.head[s], c.buf.as<float>(), *otype}}, B);
+    if (g.kind[s] == kHead) run_heads(g.layer[s], ps, {head_io(full, patch_run, s, c.buf.as<float>(), *otype)}, B);
     else run_mlp(g.layer[s], ps, {{in, c.buf.as<float>(), *otype}}, B);
     return c.buf.as<float>();
   }
@@ -1330,6 +1360,7 @@ struct Engine {
   // ---- the patched passes of one policy group -------------------------------
   struct EdgePlan {
     int e, s, v, sv;
+    int r;  // destination receiver (= v's only receiver unless v is a split head)
     const float* pv;
     int pvt;  // OutType of pv
     std::vector<int8_t> nchg, tchg, virt;
@@ -1352,8 +1383,11 @@ struct Engine {
     for (int s = P.sv; s <= last; ++s) {
       if (s > P.sv)
         for (int w : g.stage_nodes[s]) {
-          const int ri = T.rec_in[w];
-          P.nchg[w] = (ri != 0 && P.tchg[ri]) ? 1 : 0;
+          P.nchg[w] = 0;
+          for (int c = 0; c < g.n_recv(w); ++c) {  // (a split head: any of q, k, v inputs)
+            const int ri = T.rec_in[g.recv(w, c)];
+            if (ri != 0 && P.tchg[ri]) P.nchg[w] = 1;
+          }
         }
       if (s < last || loss)
         for (int t : T.by_stage[s])
@@ -1371,8 +1405,17 @@ struct Engine {
         ncons[T.parent[t]]++;
         only_child[T.parent[t]] = t;
       }
+    // a changed node's changed inputs are consumed by its kernels (never
+    // virtual); its unchanged inputs (other components of a split head) are
+    // read from the baseline
+    auto changed_inputs = [&](int w, auto&& fn) {
+      for (int c = 0; c < g.n_recv(w); ++c) {
+        const int ri = T.rec_in[g.recv(w, c)];
+        if (ri != 0 && P.tchg[ri]) fn(ri);
+      }
+    };
     for (int w = 0; w < N; ++w)
-      if (P.nchg[w] && g.stage[w] > P.sv && T.rec_in[w] != 0) ncons[T.rec_in[w]] += 2;  // never virtual
+      if (P.nchg[w] && g.stage[w] > P.sv) changed_inputs(w, [&](int ri) { ncons[ri] += 2; });
     // program order per stage -> virtual (register-only) values
     for (int s = P.sv; s <= last && loss; ++s) {
       int prev = -1;
@@ -1394,8 +1437,8 @@ struct Engine {
       if (P.tchg[t] && T.parent[t] != 0 && P.tchg[T.parent[t]])
         lastuse[T.parent[t]] = std::max(lastuse[T.parent[t]], 2 * g.stage[T.src[t]] + 1);
     for (int w = 0; w < N; ++w)
-      if (P.nchg[w] && g.stage[w] > P.sv && T.rec_in[w] != 0)
-        lastuse[T.rec_in[w]] = std::max(lastuse[T.rec_in[w]], 2 * g.stage[w]);
+      if (P.nchg[w] && g.stage[w] > P.sv)
+        changed_inputs(w, [&](int ri) { lastuse[ri] = std::max(lastuse[ri], 2 * g.stage[w]); });
     for (int t = 1; t < TS; ++t) {
       if (!P.tchg[t] || P.virt[t]) continue;
       const int def = 2 * g.stage[T.src[t]] + 1;
@@ -1449,7 +1492,7 @@ struct Engine {
       std::vector<FoldProg> progs;
       for (auto& p : plans) {
         std::vector<int> path;
-        for (int t = T.rec_in[p.v]; t != 0; t = T.parent[t]) path.push_back(t);
+        for (int t = T.rec_in[p.r]; t != 0; t = T.parent[t]) path.push_back(t);
         std::reverse(path.begin(), path.end());
         size_t k = 0;
         while (k < path.size() && T.src[path[k]] != p.s) ++k;
@@ -1487,8 +1530,21 @@ struct Engine {
         if (p.sv > s) continue;
         for (int w : nodes) {
           if (!p.nchg[w]) continue;
-          const float* in = (w == p.v) ? p.sval() : p.slot(p.tslot[T.rec_in[w]], SEG);
-          if (k == kHead) hj.push_back({in, g.head[w], p.slot(p.nslot[w], SEG), out_type(P, w)});
+          // receiver input: the patched sum (the destination receiver), a
+          // recomputed trie value, or the baseline's (unchanged component)
+          auto rin = [&](int c) -> const float* {
+            const int r = g.recv(w, c);
+            if (w == p.v && r == p.r) return p.sval();
+            const int t = T.rec_in[r];
+            if (t != 0 && p.tchg[t]) return p.slot(p.tslot[t], SEG);
+            return t == 0 ? zeros(SEG) : R.t(t);
+          };
+          const float* in = rin(0);
+          if (k == kHead) {
+            HeadIO h{in, g.head[w], p.slot(p.nslot[w], SEG), out_type(P, w)};
+            if (g.split) h.in_k = rin(1), h.in_v = rin(2);
+            hj.push_back(h);
+          }
           else if (k == kMlp) mj.push_back({in, p.slot(p.nslot[w], SEG), out_type(P, w)});
           else if (k == kUnembed) {
             uj.push_back((int)pi);
@@ -1772,6 +1828,7 @@ struct Engine {
       for (size_t k = 0; k < idx.size(); ++k) {
         const int e = edge_ids[idx[k]];
         plans[k].e = e, plans[k].s = g.esrc[e], plans[k].v = g.edst[e], plans[k].sv = g.stage[g.edst[e]];
+        plans[k].r = g.erecv[e];
         plans[k].pv = patch_value(plans[k].s, policy_for_edge(g, e, base), per_edge, &plans[k].pvt);
         plan_edge(plans[k], T, loss);
       }
@@ -1867,7 +1924,8 @@ struct Engine {
   void forward_item(const int* d_tok, const uint8_t* mask, const Policy& P, int patch_edge,
                     const float* d_patch, float* O, float* I, float* LG, const float* absent_src) {
     const size_t SEG = segf(1);
-    auto input = [&](int w) {
+    auto input = [&](int w, int c = 0) {  // node w's input (component c of a split head)
+      w = g.recv(w, c);                    // (I is indexed by receiver)
       std::vector<FoldOp> ops;
       for (int e : g.in_edges[w]) {
         const float* b;
@@ -1894,7 +1952,11 @@ struct Engine {
       if (k == kEmbed) run_embed(P, d_tok, O, 1);
       else if (k == kHead) {
         std::vector<HeadIO> hj;
-        for (int w : nodes) hj.push_back({input(w), g.head[w], O + (size_t)w * SEG, kOutF32});
+        for (int w : nodes) {
+          HeadIO h{input(w), g.head[w], O + (size_t)w * SEG, kOutF32};
+          if (g.split) h.in_k = input(w, 1), h.in_v = input(w, 2);
+          hj.push_back(h);
+        }
         run_heads(g.layer[nodes[0]], P, hj, 1);
       } else if (k == kMlp) run_mlp(g.layer[nodes[0]], P, {{input(nodes[0]), O + (size_t)nodes[0] * SEG, kOutF32}}, 1);
       else run_unembed(P, {{input(g.unembed), LG, kOutF32}}, 1, true);
@@ -1912,7 +1974,7 @@ struct Engine {
     }
     const size_t SEG = segf(1);
     DeviceBuf& outs = *pool_buf("f_outs", (size_t)g.N * SEG * 4);
-    DeviceBuf& ins = *pool_buf("f_ins", (size_t)g.N * SEG * 4);
+    DeviceBuf& ins = *pool_buf("f_ins", (size_t)g.NR * SEG * 4);
     DeviceBuf& lg = *pool_buf("f_logits", (size_t)g.S * g.V * 4);
     DeviceBuf& tk = *pool_buf("f_tok", (size_t)g.S * 4);
     DeviceBuf& pv = *pool_buf("f_patch", SEG * 4);
@@ -1937,7 +1999,7 @@ struct Engine {
     const size_t SEG = segf(1);
     DeviceBuf& oc = *pool_buf("cs_corr", (size_t)g.N * SEG * 4);
     DeviceBuf& o = *pool_buf("f_outs", (size_t)g.N * SEG * 4);
-    DeviceBuf& ins = *pool_buf("f_ins", (size_t)g.N * SEG * 4);
+    DeviceBuf& ins = *pool_buf("f_ins", (size_t)g.NR * SEG * 4);
     DeviceBuf& lg = *pool_buf("f_logits", (size_t)g.S * g.V * 4);
     std::vector<float> row(g.V);
     auto ld = [&](int i) {  // metric_logit_diff of the last row (patching.cpp:140-149)
@@ -2264,6 +2326,14 @@ int cqg_graph_info(const cqg_config* cfg, int* n_nodes, int* n_edges) {
     cqg::Graph g(*cfg);
     *n_nodes = g.N;
     *n_edges = g.E;
+  });
+}
+
+int cqg_graph_edge_comp(const cqg_config* cfg, int32_t* comp) {
+  return guarded([&] {
+    if (!cfg || !comp) throw cqg::Error(1, "cqg_graph_edge_comp: null argument");
+    cqg::Graph g(*cfg);
+    for (int e = 0; e < g.E; ++e) comp[e] = g.recv_comp[g.erecv[e]];
   });
 }
 

@@ -42,8 +42,14 @@ struct Graph {
   int N = 0, E = 0, n_stages = 0, unembed = 0;
   std::vector<int> kind, layer, head, stage;
   std::vector<int> esrc, edst;
-  std::vector<std::vector<int>> in_edges;     // ascending src
+  // receivers: one per node except the embed; a head has 3 (q, k, v inputs)
+  // under qkv_split (extension, cqg.h)
+  int split = 0, NR = 0;
+  std::vector<int> recv_node, recv_comp, node_recv, erecv;
+  std::vector<std::vector<int>> in_edges;     // per receiver, ascending src
   std::vector<std::vector<int>> stage_nodes;  // ascending index
+  int recv(int n, int c) const { return node_recv[n] + (split && kind[n] == kHead ? c : 0); }
+  int n_recv(int n) const { return n == 0 ? 0 : (split && kind[n] == kHead ? 3 : 1); }
   explicit Graph(const cqg_config& c);
   int n_mats() const { return 5 + L * (6 + (mlp ? 4 : 0)); }
   int mat(int which, int l) const;  // which: 0 w_e 1 w_pos 2 ln1g 3 ln1b 4 wq 5 wk 6 wv 7 wo
@@ -66,7 +72,7 @@ Policy policy_for_edge(const Graph& g, int e, const Policy& base);  // pahq.cpp:
 // Trie over receivers' present-source lists (the structure of sum_inputs).
 struct Trie {
   std::vector<int> parent, src;                 // node 0 = root (value 0)
-  std::vector<int> rec_in;                      // per graph node (root if no inputs)
+  std::vector<int> rec_in;                      // per receiver (root if no inputs)
   std::vector<std::vector<int>> by_stage;       // trie nodes per stage(src), parents first
   void build(const Graph& g, const uint8_t* mask);
   int size() const { return (int)parent.size(); }

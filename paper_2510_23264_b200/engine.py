@@ -43,7 +43,7 @@ class CqgPrune(C.Structure):
 class CqgConfig(C.Structure):
     _fields_ = [("n_layers", C.c_uint32), ("n_heads", C.c_uint32), ("d_model", C.c_uint32),
                 ("d_k", C.c_uint32), ("vocab", C.c_uint32), ("seq_len", C.c_uint32),
-                ("has_mlp", C.c_uint32)]
+                ("has_mlp", C.c_uint32), ("qkv_split", C.c_uint32)]
 
 
 class CqgStats(C.Structure):
@@ -260,15 +260,16 @@ def fnv1a64(data: bytes) -> int:
     return int(lib.cqg_fnv1a64(C.cast(buf, C.c_void_p), len(data)))
 
 
-def config_struct(cfg: ModelConfig) -> CqgConfig:
+def config_struct(cfg: ModelConfig, qkv_split: bool = False) -> CqgConfig:
     return CqgConfig(cfg.n_layers, cfg.n_heads, cfg.d_model, cfg.d_k, cfg.vocab, cfg.seq_len,
-                     cfg.has_mlp)
+                     cfg.has_mlp, int(bool(qkv_split)))
 
 
-def graph_edges(cfg: ModelConfig):
-    """Edge list in the reference numbering (model.cpp:192-201)."""
+def graph_edges(cfg: ModelConfig, qkv_split: bool = False):
+    """Edge list in the reference numbering (model.cpp:192-201); qkv_split:
+    the Q/K/V-split graph (extension, include/cqg.h)."""
     lib = load_library()
-    c = config_struct(cfg)
+    c = config_struct(cfg, qkv_split)
     nn, ne = C.c_int(), C.c_int()
     _check(lib.cqg_graph_info(C.byref(c), C.byref(nn), C.byref(ne)))
     src = np.empty(ne.value, np.int32)
@@ -277,31 +278,45 @@ def graph_edges(cfg: ModelConfig):
     return nn.value, src, dst
 
 
-def sweep_order(cfg: ModelConfig, mask: np.ndarray) -> np.ndarray:
-    """model.cpp:238-246 (dst descending, src descending within a dst)."""
-    n_nodes, src, dst = graph_edges(cfg)
+def graph_edge_comp(cfg: ModelConfig, qkv_split: bool = False) -> np.ndarray:
+    """Receiver component of each edge: 0/1/2 = q/k/v input of a split head."""
+    lib = load_library()
+    c = config_struct(cfg, qkv_split)
+    nn, ne = C.c_int(), C.c_int()
+    _check(lib.cqg_graph_info(C.byref(c), C.byref(nn), C.byref(ne)))
+    comp = np.empty(ne.value, np.int32)
+    _check(lib.cqg_graph_edge_comp(C.byref(c), _vp(comp)))
+    return comp
+
+
+def sweep_order(cfg: ModelConfig, mask: np.ndarray, qkv_split: bool = False) -> np.ndarray:
+    """model.cpp:238-246 (dst descending, src descending within a dst; split
+    graph: receiver descending)."""
     idx = np.nonzero(np.asarray(mask, bool))[0]
-    # edges are numbered dst-major ascending, src ascending -> reverse order
+    # edges are numbered receiver-major ascending, src ascending -> reverse order
     return idx[::-1].astype(np.int32)
 
 
 class Engine:
     """One GPU context (cqg_ctx): HBM-resident weights + dataset shard."""
 
-    def __init__(self, weights: WeightSet, device: int = 0, options: Optional[dict] = None):
+    def __init__(self, weights: WeightSet, device: int = 0, options: Optional[dict] = None,
+                 qkv_split: bool = False):
         """options: cqg_set_option knobs applied at creation (after any given
-        in the CQG_OPTS environment variable, "key=value,key=value")."""
+        in the CQG_OPTS environment variable, "key=value,key=value").
+        qkv_split: the Q/K/V-split edge graph (extension, include/cqg.h)."""
         self.lib = load_library()
         self.cfg = weights.cfg
         self.cfg.validate()
         self._mats = [np.ascontiguousarray(m, np.float32) for m in weights.mats]
         ptrs = (C.c_void_p * len(self._mats))(*[m.ctypes.data for m in self._mats])
-        c = config_struct(self.cfg)
+        self.qkv_split = bool(qkv_split)
+        c = config_struct(self.cfg, self.qkv_split)
         h = C.c_void_p()
         _check(self.lib.cqg_create(C.byref(c), C.cast(ptrs, C.c_void_p), device, C.byref(h)))
         self.h = h
         self._mats = None  # copied into HBM
-        self.n_nodes, self.edge_src, self.edge_dst = graph_edges(self.cfg)
+        self.n_nodes, self.edge_src, self.edge_dst = graph_edges(self.cfg, self.qkv_split)
         self.n_edges = len(self.edge_src)
         self.n_items = 0
         opts = {}

@@ -49,6 +49,21 @@ def test_graph_matches_reference_numbering(ref):
         assert np.array_equal(src, rs) and np.array_equal(dst, rd)
 
 
+def test_qkv_split_graph_matches_oracle():
+    """libcqg's Q/K/V-split graph (extension) equals the oracle's: sources,
+    destinations, receiver components, edge count."""
+    from oracle.oracle import Port
+    from helpers import SMALL, make
+    for cfg in (TINY, TOY, SMALL):
+        n, src, dst = eng.graph_edges(cfg, qkv_split=True)
+        comp = eng.graph_edge_comp(cfg, qkv_split=True)
+        p = Port(cfg, make(cfg)[0].mats, qkv_split=True)
+        _, _, _, ps, pd = p.graph()
+        assert np.array_equal(src, ps) and np.array_equal(dst, pd)
+        assert np.array_equal(comp, p.edge_comp())
+        assert np.array_equal(eng.graph_edge_comp(cfg), np.zeros(len(eng.graph_edges(cfg)[1]), np.int32))
+
+
 def test_sweep_order_matches_reference(ref):
     mask = np.random.RandomState(3).rand(33) < 0.5
     got = eng.sweep_order(TOY, mask)

@@ -477,3 +477,55 @@ def test_nan_logits_raise_runtime_error(opts):
     ok = e.score_edges(mask, edges, eng.PrecisionPolicy.head_quantized(), True, 0)
     assert np.array_equal(ok, np.zeros_like(ok))
     e.close()
+
+
+# --- Q/K/V-split edges (extension, BASELINE config 3) ----------------------------
+@pytest.mark.parametrize("cfg", [SMALL, TOY, MID])
+def test_qkv_split_forwards_and_scores_match_oracle(cfg):
+    """The Q/K/V-split graph (each head sums its q, k and v inputs separately,
+    include/cqg.h): forwards bitwise equal to the oracle restatement under
+    masks that drop components independently and patches on single
+    components; per-edge PAHQ scores (KL, loss and act-diff) and the base
+    policy's scores at rtol 1e-9."""
+    from oracle.oracle import Prune  # noqa: F401
+    w, ds = make(cfg, 5, 3, 6)
+    p = Port(cfg, w.mats, qkv_split=True)
+    e = eng.Engine(w, qkv_split=True)
+    assert e.n_edges == p.n_edges
+    SD = cfg.seq_len * cfg.d_model
+    rng = np.random.RandomState(2)
+    for i, pol in enumerate([Policy.head_quantized(), Policy.make(th=(cfg.n_layers - 1, 1)),
+                             Policy.all_fp32()]):
+        mask = random_mask(p.n_edges, 20 + i, 0.7)
+        pe = int(rng.choice(np.nonzero(mask)[0]))
+        pv = rng.randn(SD).astype(np.float32)
+        a = p.forward(ds.clean[1], pol, mask=mask, patch_edge=pe, patch_value=pv)
+        b = e.forward(ds.clean[1], gpol(pol), mask=mask, patch_edge=pe, patch_value=pv)
+        assert np.array_equal(bits(a), bits(b)), i
+    e.set_dataset(ds, KL)
+    for per_edge, mode, seed in ((True, 0, None), (True, 0, 31), (False, 0, 32), (True, 1, 33)):
+        mask = np.ones(p.n_edges, bool) if seed is None else random_mask(p.n_edges, seed, 0.6)
+        edges = np.nonzero(mask)[0]
+        want = p.score_edges(ds, edges, Policy.head_quantized(), per_edge=per_edge, metric=KL,
+                             mode=mode, mask=mask)
+        got = e.score_edges(mask, edges, eng.PrecisionPolicy.head_quantized(), per_edge, mode)
+        assert close(got, want), (per_edge, mode, seed, np.max(np.abs(got - want)))
+    e.close()
+
+
+def test_qkv_split_toy_acdc_matches_oracle():
+    """Full PAHQ-ACDC on the split graph of config 1: the same steps, records
+    and pruned edge set as the oracle's run_acdc (acdc.cpp:23-88)."""
+    w, ds = make(TOY, 1, 16, 2)
+    p = Port(TOY, w.mats, qkv_split=True)
+    e = eng.Engine(w, qkv_split=True)
+    e.set_dataset(ds, KL)
+    cfg = eng.method_prune_config(eng.PAHQ)
+    cfg.tau, cfg.max_steps = 0.01, 10
+    r = e.run_acdc(cfg)
+    want = p.run_acdc(ds, cfg.c(), KL)
+    assert r.steps == want.steps
+    assert np.array_equal(r.final_mask.astype(np.uint8), want.final_mask.astype(np.uint8))
+    recs = [(s.edge, int(s.kept)) for it in r.iterations for s in it.scores]
+    assert recs == [(int(a), int(k)) for (_, a, _, k) in want.records]
+    e.close()

@@ -311,3 +311,84 @@ def test_int8_forward_per_token_grids():
             q = r / (mx / 127.0) if np.any(r == mx) and mx > 0 else r / (mx / 128.0)
             assert len(np.unique(r)) <= 256
             assert np.allclose(q, np.round(q), atol=1e-4), (n, q[:4])
+
+
+# --- Q/K/V-split edges (extension, BASELINE config 3; parity unpinned) ---------
+def test_qkv_split_edge_counts():
+    """Each head has q / k / v input receivers: 32,491 edges at GPT-2-small
+    (config 3's "~32k"); 49 + 481 l per layer plus 157 into the unembed."""
+    from helpers import GPT2S
+    w = synth.random_weights(GPT2S, 1)
+    p = Port(GPT2S, w.mats, qkv_split=True)
+    assert p.n_edges == 32491
+    L, H = 3, 2
+    cfg = formats.ModelConfig(L, H, 8, 4, 11, 3, 1, 1)
+    p = Port(cfg, synth.random_weights(cfg, 1).mats, qkv_split=True)
+    # receivers: per layer 3H head inputs (1 + (H+1) l senders) + MLP (1 + (H+1) l + H)
+    want = sum(3 * H * (1 + (H + 1) * l) + 1 + (H + 1) * l + H for l in range(L)) + 1 + (H + 1) * L
+    assert p.n_edges == want
+
+
+def test_qkv_split_numbering_and_sweep_order():
+    """Edges are numbered receiver-major (node asc, component q < k < v), then
+    source ascending (model.cpp:192-201 with the receiver in place of the
+    node); the sweep order is receiver descending, source descending
+    (model.cpp:238-246)."""
+    p = Port(SMALL, make(SMALL)[0].mats, qkv_split=True)
+    k, l, h, src, dst = p.graph()
+    comp = p.edge_comp()
+    key = [(int(d), int(c), int(s)) for s, d, c in zip(src, dst, comp)]
+    assert key == sorted(key)
+    assert all(c == 0 for d, c in zip(dst, comp) if k[d] != 1)
+    assert list(p.sweep_order()) == list(range(p.n_edges))[::-1]
+
+
+@pytest.mark.parametrize("cfg", [TINY, SMALL, TOY])
+def test_qkv_split_pins_against_the_reference_graph(cfg):
+    """Where the split graph has a reference counterpart it equals it bit for
+    bit: the full graph (every receiver of a head sums the same sources), and
+    any mask that drops (u -> h.q, u -> h.k, u -> h.v) together (= dropping
+    u -> h in the reference's graph), under several policies. The unsplit
+    oracle is itself pinned to the reference library (test_port_forward_equals_reference)."""
+    w, ds = make(cfg, 4, 2, 5)
+    a, b = Port(cfg, w.mats), Port(cfg, w.mats, qkv_split=True)
+    _, _, _, sa, da = a.graph()
+    _, _, _, sb, db = b.graph()
+    idx = {(int(s), int(d)): i for i, (s, d) in enumerate(zip(sa, da))}
+    rng = np.random.RandomState(7)
+    L = cfg.n_layers
+    for pol in (Policy.head_quantized(), Policy.all_fp32(), Policy.make(th=(L - 1, 0))):
+        fa = a.forward(ds.clean[0], pol)
+        fb = b.forward(ds.clean[0], pol)
+        assert np.array_equal(bits(fa), bits(fb))
+        ma = rng.rand(a.n_edges) < 0.7
+        mb = np.array([ma[idx[(int(s), int(d))]] for s, d in zip(sb, db)])
+        fa = a.forward(ds.clean[1], pol, mask=ma)
+        fb = b.forward(ds.clean[1], pol, mask=mb)
+        assert np.array_equal(bits(fa), bits(fb))
+
+
+def test_qkv_split_patch_moves_one_component():
+    """A patch on u -> h.q changes h's queries only: patching with the clean
+    value is a no-op (test_model.cpp:381-396), and a patch on one component
+    gives a different output from the same patch on another."""
+    w, ds = make(SMALL, 4, 2, 5)
+    p = Port(SMALL, w.mats, qkv_split=True)
+    k, l, h, src, dst = p.graph()
+    comp = p.edge_comp()
+    S, D = SMALL.seq_len, SMALL.d_model
+    base = p.forward(ds.clean[0], Policy.head_quantized())
+    eq = [e for e in range(p.n_edges) if k[dst[e]] == 1 and l[dst[e]] == 1 and comp[e] == 0][0]
+    ek = eq + sum(1 for e in range(p.n_edges) if dst[e] == dst[eq] and comp[e] == 0)  # same source, k input
+    assert src[ek] == src[eq] and comp[ek] == 1
+    s = int(src[eq])
+    same = p.forward(ds.clean[0], Policy.head_quantized(), patch_edge=eq,
+                     patch_value=base[s * S * D:(s + 1) * S * D])
+    assert np.array_equal(bits(same), bits(base))
+    pv = np.random.RandomState(1).randn(S * D).astype(np.float32)
+    fq = p.forward(ds.clean[0], Policy.head_quantized(), patch_edge=eq, patch_value=pv)
+    fk = p.forward(ds.clean[0], Policy.head_quantized(), patch_edge=ek, patch_value=pv)
+    n = int(dst[eq])
+    assert not np.array_equal(fq[n * S * D:(n + 1) * S * D], fk[n * S * D:(n + 1) * S * D])
+    # nodes before the destination's stage are untouched
+    assert np.array_equal(bits(fq[:n * S * D - (h[n]) * S * D]), bits(base[:n * S * D - (h[n]) * S * D]))
