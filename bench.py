@@ -317,7 +317,11 @@ def config_block(args, n_edges_all=None, n_scored=None):
                        + (f"a strided sample of {n_scored} of the {n_edges_all} edges" if sampled
                           else "every edge"),
            "items": items, "parallelism": f"items sharded over {args.gpus} GPU(s)",
-            "low_precision": "e4m3 (reference-pinned; INT8 per-channel not implemented)",
+           "edges": "Q/K/V-split graph (extension, include/cqg.h)" if getattr(args, "qkv_split", False)
+                    else "the reference's graph (model.cpp:192-201)",
+            "low_precision": ("int8 per-channel RTN (extension, exact SIMT path)"
+                              if getattr(args, "low", "e4m3") == "int8"
+                              else "e4m3 (reference-pinned; INT8 per-channel: --low int8)"),
            "l2": "inputs >> L2 (activations per step ~GBs)"}
     if sampled:
         out["edges_sampled"] = {"scored": n_scored, "of": n_edges_all}
@@ -346,6 +350,11 @@ def main(argv=None):
     ap.add_argument("--items", type=int, default=0,
                     help="prompt batch (default: the config's; e.g. the per-GPU shard of an "
                          "8-GPU config on one GPU)")
+    ap.add_argument("--low", default="e4m3", choices=["e4m3", "int8"],
+                    help="low precision of the heads: e4m3 (reference-pinned, tensor cores) or "
+                         "int8 (per-channel RTN extension, exact path)")
+    ap.add_argument("--qkv-split", action="store_true",
+                    help="the Q/K/V-split edge graph (extension; config 3's ~32k edges)")
     ap.add_argument("--max-edges", type=int, default=0,
                     help="score an evenly strided sample of at most this many iteration-1 edges "
                          "(configs 4-5 on one GPU; reported in config.edges_sampled)")
@@ -374,7 +383,7 @@ def main(argv=None):
     items = len(ds)
     lo, hi = shard_mod.item_block(rank, world, items)
     shard = ds.subset(list(range(lo, hi)))
-    e = eng.Engine(w, device=local)
+    e = eng.Engine(w, device=local, qkv_split=args.qkv_split)
     for kv in filter(None, os.environ.get("CQG_OPTS", "").split(",")):  # e.g. exact_x2=0
         k, v = kv.split("=")
         e.set_option(k, int(v))
@@ -389,7 +398,7 @@ def main(argv=None):
     n_edges_all = len(edges)
     if args.max_edges and len(edges) > args.max_edges:  # strided: every source depth is sampled
         edges = edges[::-(-len(edges) // args.max_edges)]
-    pol = eng.PrecisionPolicy.head_quantized()
+    pol = eng.PrecisionPolicy.head_quantized(eng.P8, eng.INT8 if args.low == "int8" else eng.E4M3)
     passes_per_step = len(edges) * items
 
     def barrier():

@@ -36,7 +36,7 @@ cqg_ctx* make_cqg(const WeightSet& w, const Dataset& ds, Metric metric, int devi
   const cqg_config c{static_cast<uint32_t>(m.n_layers), static_cast<uint32_t>(m.n_heads),
                      static_cast<uint32_t>(m.d_model),  static_cast<uint32_t>(m.d_k),
                      static_cast<uint32_t>(m.vocab),    static_cast<uint32_t>(m.seq_len),
-                     static_cast<uint32_t>(m.has_mlp ? 1 : 0)};
+                     static_cast<uint32_t>(m.has_mlp ? 1 : 0), /*qkv_split=*/0u};  // the reference's graph
   cqg_ctx* ctx = nullptr;
   cqg_check(cqg_create(&c, mats.data(), device, &ctx));
   std::vector<int32_t> clean, corrupt, answer, distractor;
