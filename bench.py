@@ -466,13 +466,14 @@ def main(argv=None):
     # per multiply-add, counted as 2 flops
     simt_peak = 148 * 128 * 1.965e9 / 1e12
     traffic, traffic_note = None, None
-    tp = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
-    if os.path.exists(tp):  # committed ncu --set full capture of this kernel class
-        t = json.load(open(tp)).get(name.split(":")[-1])
-        if t:
-            traffic = t["traffic_bytes"]
-            traffic_note = (f"dram bytes of one captured launch ({t['launch']}); algorithmic "
-                            f"{t['algorithmic_bytes']} B for that launch")
+    for tp in (os.path.join(ROOT, "profiles", "r2_ncu_traffic.json"),
+               os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")):
+        if traffic is None and os.path.exists(tp):  # committed ncu --set full capture of this class
+            t = json.load(open(tp)).get(name.split(":")[-1])
+            if t:
+                traffic = t["traffic_bytes"]
+                traffic_note = (f"dram bytes of one captured launch ({t['launch']}); algorithmic "
+                                f"{t['algorithmic_bytes']} B for that launch ({os.path.basename(tp)})")
     cls = name.split(":")[-1]  # "base:" = per-source baseline runs
     if p["flops"] > 0:
         ach = p["flops"] / (p["ms"] / 1e3) / 1e12
@@ -493,7 +494,16 @@ def main(argv=None):
                 "per_kernel": {k: {"ms": v["ms"], "launches": v["launches"],
                                    "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9,
                                    "gbs": v["bytes"] / max(v["ms"], 1e-9) / 1e6}
-                               for k, v in prof.items()}}
+                               for k, v in prof.items()},
+                "per_kernel_note": "gbs = algorithmic bytes (every operand read counted, incl. re-reads "
+                                   "served by L2) / CUDA-event time; measured DRAM throughput: hbm_kernels_ncu"}
+    dp = os.path.join(ROOT, "profiles", "r2_dram_per_kernel.json")
+    if os.path.exists(dp):  # committed per-launch ncu DRAM bytes of one whole step
+        dk = json.load(open(dp))
+        roofline["hbm_kernels_ncu"] = {
+            "source": "profiles/r2_dram_per_kernel.json (" + dk["source"] + ")",
+            "kernels": {k: dk["kernels"][k] for k in dk["kernels"]
+                        if any(x in k for x in ("fold", "ln_small_kernel<4>", "kl_reduce", "attention"))}}
 
     acdc = None
     if args.acdc:  # every rank runs the loop on its item block; scores are all-reduced per iteration

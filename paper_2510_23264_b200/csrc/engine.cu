@@ -580,7 +580,7 @@ struct Engine {
         j.group_off = j.ld, j.rows = 1;
       }
       Prof pf(this, "int8_act");
-      launch_rtn_act(upload(rows), (int)rows.size(), nb * g.S, 8, st, 127);
+      launch_rtn_rows(upload(rows), (int)rows.size(), nb * g.S, 8, st, 127);
       return;
     }
     Prof pf(this, "rtn4_act");

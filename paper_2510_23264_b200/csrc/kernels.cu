@@ -1906,6 +1906,38 @@ __global__ void rtn_act_kernel(const RtnJob* __restrict__ jobs, int bits, int qm
   }
 }
 
+// Per-row groups (the INT8 extension's per-token scales): one warp per row
+// group (rows = 1), max in double over the warp, then the RTN of the row.
+__global__ void rtn_rows_kernel(const RtnJob* __restrict__ jobs, int n_groups, int bits, int qmax) {
+  const RtnJob jb = jobs[blockIdx.y];
+  const int gi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (gi >= n_groups) return;
+  float* base = jb.p + (int64_t)gi * jb.group_off;
+  double mx = 0.0;
+  for (int i = lane; i < jb.cols; i += 32) {
+    float x = base[i];
+    if (jb.gelu) base[i] = x = gelu_ref(x);
+    const double a = fabs((double)x);
+    mx = (a > mx) ? a : mx;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double y = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = (y > mx) ? y : mx;
+  }
+  __syncwarp();
+  const double delta = (mx == 0.0) ? 0.0 : __ddiv_rn(mx, ldexp(1.0, bits - 1));
+  for (int i = lane; i < jb.cols; i += 32) base[i] = rtn_apply(base[i], delta, qmax);
+}
+
+void launch_rtn_rows(const RtnJob* d_jobs, int n_jobs, int n_groups, int bits, cudaStream_t st, int qmax) {
+  for (int y0 = 0; y0 < n_jobs; y0 += 65535)
+    if (n_groups > 0)
+      rtn_rows_kernel<<<dim3((n_groups + 7) / 8, std::min(65535, n_jobs - y0)), 256, 0, st>>>(d_jobs + y0, n_groups,
+                                                                                              bits, qmax);
+}
+
 void launch_rtn_act(const RtnJob* d_jobs, int n_jobs, int n_groups, int bits, cudaStream_t st, int qmax) {
   for (int y0 = 0; y0 < n_jobs; y0 += 65535)
     if (n_groups > 0)

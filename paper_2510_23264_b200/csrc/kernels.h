@@ -176,6 +176,8 @@ struct RtnJob {
 };
 // qmax: INT8 extension clamp (127), 0 = none
 void launch_rtn_act(const RtnJob* d_jobs, int n_jobs, int n_groups, int bits, cudaStream_t st, int qmax = 0);
+// rows = 1 groups (per-token scales): one warp per group
+void launch_rtn_rows(const RtnJob* d_jobs, int n_jobs, int n_groups, int bits, cudaStream_t st, int qmax = 0);
 
 // ---- tests: exhaustive scalar checks on the device --------------------------
 void launch_e4m3_all(uint8_t* out, uint32_t lo, uint64_t count, cudaStream_t st);
