@@ -105,6 +105,25 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
     L.prec = prec, L.epi = epi;
     L.total_tiles = ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
     L.fix_mask = fmask, L.fix_tiles = ftiles, L.tile_mark = fmark, L.fix_count = cnt;
+    uint64_t* fitems;
+    uint32_t* fn;
+    int4* fst;
+    {
+      TcJob hj{};
+      hj.M = M, hj.N = N, hj.K = K;
+      // CQG_DIAG_FIX_G: tile-fixup unit (default: the engine's rule by K)
+      const char* fg = getenv("CQG_DIAG_FIX_G");
+      L.fix_g = fg ? atoi(fg) : (elem == kTcBF16 && K < 2048 ? 2 : 1);
+      std::vector<int4> sts = fixup_super_tiles(&hj, 1);
+      const size_t units = L.fix_g == 2 ? sts.size() : ntile;
+      cudaMalloc(&fitems, units * fix_item_cap(L.fix_g) * 8);
+      cudaMalloc(&fn, units * 4);
+      cudaMalloc(&fst, sts.size() * sizeof(int4));
+      cudaMemcpy(fst, sts.data(), sts.size() * sizeof(int4), cudaMemcpyHostToDevice);
+      L.fix_st = fst, L.n_fix_st = (int)sts.size();
+    }
+    L.fix_items = fitems, L.fix_n = fn;
+    if (const char* fc = getenv("CQG_DIAG_FIX_CPI")) L.fix_cpi = atoi(fc);  // tile fixup item mode
     launch_gemm_tc(L, dj, 0);
     // BF16: the chunked block fixup unless CQG_DIAG_FIX_BLK=0 (tests run both)
     const char* fe = getenv("CQG_DIAG_FIX_BLK");
@@ -134,6 +153,7 @@ int cqg_diag_gemm_tc(int elem, int prec, int epi, int M, int N, int K, const flo
     cudaMemcpy(out_tc, dC1, (size_t)M * N * 4, cudaMemcpyDeviceToHost);
     cudaMemcpy(out_exact, dC2, (size_t)M * N * 4, cudaMemcpyDeviceToHost);
     if (dfb) cudaFree(dfb);
+    cudaFree(fitems), cudaFree(fn), cudaFree(fst);
     uint64_t c[2] = {0, 0};
     cudaMemcpy(c, cnt, 16, cudaMemcpyDeviceToHost);
     *n_fix = (uint32_t)c[1];

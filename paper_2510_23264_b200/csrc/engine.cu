@@ -317,7 +317,9 @@ struct Engine {
   int64_t opt_fix_blk = 0;
   int64_t opt_fix_blk_min = 148;
   int64_t opt_kl_fused = 1;  // patched rows: unembed with the KL in its epilogue (no logits)  // ... for launches with at least this many row-tile units
-  int64_t opt_fix_cpi = 0;  // store E4M3/BF16-rounded node outputs as their codes
+  int64_t opt_fix_cpi = 0;
+  int64_t opt_fix_dry = 0;
+  int64_t opt_fix_g = 0;  // tile-fixup unit (0: by K, 1 tiles, 2 super-tiles)  // timing experiment (wrong results): fixups without chains  // store E4M3/BF16-rounded node outputs as their codes
   int64_t opt_mem_budget = 0;
   // 1: the patched passes' FP32 unembed on the tensor cores (6-term BF16
   // split) with the KL-level certificate and exact recomputation of flagged
@@ -608,7 +610,7 @@ struct Engine {
     int rows = 0, cols = 0, elem = 0;
   };
   std::map<std::tuple<int, int, int>, std::unique_ptr<PackedB>> packed;
-  DeviceBuf fix_mask, fix_tiles, tile_mark, fix_cnt, gelu_lut;
+  DeviceBuf fix_mask, fix_tiles, tile_mark, fix_cnt, gelu_lut, fix_items, fix_n;
 
   // which: 0 QKV [3D x D], 1 W_O [D x D] (per-head K slices), 2 W_in^T [4D x D],
   // 3 W_out^T [D x 4D]
@@ -670,7 +672,10 @@ struct Engine {
     L.kappa = 8.0f;
     // fixup columns per work item: adaptive (0) by default; two columns share
     // each A load for long chains (K >= 2048: measured faster on W_out)
+    // columns per fixup work item: adaptive (0) by default; two columns share
+    // each A load for long chains (K >= 2048: measured faster on W_out)
     L.fix_cpi = opt_fix_cpi ? (int)opt_fix_cpi : (a_k >= 2048 ? 2 : 0);
+    L.fix_dry = (int)opt_fix_dry;
     if (!gelu_lut.p) {
       gelu_lut.ensure(65536 * 2);
       launch_gelu_lut(gelu_lut.as<uint16_t>(), st);
@@ -709,6 +714,17 @@ struct Engine {
     const size_t had = tile_mark.bytes;
     tile_mark.ensure((size_t)total * 4);
     if (tile_mark.bytes != had) CK(cudaMemsetAsync(tile_mark.p, 0, tile_mark.bytes, st));
+    // the tile fixup's units and their item lists (built on the device):
+    // 2 x 2-tile super-tiles for short BF16 chains (W_in), else listed tiles
+    L.fix_g = opt_fix_g ? (int)opt_fix_g : (elem == kTcBF16 && a_k < 2048 ? 2 : 1);
+    std::vector<int4> sts;
+    if (L.fix_g == 2) sts = fixup_super_tiles(jobs.data(), (int)jobs.size());
+    const size_t units = L.fix_g == 2 ? sts.size() : (size_t)total;
+    fix_items.ensure(std::max<size_t>(units, 1) * fix_item_cap(L.fix_g) * 8);
+    fix_n.ensure(std::max<size_t>(units, 1) * 4);
+    L.fix_items = fix_items.as<uint64_t>();
+    L.fix_n = fix_n.as<uint32_t>();
+    L.n_fix_st = (int)sts.size();
     L.fix_mask = fix_mask.as<uint32_t>();
     L.fix_tiles = fix_tiles.as<uint32_t>();
     L.tile_mark = tile_mark.as<uint32_t>();
@@ -738,10 +754,11 @@ struct Engine {
       L.n_fix_blocks = (int)fb.size();
     }
     reserve(up_bytes(jobs.size(), sizeof(TcJob)) + up_bytes(tj_map.size(), sizeof(int)) +
-            (blk ? up_bytes(fb.size(), sizeof(int4)) : 0));
+            (blk ? up_bytes(fb.size(), sizeof(int4)) : 0) + up_bytes(sts.size(), sizeof(int4)));
     const TcJob* dj = upload(jobs);
     L.tile_job = upload(tj_map);
     if (blk) L.fix_blocks = upload(fb);
+    L.fix_st = sts.empty() ? nullptr : upload(sts);
     {
       Prof pf(this, elem == kTcBF16 ? (std::string("gemm_tc_bf16_") + name).c_str()
                                     : (std::string("gemm_tc_fp8_") + name).c_str(),
@@ -2380,6 +2397,11 @@ int cqg_set_option(cqg_ctx* ctx, const char* key, int64_t value) {
     else if (k == "fix_blk") ctx->e->opt_fix_blk = value;
     else if (k == "fix_blk_min") ctx->e->opt_fix_blk_min = value;
     else if (k == "kl_fused") ctx->e->opt_kl_fused = value;
+    else if (k == "fix_dry") ctx->e->opt_fix_dry = value;
+    else if (k == "fix_g") {
+      if (value < 0 || value > 2) throw Error(1, "fix_g must be 0, 1 or 2");
+      ctx->e->opt_fix_g = value;
+    }
     else if (k == "prefetch") ctx->e->opt_prefetch = value;
     else if (k == "mem_budget") ctx->e->opt_mem_budget = value;
     else if (k == "unembed_tc") ctx->e->opt_unembed_tc = value;

@@ -699,11 +699,37 @@ __device__ __forceinline__ void dec16(const uint4 v, float* out) {
 constexpr int kFixThreads = 512;
 constexpr int kFixCols = 4;   // flagged columns of one row per work item
 constexpr int kFixPer = 2;    // work items per thread per round
-constexpr int kFixStages = 4;
-constexpr int kFixMaxSplit = 4;  // CTAs sharing one flagged tile when tiles are few
-constexpr int kFixMaxItems = kTcBM * kTcBN / kFixCols + kTcBM;
-constexpr size_t kFixSmem = 1024 + (size_t)kFixStages * (kAStage + kBStage) + 256 +
-                            (size_t)kFixMaxItems * sizeof(uint64_t) + 1024;
+// The fixup works on 2 x 2-tile super-tiles (256 x 256 outputs): the chains
+// of ~4x as many flagged elements are in flight per SM (the chains are
+// latency-bound: one dependent FHFMA chain per flagged element), and each
+// K slice of the 256 A rows and 256 B rows is streamed once for 4 tiles.
+constexpr int kFixStages = 6;  // ring slots (max) of g = 1 units (3 for g = 2)
+#ifndef L_FIX_SLOTS1
+#define L_FIX_SLOTS1 4
+#endif
+constexpr int kFixRows = 2 * kTcBM;                        // super-tile rows (= columns)
+constexpr int kFixStageBytes = kFixRows * kBKBytes;        // 32 KB per operand per stage
+constexpr int kFixMaxSplit = 4;  // CTAs sharing one super-tile when they are few
+constexpr int kFixMaxItems = kFixRows * kFixRows / kFixCols + kFixRows;
+// units of the tile fixup: 2 x 2-tile super-tiles (fix_g 2, the host table
+// fix_st; BF16 K < 2048, where the chains are short and many flagged tiles
+// share rows) or the GEMM's listed flagged tiles (fix_g 1, fix_tiles, count
+// on the device; long chains and the near-empty E4M3 launches)
+__host__ __device__ constexpr int fix_cap(int g) { return g * kTcBM * g * kTcBN / kFixCols + g * kTcBM; }
+__device__ __forceinline__ int fix_n_units(const TcLaunch& L) {
+  return L.fix_g == 2 ? L.n_fix_st : (int)*L.fix_count;
+}
+__device__ __forceinline__ int4 fix_unit(const TcLaunch& L, const TcJob* jobs, int i) {
+  if (L.fix_g == 2) return L.fix_st[i];
+  const int tile = (int)L.fix_tiles[i];
+  const int j = job_of(L, jobs, tile);
+  const int tiles_n = (jobs[j].N + kTcBN - 1) / kTcBN;
+  return make_int4(j, (tile - jobs[j].tile0) / tiles_n, (tile - jobs[j].tile0) % tiles_n, 0);
+}
+constexpr size_t kFixSmem = 1024 + (size_t)3 * 2 * kFixStageBytes + 256 + 1024;
+// ring slots and slot size per operand of a unit of g x g tiles (same bytes)
+__device__ __forceinline__ int fix_slots(int g) { return g == 2 ? 3 : L_FIX_SLOTS1; }
+__device__ __forceinline__ int fix_slot_bytes(int g) { return g * kTcBM * kBKBytes; }
 
 // A row's norm carries a sign bit when the row holds a value whose products
 // might not be exact in FP32 (rownorm_kernel); otherwise fl(s + fl(a*b)) ==
@@ -794,38 +820,176 @@ struct FixItem {
   float acc[kFixCols];
 };
 
+// A TMA stream of the tile fixup: one round of one super-tile's K extent.
+struct FixStream {
+  int valid, arow, brow, bk0, nk, g;  // g: 128-row boxes per operand
+};
+
+template <int ELEM>
+__device__ __forceinline__ void fix_issue(const TcLaunch& L, uint8_t* sA, uint8_t* sB, uint64_t* full,
+                                          uint64_t* empty, uint32_t& ld, const FixStream& f, int kb) {
+  constexpr int bke = kBKBytes / (ELEM == kTcBF16 ? 2 : 1);
+  const int ns = fix_slots(f.g);
+  const int s = ld % ns;
+  mbar_wait(&empty[s], ((ld / ns) & 1) ^ 1);
+  mbar_expect_tx(&full[s], 2 * f.g * kTcBM * kBKBytes);
+  uint8_t* a = sA + s * fix_slot_bytes(f.g);
+  uint8_t* b = sB + s * fix_slot_bytes(f.g);
+  // g 128-row boxes per operand: row r of the unit sits at r * 128 B (past a
+  // job's or tensor's last row: unused rows / TMA zero fill)
+  for (int h = 0; h < f.g; ++h) {
+    tma_load_2d(a + h * kTcBM * kBKBytes, &L.tmA, &full[s], kb * bke, f.arow + h * kTcBM);
+    tma_load_2d(b + h * kTcBN * kBKBytes, &L.tmB, &full[s], f.bk0 + kb * bke, f.brow + h * kTcBN);
+  }
+  ++ld;
+}
+
 // One round of the TMA ring over the tile's K extent for this thread's items.
+// The producer (thread 0) keeps the ring full across rounds: once the current
+// stream's stages are all issued it issues the next round's (nxt), so the
+// next tile's first stages arrive while this round's chains finish.
 template <int ELEM, int CPI>
 __device__ __forceinline__ void fix_round(const TcLaunch& L, FixItem (&w)[kFixPer], uint8_t* sA,
-                                          uint8_t* sB, uint64_t* full, uint64_t* empty, int nk,
-                                          int kbytes, int arow, int brow, int bk0, uint32_t& ld,
-                                          uint32_t& it) {
-  constexpr int esz = ELEM == kTcBF16 ? 2 : 1;
-  constexpr int bke = kBKBytes / esz;
+                                          uint8_t* sB, uint64_t* full, uint64_t* empty,
+                                          const FixStream& cur, const FixStream& nxt, int& nxt_issued,
+                                          int kbytes, uint32_t& ld, uint32_t& it) {
   const int tid = threadIdx.x, lane = tid & 31;
+  const int nk = cur.nk;
   for (int kb = 0; kb < nk; ++kb, ++it) {
-    const int s = it % kFixStages;
-    mbar_wait(&full[s], (it / kFixStages) & 1);
-    const uint32_t a0 = smem_u32(sA + s * kAStage), b0 = smem_u32(sB + s * kBStage);
+    const int ns = fix_slots(cur.g);
+    const int s = it % ns;
+    if (L.fix_dry != 2) mbar_wait(&full[s], (it / ns) & 1);
+    const uint32_t a0 = smem_u32(sA + s * fix_slot_bytes(cur.g)), b0 = smem_u32(sB + s * fix_slot_bytes(cur.g));
     const int nu = min(8, (kbytes - kb * kBKBytes) / 16);
 #pragma unroll
     for (int j = 0; j < kFixPer; ++j) {
-      if (w[j].row < 0) continue;
+      // (timing experiments, wrong results: fix_dry 1 streams without chains,
+      // 2 runs the chains on whatever shared memory holds, without streaming)
+      if (w[j].row < 0 || L.fix_dry == 1) continue;
       const uint32_t ar = a0 + w[j].row * kBKBytes, ra16 = (w[j].row & 7) << 4;
       if (w[j].fma) fix_chunk<ELEM, true, CPI>(ar, ra16, b0, w[j].col, nu, w[j].acc);
       else fix_chunk<ELEM, false, CPI>(ar, ra16, b0, w[j].col, nu, w[j].acc);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    if (tid == 0 && kb + kFixStages < nk) {
-      const int ss = ld % kFixStages;
-      mbar_wait(&empty[ss], ((ld / kFixStages) & 1) ^ 1);
-      mbar_expect_tx(&full[ss], kAStage + kBStage);
-      tma_load_2d(sA + ss * kAStage, &L.tmA, &full[ss], (kb + kFixStages) * bke, arow);
-      tma_load_2d(sB + ss * kBStage, &L.tmB, &full[ss], bk0 + (kb + kFixStages) * bke, brow);
-      ++ld;
+    if (tid == 0 && L.fix_dry != 2) {
+      const int ns2 = fix_slots(cur.g);
+      if (kb + ns2 < nk) fix_issue<ELEM>(L, sA, sB, full, empty, ld, cur, kb + ns2);
+      else if (nxt.valid && kb + ns2 - nk < nxt.nk && nxt_issued == kb + ns2 - nk) {
+        fix_issue<ELEM>(L, sA, sB, full, empty, ld, nxt, nxt_issued);
+        ++nxt_issued;
+      }
     }
   }
+}
+
+// Item lists of the launch's super-tiles (fix_plan_kernel): per super-tile,
+// up to kFixMaxItems 64-bit items  row | ncol << 8 | col_c << (16 + 12 c)
+// (rows / columns 0..255 of the super-tile), the FMA-safety of the item in
+// bit 27 (col_0's spare bit 11), and the count n | cpi << 24 in fix_n. Built
+// once per launch by a separate kernel, so the fixup's per-super-tile setup
+// is one load of n and one load of each thread's items.
+constexpr uint64_t kFixItemFma = 1ull << 27;
+
+template <int ELEM>
+__global__ void __launch_bounds__(kFixRows) fix_plan_kernel(const __grid_constant__ TcLaunch L,
+                                                            const TcJob* __restrict__ jobs) {
+  __shared__ int wsum[kFixRows / 32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = L.fix_g, n_units = fix_n_units(L), cap = fix_cap(g);
+  for (int si = blockIdx.x; si < n_units; si += gridDim.x) {
+    const int4 sd = fix_unit(L, jobs, si);  // job, first row tile, first column tile
+    const TcJob& jb = jobs[sd.x];
+    const int tiles_m = (jb.M + kTcBM - 1) / kTcBM, tiles_n = (jb.N + kTcBN - 1) / kTcBN;
+    const int mt = sd.y + tid / kTcBM, rr = tid % kTcBM, q = rr >> 5;
+    uint32_t wm[8];
+#pragma unroll
+    for (int ct = 0; ct < 2; ++ct) {
+      uint4 m = make_uint4(0u, 0u, 0u, 0u);
+      uint32_t parts = 0u;
+      if (tid < g * kTcBM && ct < g && mt < tiles_m && sd.z + ct < tiles_n) {
+        const int tile = jb.tile0 + mt * tiles_n + sd.z + ct;
+        parts = L.tile_mark[tile];
+        if (parts) m = *reinterpret_cast<const uint4*>(L.fix_mask + (size_t)tile * kFixWords + rr * 4);
+      }
+      wm[4 * ct + 0] = (parts >> q) & 1u ? m.x : 0u;
+      wm[4 * ct + 1] = (parts >> q) & 1u ? m.y : 0u;
+      wm[4 * ct + 2] = (parts >> (q + 4)) & 1u ? m.z : 0u;
+      wm[4 * ct + 3] = (parts >> (q + 4)) & 1u ? m.w : 0u;
+    }
+    int pc = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pc += __popc(wm[k]);
+    if (!__syncthreads_or(pc)) {  // nothing flagged in this unit (most E4M3 tiles)
+      if (tid == 0) L.fix_n[si] = 0u;
+      continue;
+    }
+    int tot = pc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    __syncthreads();  // (wsum reuse)
+    if (lane == 0) wsum[warp] = tot;
+    __syncthreads();
+    int n_el = 0;
+#pragma unroll
+    for (int w = 0; w < kFixRows / 32; ++w) n_el += wsum[w];
+    // columns per item: one while the fixup CTA has idle threads, up to
+    // kFixCols when there is work to spare or the list would overflow
+    const int need = (n_el + kFixThreads * kFixPer - 1) / (kFixThreads * kFixPer);
+    const int cap_cpi = n_el + g * kTcBM <= cap ? 1 : (n_el / 2 + g * kTcBM <= cap ? 2 : kFixCols);
+    const int cpi = L.fix_cpi ? max(L.fix_cpi, cap_cpi) : max(cap_cpi, need <= 1 ? 1 : (need == 2 ? 2 : kFixCols));
+    const int cnt = (pc + cpi - 1) / cpi;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    __syncthreads();
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int pos = incl - cnt, n = 0;
+    for (int w = 0; w < kFixRows / 32; ++w) {
+      if (w < warp) pos += wsum[w];
+      n += wsum[w];
+    }
+    const int grow = sd.y * kTcBM + tid;  // row within the job
+    // (rows past the job have no flagged elements: their norms are not read)
+    const bool row_ok = ELEM == kTcE4M3 || grow >= jb.M || a_fma_safe(L, jb.a_row0 + grow);
+    uint64_t* out = L.fix_items + (size_t)si * cap;
+    uint64_t item = 0;
+    int nc = 0;
+    bool ok = row_ok;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t mm = wm[k];
+      while (mm) {
+        const int bit = __ffs(mm) - 1;
+        mm &= mm - 1;
+        const int col = k * 32 + bit;
+        item |= (uint64_t)col << (16 + 12 * nc);
+        if (ELEM == kTcBF16) ok = ok && fma_safe(jb.b_norm[sd.z * kTcBN + col]);
+        if (++nc == cpi) {
+          out[pos++] = item | (uint64_t)tid | ((uint64_t)nc << 8) | (ok ? kFixItemFma : 0ull);
+          item = 0, nc = 0, ok = row_ok;
+        }
+      }
+    }
+    if (nc) out[pos++] = item | (uint64_t)tid | ((uint64_t)nc << 8) | (ok ? kFixItemFma : 0ull);
+    if (tid == 0) L.fix_n[si] = (uint32_t)n | ((uint32_t)cpi << 24);
+  }
+}
+
+// The stream (geometry) of super-tile si
+template <int ELEM>
+__device__ __forceinline__ FixStream fix_stream_of(const TcLaunch& L, const TcJob* jobs, uint32_t si) {
+  const int4 sd = fix_unit(L, jobs, (int)si);
+  const TcJob& jb = jobs[sd.x];
+  FixStream f;
+  f.valid = 1, f.arow = jb.a_row0 + sd.y * kTcBM, f.brow = jb.b_row0 + sd.z * kTcBN, f.bk0 = jb.b_k0;
+  f.nk = (jb.K * (ELEM == kTcBF16 ? 2 : 1) + kBKBytes - 1) / kBKBytes;
+  f.g = L.fix_g;
+  return f;
 }
 
 // Exact sequential recomputation of the flagged elements (dot_col order,
@@ -844,129 +1008,91 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   // the compiler keeps every derived access in the shared address space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kFixStages * kAStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kFixStages * kBStage);
+  const int ring = fix_slots(L.fix_g) * fix_slot_bytes(L.fix_g);  // bytes per operand
+  uint8_t* sB = smem + ring;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + ring);
   uint64_t* empty = full + kFixStages;
-  int* wsum = reinterpret_cast<int*>(empty + kFixStages);  // [8]
-  uint64_t* items = reinterpret_cast<uint64_t*>(smem + kFixStages * (kAStage + kBStage) + 256);
   constexpr int esz = ELEM == kTcBF16 ? 2 : 1;
-  constexpr int bke = kBKBytes / esz;
   constexpr int kWarps = kFixThreads / 32;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int s = 0; s < kFixStages; ++s) {
+    for (int s = 0; s < fix_slots(L.fix_g); ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const uint32_t n_tiles = *L.fix_count;
+  const uint32_t n_tiles = *L.fix_count;  // (listed GEMM tiles: their marks are reset at the end)
   uint32_t ld = 0, it = 0;  // TMA loads issued / chunks consumed (ring phases)
-  // Few flagged tiles (small launches): split each tile's work items over up
-  // to kFixMaxSplit CTAs (each streams the tile's operands; L2 absorbs the
-  // repeats) so every SM has work.
-  const uint32_t split = n_tiles ? min((uint32_t)kFixMaxSplit, max(1u, gridDim.x / n_tiles)) : 1u;
-  for (uint32_t vt = blockIdx.x; vt < n_tiles * split; vt += gridDim.x) {
-    const uint32_t ti = vt / split, part = vt % split;
-    const int tile = (int)L.fix_tiles[ti];
-    // ---- work items: row | ncol << 8 | col_c << (16 + 12 c). Columns per item
-    // adapt to the tile's flagged count: one per item while the CTA has idle
-    // threads (parallelism), up to kFixCols when there is work to spare.
-    int pc = 0;
-    uint32_t wm[4] = {0, 0, 0, 0};
-    if (tid < kTcBM) {
-      const uint32_t parts = L.tile_mark[tile];
-      const uint4 m = *reinterpret_cast<const uint4*>(L.fix_mask + (size_t)tile * kFixWords + tid * 4);
-      const int q = tid >> 5;
-      wm[0] = (parts >> q) & 1u ? m.x : 0u;
-      wm[1] = (parts >> q) & 1u ? m.y : 0u;
-      wm[2] = (parts >> (q + 4)) & 1u ? m.z : 0u;
-      wm[3] = (parts >> (q + 4)) & 1u ? m.w : 0u;
-      pc = __popc(wm[0]) + __popc(wm[1]) + __popc(wm[2]) + __popc(wm[3]);
-    }
-    int tot = pc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    if (tid < kTcBM && lane == 0) wsum[4 + warp] = tot;
-    __syncthreads();
-    const int n_el = wsum[4] + wsum[5] + wsum[6] + wsum[7];
-    const int need = (n_el + kFixThreads * kFixPer - 1) / (kFixThreads * kFixPer);
-    // a requested width is raised where the item list would overflow its
-    // shared-memory capacity (n_el / cpi + one partial item per row)
-    const int cap_cpi = n_el + kTcBM <= kFixMaxItems ? 1 : (n_el / 2 + kTcBM <= kFixMaxItems ? 2 : kFixCols);
-    const int cpi = L.fix_cpi ? max(L.fix_cpi, cap_cpi) : (need <= 1 ? 1 : (need == 2 ? 2 : kFixCols));
-    const int cnt = (pc + cpi - 1) / cpi;
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (tid < kTcBM && lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    if (tid < kTcBM) {
-      int pos = incl - cnt;
-      for (int p = 0; p < warp; ++p) pos += wsum[p];
-      uint64_t item = 0;
-      int nc = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        uint32_t m = wm[k];
-        while (m) {
-          const int bit = __ffs(m) - 1;
-          m &= m - 1;
-          item |= (uint64_t)(k * 32 + bit) << (16 + 12 * nc);
-          if (++nc == cpi) {
-            items[pos++] = item | (uint64_t)tid | ((uint64_t)nc << 8);
-            item = 0, nc = 0;
-          }
-        }
-      }
-      if (nc) items[pos++] = item | (uint64_t)tid | ((uint64_t)nc << 8);
-    }
-    __syncthreads();  // (tile_mark is cleared by the last CTA at the end)
-    const int n = wsum[0] + wsum[1] + wsum[2] + wsum[3];
-    const TcJob jb = jobs[job_of(L, jobs, tile)];
-    const int tiles_n = (jb.N + kTcBN - 1) / kTcBN;
-    const int mt = (tile - jb.tile0) / tiles_n, nt = (tile - jb.tile0) % tiles_n;
-    const int arow = jb.a_row0 + mt * kTcBM, brow = jb.b_row0 + nt * kTcBN;
+  // Few super-tiles (small launches): split each one's work items over up to
+  // kFixMaxSplit CTAs (each streams the operands; L2 absorbs the repeats) so
+  // every SM has work.
+  const uint32_t n_st = (uint32_t)fix_n_units(L);
+  const uint32_t split = n_st ? min((uint32_t)kFixMaxSplit, max(1u, gridDim.x / n_st)) : 1u;
+  const uint32_t n_vt = n_st * split;
+  const int cap = fix_cap(L.fix_g);
+  auto range = [&](uint32_t vt, int& lo, int& hi) {  // item range of virtual tile vt
+    const uint32_t n = L.fix_n[vt / split] & 0xFFFFFFu, part = vt % split;
+    lo = (int)((uint64_t)n * part / split), hi = (int)((uint64_t)n * (part + 1) / split);
+  };
+  // thread 0's lookahead: the next round's stream and how many of its stages are issued
+  FixStream nxt{0, 0, 0, 0, 0, 1};
+  int nxt_issued = 0;
+  for (uint32_t vt = blockIdx.x; vt < n_vt; vt += gridDim.x) {
+    int e_lo, e_hi;
+    range(vt, e_lo, e_hi);
+    if (e_lo >= e_hi) continue;
+    const uint32_t ti = vt / split;  // super-tile
+    const int cpi = (int)(L.fix_n[ti] >> 24);
+    const int4 sd = fix_unit(L, jobs, (int)ti);
+    const TcJob jb = jobs[sd.x];
+    const int mt = sd.y, nt = sd.z;  // first row / column tile
+    const FixStream cur = fix_stream_of<ELEM>(L, jobs, ti);
     const int kbytes = jb.K * esz;
-    const int nk = (kbytes + kBKBytes - 1) / kBKBytes;
-    const int e_lo = (int)((uint64_t)n * part / split), e_hi = (int)((uint64_t)n * (part + 1) / split);
+    const uint64_t* items = L.fix_items + (size_t)ti * cap;
     for (int e0 = e_lo; e0 < e_hi; e0 += kFixThreads * kFixPer) {
-      if (tid == 0) {  // prologue: fill the ring
-        for (int kb = 0; kb < min(kFixStages, nk); ++kb, ++ld) {
-          const int s = ld % kFixStages;
-          mbar_wait(&empty[s], ((ld / kFixStages) & 1) ^ 1);
-          mbar_expect_tx(&full[s], kAStage + kBStage);
-          tma_load_2d(sA + s * kAStage, &L.tmA, &full[s], kb * bke, arow);
-          tma_load_2d(sB + s * kBStage, &L.tmB, &full[s], jb.b_k0 + kb * bke, brow);
+      if (tid == 0 && L.fix_dry != 2) {
+        // prologue: the stages of this round the previous round did not issue
+        for (int kb = nxt_issued; kb < min(fix_slots(cur.g), cur.nk); ++kb)
+          fix_issue<ELEM>(L, sA, sB, full, empty, ld, cur, kb);
+        nxt_issued = 0;
+        // the round after this one: this unit again, or the next non-empty virtual unit
+        nxt.valid = 0;
+        if (e0 + kFixThreads * kFixPer < e_hi) {
+          nxt = cur;
+        } else {
+          for (uint32_t v2 = vt + gridDim.x; v2 < n_vt; v2 += gridDim.x) {
+            int l2, h2;
+            range(v2, l2, h2);
+            if (l2 < h2) {
+              nxt = fix_stream_of<ELEM>(L, jobs, v2 / split);
+              break;
+            }
+          }
         }
       }
       FixItem w[kFixPer];
 #pragma unroll
       for (int j = 0; j < kFixPer; ++j) {
         const int e = e0 + j * kFixThreads + tid;
-        const uint64_t item = e < e_hi ? items[e] : 0ull;
-        w[j].row = e < e_hi ? (int)(item & 0xFF) : -1;
+        const uint64_t item = e < e_hi ? __ldg(items + e) : 0ull;
+        w[j].row = e < e_hi ? (int)(item & 0xFF) : -1;  // (0..255: the super-tile row)
         w[j].nc = (int)((item >> 8) & 0xFF);
-        bool ok = e < e_hi && (ELEM == kTcE4M3 || a_fma_safe(L, jb.a_row0 + mt * kTcBM + w[j].row));
+        w[j].fma = (item & kFixItemFma) != 0;
 #pragma unroll
         for (int c = 0; c < kFixCols; ++c) {
           // missing columns of a short item repeat its first (results unused)
-          w[j].col[c] = c < w[j].nc ? (int)((item >> (16 + 12 * c)) & 0xFFF) : (int)((item >> 16) & 0xFFF);
+          w[j].col[c] = c < w[j].nc ? (int)((item >> (16 + 12 * c)) & 0x7FF) : (int)((item >> 16) & 0x7FF);
           w[j].acc[c] = 0.f;
-          if (ELEM == kTcBF16 && c < w[j].nc) ok = ok && fma_safe(jb.b_norm[nt * kTcBN + w[j].col[c]]);
         }
-        w[j].fma = ok;
       }
-      if (cpi == 1) fix_round<ELEM, 1>(L, w, sA, sB, full, empty, nk, kbytes, arow, brow, jb.b_k0, ld, it);
-      else if (cpi == 2) fix_round<ELEM, 2>(L, w, sA, sB, full, empty, nk, kbytes, arow, brow, jb.b_k0, ld, it);
-      else fix_round<ELEM, kFixCols>(L, w, sA, sB, full, empty, nk, kbytes, arow, brow, jb.b_k0, ld, it);
+      if (cpi == 1) fix_round<ELEM, 1>(L, w, sA, sB, full, empty, cur, nxt, nxt_issued, kbytes, ld, it);
+      else if (cpi == 2) fix_round<ELEM, 2>(L, w, sA, sB, full, empty, cur, nxt, nxt_issued, kbytes, ld, it);
+      else fix_round<ELEM, kFixCols>(L, w, sA, sB, full, empty, cur, nxt, nxt_issued, kbytes, ld, it);
 #pragma unroll
       for (int j = 0; j < kFixPer; ++j) {
-        if (w[j].row < 0) continue;
+        if (w[j].row < 0 || L.fix_dry) continue;  // (timing experiments store nothing)
 #pragma unroll
         for (int c = 0; c < kFixCols; ++c) {
           if (c >= w[j].nc) continue;
@@ -979,7 +1105,6 @@ __global__ void __launch_bounds__(kFixThreads, 1)
         }
       }
     }
-    __syncthreads();  // item list reuse
   }
   // The last CTA to finish clears the listed tiles' marks and the count for
   // the next launch (fix_count[1] counts finished CTAs).
@@ -1454,13 +1579,31 @@ void launch_gemm_tc(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
 
 void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) {
   if (L.total_tiles <= 0) return;
-  const int grid = std::min(L.total_tiles * kFixMaxSplit, 148);
+  const int units = L.fix_g == 2 ? L.n_fix_st : L.total_tiles;  // (g 1: an upper bound)
+  if (units <= 0) return;
+  // item lists of the launch's units
+  if (L.elem == kTcBF16) fix_plan_kernel<kTcBF16><<<std::min(units, 4 * 148), kFixRows, 0, st>>>(L, d_jobs);
+  else fix_plan_kernel<kTcE4M3><<<std::min(units, 4 * 148), kFixRows, 0, st>>>(L, d_jobs);
+  const int grid = std::min(units * kFixMaxSplit, 148);
+  // shared memory of the unit size's ring (a smaller carve-out leaves L1 to the item loads)
+  const int slots = L.fix_g == 2 ? 3 : L_FIX_SLOTS1;
+  const size_t smem = 1024 + (size_t)2 * slots * L.fix_g * kTcBM * kBKBytes + 256 + 1024;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFixSmem);
-    kern<<<grid, kFixThreads, kFixSmem, st>>>(L, d_jobs);
+    kern<<<grid, kFixThreads, smem, st>>>(L, d_jobs);
   };
   if (L.elem == kTcBF16) go(gemm_fixup_kernel<kTcBF16>);
   else go(gemm_fixup_kernel<kTcE4M3>);
+}
+
+std::vector<int4> fixup_super_tiles(const TcJob* jobs, int n_jobs) {
+  std::vector<int4> st;
+  for (int j = 0; j < n_jobs; ++j) {
+    const int tm = (jobs[j].M + kTcBM - 1) / kTcBM, tn = (jobs[j].N + kTcBN - 1) / kTcBN;
+    for (int m = 0; m < tm; m += 2)
+      for (int n = 0; n < tn; n += 2) st.push_back(make_int4(j, m, n, 0));
+  }
+  return st;
 }
 
 std::vector<int4> fixup_chunks(const TcJob* jobs, int n_jobs, int ctas) {

@@ -55,12 +55,18 @@ struct TcLaunch {
                         // valid for the 32 x 64 parts whose bit is set in tile_mark
   uint32_t* fix_tiles;  // [total_tiles] tiles with flagged elements
   uint32_t* tile_mark;  // [total_tiles] flagged-part bits (q + 4*half); zero between launches
+  int fix_g;            // tile-fixup unit: 2 (2 x 2-tile super-tiles, fix_st) or 1 (listed tiles)
+  const int4* fix_st;   // [n_fix_st] the launch's 2 x 2-tile super-tiles {job, row tile, col tile, 0}
+  int n_fix_st;
+  uint64_t* fix_items;  // [units][fix_item_cap(fix_g)] item lists (fix_plan_kernel)
+  uint32_t* fix_n;      // [units] items | columns-per-item << 24 of each unit
   uint32_t* fix_count;  // [0] tiles listed by this launch, [1] fixup CTAs finished (both
                         //   zeroed by the fixup's last CTA),
                         // [2..3] u64 running total of flagged elements,
                         // [4] block-fixup chunk queue (reset by its last CTA)
   float kappa;
   int fix_cpi;  // fixup columns per work item: 0 adaptive, else 1 / 2 / 4
+  int fix_dry;  // timing experiment only: the tile fixup streams and stages but runs no chains
   const int* tile_job;  // [total_tiles] job index of each tile (may be null: binary search)
   const uint16_t* gelu_lut;  // bf16 -> round_bf16(gelu(x)) for all 2^16 inputs
   // block fixup (BF16): SW32 maps of A / B (32-byte K slices x 256 rows) and
@@ -83,6 +89,8 @@ void launch_gemm_fixup_blk(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t 
 // the chunk list of a launch's jobs: 4-row-tile chunks first, then 2, then 1
 // (persistent CTAs take them in order: a balanced tail)
 std::vector<int4> fixup_chunks(const TcJob* jobs, int n_jobs, int ctas);
+// the tile fixup's 2 x 2-tile super-tiles of a launch's jobs (gemm_tc.cu)
+std::vector<int4> fixup_super_tiles(const TcJob* jobs, int n_jobs);
 bool tc_make_map_sw32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols_elems,
                       uint64_t pitch_bytes);
 // lut[b] = enc_bf16(round_bf16(gelu_ref(dec_bf16(b)))) (glibc-exact erff)
@@ -104,5 +112,7 @@ void launch_split_cols(const float* w, int D, int V, uint16_t* out, float* wnorm
 constexpr int kTcBM = 128;
 constexpr int kTcBN = 128;
 constexpr int kFixWords = kTcBM * kTcBN / 32;
+// item capacity of one tile-fixup unit of g x g tiles (= fix_cap in gemm_tc.cu)
+constexpr int fix_item_cap(int g) { return g * kTcBM * g * kTcBN / 4 + g * kTcBM; }
 
 }  // namespace cqg

@@ -182,14 +182,21 @@ def _bf16_grid(x):
 
 @pytest.mark.parametrize("K,M,N,blk", [(768, 256, 256, "1"), (3072, 256, 256, "1"),
                                        (768, 640, 896, "1"), (3072, 136, 768, "1"),
-                                       (768, 256, 256, "0"), (3072, 256, 256, "0")])
+                                       (768, 256, 256, "0"), (3072, 256, 256, "0"),
+                                       (768, 256, 256, "0:2"), (3072, 136, 768, "0:1"),
+                                       (768, 384, 384, "0:0:1"), (3072, 384, 256, "0:0:2")])
 def test_tc_gemm_bitexact_incl_non_fma_rows(K, M, N, blk, monkeypatch):
     """BF16 x BF16 on tcgen05 + certified fixup equals the sequential FP32 dot
     (kernels.cpp:44-52) bit for bit, also for rows holding values whose products
     are not exact in FP32 (|x| < 2^-67: the fixup then keeps fmul + fadd).
     blk: the chunked block fixup (engine option fix_blk; shapes with partial
     chunks and several chunks) or the per-tile fixup (the default)."""
-    monkeypatch.setenv("CQG_DIAG_FIX_BLK", blk)
+    monkeypatch.setenv("CQG_DIAG_FIX_BLK", blk.split(":")[0])
+    if ":" in blk:  # tile fixup: forced columns per item (fix_cpi), unit size (fix_g)
+        f = blk.split(":")
+        monkeypatch.setenv("CQG_DIAG_FIX_CPI", f[1])
+        if len(f) > 2:
+            monkeypatch.setenv("CQG_DIAG_FIX_G", f[2])
     rng = np.random.RandomState(K)
     A = _bf16_grid(rng.randn(M, K).astype(np.float32))
     A[::7, ::5] = _bf16_grid(np.float32(3e-23) * rng.randn(len(range(0, M, 7)), len(range(0, K, 5))))
@@ -349,7 +356,7 @@ MID = formats.ModelConfig(2, 4, 128, 32, 300, 16, 1, 1)
 @pytest.mark.parametrize("opts", [{}, {"packed": 0}, {"exact_x2": 0}, {"fix_cpi": 1},
                                   {"fix_cpi": 2}, {"fix_cpi": 4}, {"exact": 1},
                                   {"kl_fused": 0}, {"fix_blk": 1, "fix_blk_min": 1},
-                                  {"prefetch": 1}])
+                                  {"prefetch": 1}, {"fix_g": 1}, {"fix_g": 2}])
 def test_engine_options_match_oracle(opts):
     w, ds = make(MID, 3, 10, 4)
     p = Port(MID, w.mats)
