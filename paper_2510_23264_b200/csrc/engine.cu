@@ -334,6 +334,8 @@ struct Engine {
   ~Engine() {
     if (comm) nccl().CommDestroy(comm);
     if (h_stage) cudaFreeHost(h_stage);
+    for (cudaEvent_t ev : stage_ev)
+      if (ev) cudaEventDestroy(ev);
     if (st_pf) cudaStreamSynchronize(st_pf), cudaStreamDestroy(st_pf);
     if (st) cudaStreamDestroy(st);
   }
@@ -385,18 +387,33 @@ struct Engine {
   // the same launch can wrap (or grow) the ring under an earlier one.
   static size_t up_bytes(size_t n, size_t sz) { return ((std::max<size_t>(n, 1) * sz) + 15) & ~size_t(15); }
 
+  // The staging ring (pinned host + device) of the launches' job lists, in two
+  // halves: when one fills, an event marks the end of the work that reads it
+  // and the other half is reused once its own event has completed (long
+  // done in steady state), so the host never drains the GPU to recycle it.
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  bool stage_ev_set[2] = {false, false};
+  int stage_half = 0;
   void reserve(size_t total) {
-    if (total > stage_cap) {
+    if (2 * total > stage_cap) {
       CK(cudaStreamSynchronize(st));
       if (h_stage) cudaFreeHost(h_stage);
-      stage_cap = std::max<size_t>({total, stage_cap * 2, size_t(16) << 20});
+      stage_cap = std::max<size_t>({4 * total, stage_cap * 2, size_t(64) << 20});
       CK(cudaMallocHost(&h_stage, stage_cap));
       d_stage.ensure(stage_cap);
-      stage_off = 0;
+      stage_off = 0, stage_half = 0, stage_ev_set[0] = stage_ev_set[1] = false;
     }
-    if (stage_off + total > stage_cap) {
-      CK(cudaStreamSynchronize(st));
-      stage_off = 0;
+    const size_t half = stage_cap / 2;
+    if (stage_off + total > (size_t)(stage_half + 1) * half) {
+      if (!stage_ev[0]) {
+        CK(cudaEventCreateWithFlags(&stage_ev[0], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&stage_ev[1], cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(stage_ev[stage_half], st));
+      stage_ev_set[stage_half] = true;
+      stage_half ^= 1;
+      if (stage_ev_set[stage_half]) CK(cudaEventSynchronize(stage_ev[stage_half]));
+      stage_off = (size_t)stage_half * half;
     }
   }
 

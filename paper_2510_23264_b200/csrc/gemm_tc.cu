@@ -719,6 +719,14 @@ __host__ __device__ constexpr int fix_cap(int g) { return g * kTcBM * g * kTcBN 
 __device__ __forceinline__ int fix_n_units(const TcLaunch& L) {
   return L.fix_g == 2 ? L.n_fix_st : (int)*L.fix_count;
 }
+template <int G>
+__device__ __forceinline__ int4 fix_unit_g(const TcLaunch& L, const TcJob* jobs, int i) {
+  if (G == 2) return L.fix_st[i];
+  const int tile = (int)L.fix_tiles[i];
+  const int j = job_of(L, jobs, tile);
+  const int tiles_n = (jobs[j].N + kTcBN - 1) / kTcBN;
+  return make_int4(j, (tile - jobs[j].tile0) / tiles_n, (tile - jobs[j].tile0) % tiles_n, 0);
+}
 __device__ __forceinline__ int4 fix_unit(const TcLaunch& L, const TcJob* jobs, int i) {
   if (L.fix_g == 2) return L.fix_st[i];
   const int tile = (int)L.fix_tiles[i];
@@ -728,8 +736,7 @@ __device__ __forceinline__ int4 fix_unit(const TcLaunch& L, const TcJob* jobs, i
 }
 constexpr size_t kFixSmem = 1024 + (size_t)3 * 2 * kFixStageBytes + 256 + 1024;
 // ring slots and slot size per operand of a unit of g x g tiles (same bytes)
-__device__ __forceinline__ int fix_slots(int g) { return g == 2 ? 3 : L_FIX_SLOTS1; }
-__device__ __forceinline__ int fix_slot_bytes(int g) { return g * kTcBM * kBKBytes; }
+template <int G> constexpr int kFixSlots = G == 2 ? 3 : L_FIX_SLOTS1;
 
 // A row's norm carries a sign bit when the row holds a value whose products
 // might not be exact in FP32 (rownorm_kernel); otherwise fl(s + fl(a*b)) ==
@@ -825,19 +832,20 @@ struct FixStream {
   int valid, arow, brow, bk0, nk, g;  // g: 128-row boxes per operand
 };
 
-template <int ELEM>
+template <int ELEM, int G>
 __device__ __forceinline__ void fix_issue(const TcLaunch& L, uint8_t* sA, uint8_t* sB, uint64_t* full,
                                           uint64_t* empty, uint32_t& ld, const FixStream& f, int kb) {
   constexpr int bke = kBKBytes / (ELEM == kTcBF16 ? 2 : 1);
-  const int ns = fix_slots(f.g);
+  constexpr int ns = kFixSlots<G>, sb = G * kTcBM * kBKBytes;
   const int s = ld % ns;
   mbar_wait(&empty[s], ((ld / ns) & 1) ^ 1);
-  mbar_expect_tx(&full[s], 2 * f.g * kTcBM * kBKBytes);
-  uint8_t* a = sA + s * fix_slot_bytes(f.g);
-  uint8_t* b = sB + s * fix_slot_bytes(f.g);
-  // g 128-row boxes per operand: row r of the unit sits at r * 128 B (past a
+  mbar_expect_tx(&full[s], 2 * sb);
+  uint8_t* a = sA + s * sb;
+  uint8_t* b = sB + s * sb;
+  // G 128-row boxes per operand: row r of the unit sits at r * 128 B (past a
   // job's or tensor's last row: unused rows / TMA zero fill)
-  for (int h = 0; h < f.g; ++h) {
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
     tma_load_2d(a + h * kTcBM * kBKBytes, &L.tmA, &full[s], kb * bke, f.arow + h * kTcBM);
     tma_load_2d(b + h * kTcBN * kBKBytes, &L.tmB, &full[s], f.bk0 + kb * bke, f.brow + h * kTcBN);
   }
@@ -848,18 +856,18 @@ __device__ __forceinline__ void fix_issue(const TcLaunch& L, uint8_t* sA, uint8_
 // The producer (thread 0) keeps the ring full across rounds: once the current
 // stream's stages are all issued it issues the next round's (nxt), so the
 // next tile's first stages arrive while this round's chains finish.
-template <int ELEM, int CPI>
+template <int ELEM, int G, int CPI>
 __device__ __forceinline__ void fix_round(const TcLaunch& L, FixItem (&w)[kFixPer], uint8_t* sA,
                                           uint8_t* sB, uint64_t* full, uint64_t* empty,
                                           const FixStream& cur, const FixStream& nxt, int& nxt_issued,
                                           int kbytes, uint32_t& ld, uint32_t& it) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int nk = cur.nk;
+  constexpr int ns = kFixSlots<G>, sb = G * kTcBM * kBKBytes;
   for (int kb = 0; kb < nk; ++kb, ++it) {
-    const int ns = fix_slots(cur.g);
     const int s = it % ns;
     if (L.fix_dry != 2) mbar_wait(&full[s], (it / ns) & 1);
-    const uint32_t a0 = smem_u32(sA + s * fix_slot_bytes(cur.g)), b0 = smem_u32(sB + s * fix_slot_bytes(cur.g));
+    const uint32_t a0 = smem_u32(sA + s * sb), b0 = smem_u32(sB + s * sb);
     const int nu = min(8, (kbytes - kb * kBKBytes) / 16);
 #pragma unroll
     for (int j = 0; j < kFixPer; ++j) {
@@ -873,10 +881,9 @@ __device__ __forceinline__ void fix_round(const TcLaunch& L, FixItem (&w)[kFixPe
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (tid == 0 && L.fix_dry != 2) {
-      const int ns2 = fix_slots(cur.g);
-      if (kb + ns2 < nk) fix_issue<ELEM>(L, sA, sB, full, empty, ld, cur, kb + ns2);
-      else if (nxt.valid && kb + ns2 - nk < nxt.nk && nxt_issued == kb + ns2 - nk) {
-        fix_issue<ELEM>(L, sA, sB, full, empty, ld, nxt, nxt_issued);
+      if (kb + ns < nk) fix_issue<ELEM, G>(L, sA, sB, full, empty, ld, cur, kb + ns);
+      else if (nxt.valid && kb + ns - nk < nxt.nk && nxt_issued == kb + ns - nk) {
+        fix_issue<ELEM, G>(L, sA, sB, full, empty, ld, nxt, nxt_issued);
         ++nxt_issued;
       }
     }
@@ -981,14 +988,14 @@ __global__ void __launch_bounds__(kFixRows) fix_plan_kernel(const __grid_constan
 }
 
 // The stream (geometry) of super-tile si
-template <int ELEM>
+template <int ELEM, int G>
 __device__ __forceinline__ FixStream fix_stream_of(const TcLaunch& L, const TcJob* jobs, uint32_t si) {
-  const int4 sd = fix_unit(L, jobs, (int)si);
+  const int4 sd = fix_unit_g<G>(L, jobs, (int)si);
   const TcJob& jb = jobs[sd.x];
   FixStream f;
   f.valid = 1, f.arow = jb.a_row0 + sd.y * kTcBM, f.brow = jb.b_row0 + sd.z * kTcBN, f.bk0 = jb.b_k0;
   f.nk = (jb.K * (ELEM == kTcBF16 ? 2 : 1) + kBKBytes - 1) / kBKBytes;
-  f.g = L.fix_g;
+  f.g = G;
   return f;
 }
 
@@ -1000,7 +1007,7 @@ __device__ __forceinline__ FixStream fix_stream_of(const TcLaunch& L, const TcJo
 // to kFixCols flagged columns of one row (the A unit is loaded once for all).
 // Where every product is exact in FP32 the chain uses FMA (identical
 // result), for BF16 straight from the packed pairs (FHFMA.BF16).
-template <int ELEM>
+template <int ELEM, int G>
 __global__ void __launch_bounds__(kFixThreads, 1)
     gemm_fixup_kernel(const __grid_constant__ TcLaunch L, const TcJob* __restrict__ jobs) {
   extern __shared__ uint8_t smem_raw[];
@@ -1008,7 +1015,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   // the compiler keeps every derived access in the shared address space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
-  const int ring = fix_slots(L.fix_g) * fix_slot_bytes(L.fix_g);  // bytes per operand
+  constexpr int ring = kFixSlots<G> * G * kTcBM * kBKBytes;  // bytes per operand
   uint8_t* sB = smem + ring;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + ring);
   uint64_t* empty = full + kFixStages;
@@ -1016,7 +1023,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   constexpr int kWarps = kFixThreads / 32;
   const int tid = threadIdx.x;
   if (tid == 0) {
-    for (int s = 0; s < fix_slots(L.fix_g); ++s) {
+    for (int s = 0; s < kFixSlots<G>; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kWarps);
     }
@@ -1028,10 +1035,10 @@ __global__ void __launch_bounds__(kFixThreads, 1)
   // Few super-tiles (small launches): split each one's work items over up to
   // kFixMaxSplit CTAs (each streams the operands; L2 absorbs the repeats) so
   // every SM has work.
-  const uint32_t n_st = (uint32_t)fix_n_units(L);
+  const uint32_t n_st = G == 2 ? (uint32_t)L.n_fix_st : *L.fix_count;
   const uint32_t split = n_st ? min((uint32_t)kFixMaxSplit, max(1u, gridDim.x / n_st)) : 1u;
   const uint32_t n_vt = n_st * split;
-  const int cap = fix_cap(L.fix_g);
+  constexpr int cap = fix_cap(G);
   auto range = [&](uint32_t vt, int& lo, int& hi) {  // item range of virtual tile vt
     const uint32_t n = L.fix_n[vt / split] & 0xFFFFFFu, part = vt % split;
     lo = (int)((uint64_t)n * part / split), hi = (int)((uint64_t)n * (part + 1) / split);
@@ -1045,17 +1052,17 @@ __global__ void __launch_bounds__(kFixThreads, 1)
     if (e_lo >= e_hi) continue;
     const uint32_t ti = vt / split;  // super-tile
     const int cpi = (int)(L.fix_n[ti] >> 24);
-    const int4 sd = fix_unit(L, jobs, (int)ti);
+    const int4 sd = fix_unit_g<G>(L, jobs, (int)ti);
     const TcJob jb = jobs[sd.x];
     const int mt = sd.y, nt = sd.z;  // first row / column tile
-    const FixStream cur = fix_stream_of<ELEM>(L, jobs, ti);
+    const FixStream cur = fix_stream_of<ELEM, G>(L, jobs, ti);
     const int kbytes = jb.K * esz;
     const uint64_t* items = L.fix_items + (size_t)ti * cap;
     for (int e0 = e_lo; e0 < e_hi; e0 += kFixThreads * kFixPer) {
       if (tid == 0 && L.fix_dry != 2) {
         // prologue: the stages of this round the previous round did not issue
-        for (int kb = nxt_issued; kb < min(fix_slots(cur.g), cur.nk); ++kb)
-          fix_issue<ELEM>(L, sA, sB, full, empty, ld, cur, kb);
+        for (int kb = nxt_issued; kb < min(kFixSlots<G>, cur.nk); ++kb)
+          fix_issue<ELEM, G>(L, sA, sB, full, empty, ld, cur, kb);
         nxt_issued = 0;
         // the round after this one: this unit again, or the next non-empty virtual unit
         nxt.valid = 0;
@@ -1066,7 +1073,7 @@ __global__ void __launch_bounds__(kFixThreads, 1)
             int l2, h2;
             range(v2, l2, h2);
             if (l2 < h2) {
-              nxt = fix_stream_of<ELEM>(L, jobs, v2 / split);
+              nxt = fix_stream_of<ELEM, G>(L, jobs, v2 / split);
               break;
             }
           }
@@ -1087,9 +1094,9 @@ __global__ void __launch_bounds__(kFixThreads, 1)
           w[j].acc[c] = 0.f;
         }
       }
-      if (cpi == 1) fix_round<ELEM, 1>(L, w, sA, sB, full, empty, cur, nxt, nxt_issued, kbytes, ld, it);
-      else if (cpi == 2) fix_round<ELEM, 2>(L, w, sA, sB, full, empty, cur, nxt, nxt_issued, kbytes, ld, it);
-      else fix_round<ELEM, kFixCols>(L, w, sA, sB, full, empty, cur, nxt, nxt_issued, kbytes, ld, it);
+      if (cpi == 1) fix_round<ELEM, G, 1>(L, w, sA, sB, full, empty, cur, nxt, nxt_issued, kbytes, ld, it);
+      else if (cpi == 2) fix_round<ELEM, G, 2>(L, w, sA, sB, full, empty, cur, nxt, nxt_issued, kbytes, ld, it);
+      else fix_round<ELEM, G, kFixCols>(L, w, sA, sB, full, empty, cur, nxt, nxt_issued, kbytes, ld, it);
 #pragma unroll
       for (int j = 0; j < kFixPer; ++j) {
         if (w[j].row < 0 || L.fix_dry) continue;  // (timing experiments store nothing)
@@ -1592,8 +1599,13 @@ void launch_gemm_fixup(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t st) 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFixSmem);
     kern<<<grid, kFixThreads, smem, st>>>(L, d_jobs);
   };
-  if (L.elem == kTcBF16) go(gemm_fixup_kernel<kTcBF16>);
-  else go(gemm_fixup_kernel<kTcE4M3>);
+  if (L.elem == kTcBF16) {
+    if (L.fix_g == 2) go(gemm_fixup_kernel<kTcBF16, 2>);
+    else go(gemm_fixup_kernel<kTcBF16, 1>);
+  } else {
+    if (L.fix_g == 2) go(gemm_fixup_kernel<kTcE4M3, 2>);
+    else go(gemm_fixup_kernel<kTcE4M3, 1>);
+  }
 }
 
 std::vector<int4> fixup_super_tiles(const TcJob* jobs, int n_jobs) {
