@@ -10,6 +10,8 @@
 
 #include "gemm_tc.h"
 
+#include <omp.h>
+
 #include <algorithm>
 #include <array>
 #include <chrono>
@@ -338,6 +340,13 @@ struct Engine {
       if (ev) cudaEventDestroy(ev);
     if (st_pf) cudaStreamSynchronize(st_pf), cudaStreamDestroy(st_pf);
     if (st) cudaStreamDestroy(st);
+  }
+
+  // host threads for the per-edge plans: a few (the launching thread must
+  // keep its core; OpenMP workers spin between regions)
+  static int plan_threads() {
+    static const int n = std::max(1, std::min(6, omp_get_num_procs() / 4));
+    return n;
   }
 
   // ---- the next group's FP32 slices into L2 on the side stream (a6) ---------
@@ -1864,8 +1873,20 @@ struct Engine {
         plans[k].e = e, plans[k].s = g.esrc[e], plans[k].v = g.edst[e], plans[k].sv = g.stage[g.edst[e]];
         plans[k].r = g.erecv[e];
         plans[k].pv = patch_value(plans[k].s, policy_for_edge(g, e, base), per_edge, &plans[k].pvt);
-        plan_edge(plans[k], T, loss);
       }
+      // the per-edge plans are independent host work (O(trie) each): on all
+      // host threads, so the host keeps ahead of the GPU on small groups
+      std::string plan_err;
+#pragma omp parallel for schedule(dynamic, 4) num_threads(plan_threads()) if (idx.size() > 32)
+      for (long k = 0; k < (long)idx.size(); ++k) {
+        try {
+          plan_edge(plans[(size_t)k], T, loss);
+        } catch (const std::exception& ex) {
+#pragma omp critical
+          plan_err = ex.what();
+        }
+      }
+      if (!plan_err.empty()) throw Error(2, plan_err);
       std::vector<size_t> ord(idx.size());
       std::iota(ord.begin(), ord.end(), 0);
       std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return plans[a].sv < plans[b].sv; });
