@@ -56,3 +56,22 @@ def test_gpus_flag_self_launches_ranks():
     lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
     assert json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_config_block_reports_samples_and_extensions():
+    """The workload block names what was measured: strided edge samples
+    (configs 4-5 on one GPU), one GPU's item shard, the Q/K/V-split graph and
+    the INT8 extension, so a sampled or extension line cannot pass for the
+    headline workload."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    a = argparse.Namespace(config="pythia", gpus=1, items=64, qkv_split=True, low="int8")
+    c = bench.config_block(a, 80965, 1500)
+    assert c["edges_sampled"] == {"scored": 1500, "of": 80965}
+    assert c["items"] == 64 and "items_note" in c
+    assert "Q/K/V-split" in c["edges"] and c["low_precision"].startswith("int8")
+    a = argparse.Namespace(config="gpt2s", gpus=1, items=0, qkv_split=False, low="e4m3")
+    c = bench.config_block(a, 11611, 11611)
+    assert "edges_sampled" not in c and c["items"] == 64 and "every edge" in c["workload"]
+    assert bench.CONFIGS["pythia"]["cfg"].d_k == 128 and bench.CONFIGS["pythia"]["cfg"].seq_len == 32

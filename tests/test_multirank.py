@@ -14,7 +14,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from oracle.oracle import KL, LOGITDIFF, Policy, Port
+from oracle.oracle import INT8, KL, LOGITDIFF, Policy, Port
 from paper_2510_23264_b200 import shard
 from helpers import SMALL, TOY, make
 
@@ -29,16 +29,16 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cfg, items, metric, out_path):
+def _worker(rank, world, port, cfg, items, metric, out_path, split=False, mode=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         w, ds = make(cfg, 1, items, 2)
-        p = Port(cfg, w.mats)
+        p = Port(cfg, w.mats, qkv_split=split)
         lo, hi = shard.item_block(rank, world, items)
         edges = p.sweep_order()
         part = shard.partial_sums(
-            p.score_edges(ds.subset(list(range(lo, hi))), edges, Policy.head_quantized(),
+            p.score_edges(ds.subset(list(range(lo, hi))), edges, Policy.head_quantized(mode=mode),
                           True, metric), hi - lo)
         t = torch.from_numpy(part)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -61,14 +61,17 @@ def test_item_block_partition():
         shard.item_block(2, 2, 4)
 
 
-@pytest.mark.parametrize("cfg,items,metric", [(SMALL, 5, KL), (TOY, 4, KL), (SMALL, 4, LOGITDIFF)])
-def test_two_rank_scores_match_single(tmp_path, cfg, items, metric):
+@pytest.mark.parametrize("cfg,items,metric,split,mode", [
+    (SMALL, 5, KL, False, 0), (TOY, 4, KL, False, 0), (SMALL, 4, LOGITDIFF, False, 0),
+    # the extensions shard the same way: Q/K/V-split graph, INT8 low precision
+    (SMALL, 4, KL, True, 0), (TOY, 3, KL, False, INT8)])
+def test_two_rank_scores_match_single(tmp_path, cfg, items, metric, split, mode):
     out = str(tmp_path / "combined.npy")
-    mp.start_processes(_worker, args=(2, _free_port(), cfg, items, metric, out), nprocs=2,
+    mp.start_processes(_worker, args=(2, _free_port(), cfg, items, metric, out, split, mode), nprocs=2,
                        join=True, start_method="spawn")
     combined = np.load(out)
     w, ds = make(cfg, 1, items, 2)
-    p = Port(cfg, w.mats)
-    full = p.score_edges(ds, p.sweep_order(), Policy.head_quantized(), True, metric)
+    p = Port(cfg, w.mats, qkv_split=split)
+    full = p.score_edges(ds, p.sweep_order(), Policy.head_quantized(mode=mode), True, metric)
     assert combined.shape == full.shape
     np.testing.assert_allclose(combined, full, rtol=RTOL, atol=1e-300)
