@@ -21,7 +21,7 @@ constexpr int kStages = 4;
 constexpr int kBKBytes = 128;  // one SW128 atom row
 constexpr int kAStage = kTcBM * kBKBytes;  // 16 KB
 constexpr int kBStage = kTcBN * kBKBytes;  // 16 KB
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;  // 4 per TMEM lane quarter, one 32-column chunk each
 constexpr int kEpiWarp0 = 3;  // warps: 0 TMA, 1 MMA, 2 tile metadata, 3.. epilogue
 constexpr int kThreads = 32 * kEpiWarp0 + 32 * kEpiWarps;
 constexpr size_t kStageFloats = 32 * 36;  // per epilogue warp store staging
@@ -261,10 +261,177 @@ __device__ __forceinline__ uint32_t gelu_code(uint32_t c, const uint16_t* lut_s,
   return r;
 }
 
-// Epilogue of one tile for one warp: 32 TMEM lanes (rows) x 64 columns.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+      "[%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Per-lane state of one epilogue chunk (32 rows x 32 columns of a tile).
+struct EpiRow {
+  float oss;      // sum of squares of the stored outputs (out_ss)
+  bool obad;      // a stored output is not FMA-safe
+};
+
+// 16 columns [c0, c0 + 16) of the warp's chunk: TMEM -> rounding ->
+// certificate flags (returned, bit j = column c0 + j) -> GELU -> out_ss;
+// FP32 values to the staging row (stage, when the job stores FP32) and the
+// packed codes to pk (BF16: 8 words, E4M3: 4 words).
+template <int ELEM, int PREC, int EPI>
+__device__ __forceinline__ uint32_t epilogue16(const TcLaunch& L, const TileMeta& md, uint32_t tacc, int q,
+                                               int c0, int ncol, bool rvalid, float na, float sk, float ku,
+                                               bool two, float* srow, uint32_t* pk, EpiRow& st,
+                                               const uint16_t* gelu_s) {
+  const TcJob& jb = md.jb;
+  constexpr int kSplitE = split_of(ELEM, PREC);
+  uint32_t r[16];
+  tmem_ld16(tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
+  // split accumulation: r = first-half sum, r2 = second half; acc = r + r2,
+  // and |first half| joins the margin's scale (h1)
+  float h1[kSplitE == 2 ? 16 : 1];
+  if (kSplitE == 2) {
+    if (two) {
+      uint32_t r2[16];
+      tmem_ld16(tacc + kTcBN + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r2);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        h1[j] = fabsf(__uint_as_float(r[j]));
+        r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) h1[j] = 0.f;
+    }
+  }
+  uint32_t fl = 0;
+  float v[16];
+  bool have_codes = false;
+  // E4M3 x E4M3 products are multiples of 2^-18; if every partial sum is
+  // below 2^6 (|s_k| <= ||a|| ||b||) all of them are exact in FP32, so the
+  // reference's sequential sum is the exact sum and so is the tensor-core
+  // sum: the rounding is certified without a fixup. Checked for the whole
+  // warp chunk at once (uniform branch) with the chunk's largest column norm.
+  const bool cert_all = ELEM == kTcE4M3 && PREC == 0 &&
+                        __all_sync(0xffffffffu, na * md.nbmax[c0 >> 5] < 63.99f);
+  if (PREC == 0 && cert_all) {
+#pragma unroll
+    for (int j = 0; j < 16; j += 4)
+      pk[j >> 2] = e4m3x2_code(__uint_as_float(r[j]), __uint_as_float(r[j + 1])) |
+                   (e4m3x2_code(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])) << 16);
+    have_codes = true;
+    if (jb.out_f32 || EPI == 1 || L.out_ss) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        const float2 x = e4m3x2_value(pk[j >> 2] & 0xFFFFu), y = e4m3x2_value(pk[j >> 2] >> 16);
+        v[j] = x.x, v[j + 1] = x.y, v[j + 2] = y.x, v[j + 3] = y.y;
+      }
+    }
+  } else if (PREC == 1 && ncol > 0) {
+    // BF16: RNE by integer add, certificate in integer form
+    const float nas = na / sk;
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {
+      const float4 t4 = *reinterpret_cast<const float4*>(md.nb + c0 + j);
+      const float nb4[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float acc = __uint_as_float(r[j + t]);
+        v[j + t] = round_bf16(acc);
+        float sc = fabsf(acc);
+        if (kSplitE == 2) sc = fmaxf(sc, h1[(j + t) & (kSplitE == 2 ? 15 : 0)]);
+        const float m = ku * fmaxf(sc, nas * nb4[t]);
+        if (bf16_ambiguous(acc, m)) fl |= 1u << (j + t);
+      }
+    }
+    if (!rvalid) fl = 0;
+    if (ncol < 16) fl &= (1u << max(ncol, 0)) - 1u;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) round_pair<PREC>(v[j], v[j + 1]);
+    if (PREC != 2 && ncol > 0) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        float lo[2], hi[2];
+        bool chk[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const float nb = md.nb[c0 + j + t];  // (uniform: broadcast shared loads)
+          const float acc = __uint_as_float(r[j + t]);
+          chk[t] = !(ELEM == kTcE4M3 && na * nb < 63.99f);
+          const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
+          lo[t] = acc - m, hi[t] = acc + m;
+          if (!(acc == acc)) fl |= 1u << (j + t);
+        }
+        if (chk[0] || chk[1]) {
+          round_pair<PREC>(lo[0], lo[1]);
+          round_pair<PREC>(hi[0], hi[1]);
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+            if (chk[t] && !(lo[t] == hi[t])) fl |= 1u << (j + t);
+        }
+      }
+      if (!rvalid) fl = 0;
+      if (ncol < 16) fl &= (1u << max(ncol, 0)) - 1u;
+    }
+  }
+  if (EPI == 1 && ncol > 0) {
+    if (PREC == 1) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        v[j] = __uint_as_float(gelu_code(__float_as_uint(v[j]) >> 16, gelu_s, L.gelu_lut) << 16);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = round_out(gelu_ref(v[j]), PREC);
+      have_codes = false;
+    }
+  }
+  if (L.out_ss && ncol > 0 && rvalid) {
+    // (columns >= ncol hold zero-padded accumulators: they add nothing)
+    uint32_t ebad = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      // a flagged element is recomputed later: bound |final| by the
+      // neighbouring rounding candidates (GELU is 1.13-Lipschitz)
+      const float vb = (fl >> j) & 1u ? fabsf(v[j]) + 0.02f * fabsf(__uint_as_float(r[j])) : v[j];
+      st.oss = fmaf(vb, vb, st.oss);
+      // not FMA-safe: nonzero |v| outside [2^-67, 2^64)
+      const uint32_t ab = __float_as_uint(v[j]) & 0x7FFFFFFFu;
+      ebad |= (uint32_t)(ab - (60u << 23) >= (131u << 23)) & (uint32_t)(ab != 0u);
+    }
+    st.obad = st.obad || ebad != 0;
+  }
+  if (jb.out_f32) {
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(srow + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+  }
+  if (jb.out_pack) {
+    if (PREC == 1) {
+#pragma unroll
+      for (int w = 0; w < 8; ++w)
+        pk[w] = (__float_as_uint(v[2 * w]) >> 16) | (__float_as_uint(v[2 * w + 1]) & 0xFFFF0000u);
+    } else if (!have_codes) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        pk[w] = enc_e4m3(v[4 * w]) | ((uint32_t)enc_e4m3(v[4 * w + 1]) << 8) |
+                ((uint32_t)enc_e4m3(v[4 * w + 2]) << 16) | ((uint32_t)enc_e4m3(v[4 * w + 3]) << 24);
+    }
+  }
+  return fl;
+}
+
+// Epilogue of one tile for one warp: 32 TMEM lanes (rows) x 32 columns
+// (column chunk cq of the tile), in two 16-column halves (registers: 16
+// epilogue warps share the SM's register file).
 template <int ELEM, int PREC, int EPI>
 __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TileMeta& md, int tile,
-                                              uint32_t tacc, int q, int half, int lane, float* stage,
+                                              uint32_t tacc, int q, int cq, int lane, float* stage,
                                               const uint16_t* gelu_s) {
   const TcJob& jb = md.jb;
   const int mt = md.mt, nt = md.nt;
@@ -272,246 +439,98 @@ __device__ __forceinline__ void epilogue_tile(const TcLaunch& L, const TileMeta&
   const bool rvalid = row < jb.M;
   const float sk = sqrtf((float)jb.K);
   const float na = md.na[q * 32 + lane];
-  float oss = 0.f;  // sum of squares of this lane's stored outputs (out_ss)
-  bool obad = false;
   const float ku = L.kappa * 5.9604644775390625e-08f * sk;
   const int row0 = mt * kTcBM + q * 32;
   const int nrow = min(32, jb.M - row0);
-  uint32_t flagged0 = 0, flagged1 = 0;
   constexpr int kSplitE = split_of(ELEM, PREC);
   // the second accumulator exists when K spans at least two k-blocks
   const bool two = kSplitE == 2 && (jb.K * (ELEM == kTcBF16 ? 2 : 1) + kBKBytes - 1) / kBKBytes >= 2;
-  // one 32-column chunk per iteration, not unrolled: the epilogue body is
-  // large and the unrolled pair thrashed the instruction cache
-#pragma unroll 1
-  for (int cc = 0; cc < 2; ++cc) {
-    const int c0 = half * 64 + cc * 32;
-    uint32_t r[32];
-    tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
-    // split accumulation: r = first-half sum, r2 = second half; acc = r + r2,
-    // and |first half| joins the margin's scale (h1)
-    float h1[kSplitE == 2 ? 32 : 1];
-    if (kSplitE == 2) {
-      if (two) {
-        uint32_t r2[32];
-        tmem_ld32(tacc + kTcBN + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r2);
+  const int c0 = cq * 32;
+  const int colb = nt * kTcBN + c0;
+  const int ncol = min(32, jb.N - colb);
+  EpiRow st{0.f, false};
+  uint32_t pk[16];  // packed output codes of the 32 columns (BF16: 16 words, E4M3: 8)
+  constexpr int hw = PREC == 1 ? 8 : 4;  // packed words per 16 columns
+  uint32_t fl = epilogue16<ELEM, PREC, EPI>(L, md, tacc, q, c0, ncol, rvalid, na, sk, ku, two,
+                                            stage + lane * 36, pk, st, gelu_s);
+  fl |= epilogue16<ELEM, PREC, EPI>(L, md, tacc, q, c0 + 16, ncol - 16, rvalid, na, sk, ku, two,
+                                    stage + lane * 36 + 16, pk + hw, st, gelu_s) << 16;
+  // Stores: the 32 x 32 block is transposed through a warp-private smem
+  // tile with 16-byte accesses (row pitch padded by 4 words: conflict-free),
+  // then written as whole row segments with 16-byte global stores.
+  if (ncol > 0) {
+    uint32_t* sw = reinterpret_cast<uint32_t*>(stage);
+    if (jb.out_f32) {
+      __syncwarp();
+      const bool vec = ncol == 32 && ((reinterpret_cast<uintptr_t>(jb.out_f32) & 15) == 0) && (jb.ldo & 3) == 0;
+      if (vec) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          h1[j] = fabsf(__uint_as_float(r[j]));
-          r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
+        for (int it = 0; it < 8; ++it) {
+          const int rr = it * 4 + (lane >> 3), cw = (lane & 7) * 4;
+          if (rr < nrow)
+            *reinterpret_cast<float4*>(jb.out_f32 + (int64_t)(row0 + rr) * jb.ldo + colb + cw) =
+                *reinterpret_cast<const float4*>(stage + rr * 36 + cw);
         }
       } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) h1[j] = 0.f;
+        float* dst = jb.out_f32 + (int64_t)row0 * jb.ldo + colb + lane;
+        for (int rr = 0; rr < nrow; ++rr)
+          if (lane < ncol) dst[(int64_t)rr * jb.ldo] = stage[rr * 36 + lane];
       }
+      __syncwarp();
     }
-    uint32_t fl = 0;
-    const int colb = nt * kTcBN + c0;
-    const int ncol = min(32, jb.N - colb);
-    float v[32];
-    uint32_t e8[8];  // E4M3 codes (PREC 0 fast path), 4 per word
-    bool have_codes = false;
-    // E4M3 x E4M3 products are multiples of 2^-18; if every partial sum is
-    // below 2^6 (|s_k| <= ||a|| ||b||) all of them are exact in FP32, so the
-    // reference's sequential sum is the exact sum and so is the tensor-core
-    // sum: the rounding is certified without a fixup. Checked for the whole
-    // warp chunk at once (uniform branch) with the chunk's largest column norm.
-    const bool cert_all = ELEM == kTcE4M3 && PREC == 0 &&
-                          __all_sync(0xffffffffu, na * md.nbmax[c0 >> 5] < 63.99f);
-    if (PREC == 0 && cert_all) {
+    if (jb.out_pack) {
+      constexpr int esz = PREC == 1 ? 2 : 1;
+      constexpr int words = 32 * esz / 4;  // per row: 16 (bf16) or 8 (e4m3)
+      constexpr int pitch = words + 4;
+      uint8_t* base = reinterpret_cast<uint8_t*>(jb.out_pack);
+      const bool vec = ncol == 32 && ((reinterpret_cast<uintptr_t>(base) & 15) == 0) &&
+                       ((int64_t)jb.ldo * esz) % 16 == 0 && (colb * esz) % 16 == 0;
+      if (vec) {
 #pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        e8[j >> 2] = e4m3x2_code(__uint_as_float(r[j]), __uint_as_float(r[j + 1])) |
-                     (e4m3x2_code(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])) << 16);
-      have_codes = true;
-      if (jb.out_f32 || EPI == 1 || L.out_ss) {
+        for (int w = 0; w < words; w += 4)
+          *reinterpret_cast<uint4*>(sw + lane * pitch + w) = make_uint4(pk[w], pk[w + 1], pk[w + 2], pk[w + 3]);
+        __syncwarp();
+        constexpr int lanes_per_row = words / 4;  // 4 (bf16) or 2 (e4m3)
+        constexpr int rows_per_it = 32 / lanes_per_row;
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          const float2 x = e4m3x2_value(e8[j >> 2] & 0xFFFFu), y = e4m3x2_value(e8[j >> 2] >> 16);
-          v[j] = x.x, v[j + 1] = x.y, v[j + 2] = y.x, v[j + 3] = y.y;
+        for (int it = 0; it < 32 / rows_per_it; ++it) {
+          const int rr = it * rows_per_it + lane / lanes_per_row, cw = (lane % lanes_per_row) * 4;
+          if (rr < nrow)
+            *reinterpret_cast<uint4*>(base + ((int64_t)(row0 + rr) * jb.ldo + colb) * esz + cw * 4) =
+                *reinterpret_cast<const uint4*>(sw + rr * pitch + cw);
         }
-      }
-    } else if (PREC == 1 && ncol > 0) {
-      // BF16: RNE by integer add, certificate in integer form
-      const float nas = na / sk;
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        const float4 t4 = *reinterpret_cast<const float4*>(md.nb + c0 + j);
-        const float nb4[4] = {t4.x, t4.y, t4.z, t4.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const float acc = __uint_as_float(r[j + t]);
-          v[j + t] = round_bf16(acc);
-          float sc = fabsf(acc);
-          if (kSplitE == 2) sc = fmaxf(sc, h1[(j + t) & (kSplitE == 2 ? 31 : 0)]);
-          const float m = ku * fmaxf(sc, nas * nb4[t]);
-          if (bf16_ambiguous(acc, m)) fl |= 1u << (j + t);
-        }
-      }
-      if (!rvalid) fl = 0;
-      if (ncol < 32) fl &= (1u << ncol) - 1u;
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) round_pair<PREC>(v[j], v[j + 1]);
-      if (PREC != 2 && ncol > 0) {
-        float nbv[32];  // uniform across the warp: broadcast shared loads
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          const float4 t4 = *reinterpret_cast<const float4*>(md.nb + c0 + j);
-          nbv[j] = t4.x, nbv[j + 1] = t4.y, nbv[j + 2] = t4.z, nbv[j + 3] = t4.w;
-        }
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          float lo[2], hi[2];
-          bool chk[2];
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            const float nb = nbv[j + t];
-            const float acc = __uint_as_float(r[j + t]);
-            chk[t] = !(ELEM == kTcE4M3 && na * nb < 63.99f);
-            const float m = ku * fmaxf(fabsf(acc), na * nb / sk);
-            lo[t] = acc - m, hi[t] = acc + m;
-            if (!(acc == acc)) fl |= 1u << (j + t);
-          }
-          if (chk[0] || chk[1]) {
-            round_pair<PREC>(lo[0], lo[1]);
-            round_pair<PREC>(hi[0], hi[1]);
-#pragma unroll
-            for (int t = 0; t < 2; ++t)
-              if (chk[t] && !(lo[t] == hi[t])) fl |= 1u << (j + t);
-          }
-        }
-        if (!rvalid) fl = 0;
-        if (ncol < 32) fl &= (1u << ncol) - 1u;
-      }
-    }
-    if (EPI == 1 && ncol > 0) {
-      if (PREC == 1) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          v[j] = __uint_as_float(gelu_code(__float_as_uint(v[j]) >> 16, gelu_s, L.gelu_lut) << 16);
+        __syncwarp();
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = round_out(gelu_ref(v[j]), PREC);
-        have_codes = false;
+        for (int w = 0; w < words; ++w) sw[lane * (words + 1) + w] = pk[w];
+        __syncwarp();
+        for (int rr = 0; rr < nrow; ++rr) {
+          if (lane < ncol) {
+            const uint32_t wv = sw[rr * (words + 1) + lane * esz / 4];
+            const int64_t o = (int64_t)(row0 + rr) * jb.ldo + colb + lane;
+            if (PREC == 1) reinterpret_cast<uint16_t*>(base)[o] = (uint16_t)(wv >> (16 * (lane & 1)));
+            else base[o] = (uint8_t)(wv >> (8 * (lane & 3)));
+          }
+        }
+        __syncwarp();
       }
     }
-    if (L.out_ss && ncol > 0 && rvalid) {
-      // (columns >= ncol hold zero-padded accumulators: they add nothing)
-      uint32_t ebad = 0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        // a flagged element is recomputed later: bound |final| by the
-        // neighbouring rounding candidates (GELU is 1.13-Lipschitz)
-        const float vb = (fl >> j) & 1u ? fabsf(v[j]) + 0.02f * fabsf(__uint_as_float(r[j])) : v[j];
-        oss = fmaf(vb, vb, oss);
-        // not FMA-safe: nonzero |v| outside [2^-67, 2^64)
-        const uint32_t ab = __float_as_uint(v[j]) & 0x7FFFFFFFu;
-        ebad |= (uint32_t)(ab - (60u << 23) >= (131u << 23)) & (uint32_t)(ab != 0u);
-      }
-      obad = obad || ebad != 0;
-    }
-    // Stores: the 32 x 32 block is transposed through a warp-private smem
-    // tile with 16-byte accesses (row pitch padded by 4 words: conflict-free),
-    // then written as whole row segments with 16-byte global stores.
-    if (ncol > 0) {
-      uint32_t* sw = reinterpret_cast<uint32_t*>(stage);
-      if (jb.out_f32) {
-        const bool vec = ncol == 32 && ((reinterpret_cast<uintptr_t>(jb.out_f32) & 15) == 0) && (jb.ldo & 3) == 0;
-        if (vec) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(stage + lane * 36 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          __syncwarp();
-#pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int rr = it * 4 + (lane >> 3), cw = (lane & 7) * 4;
-            if (rr < nrow)
-              *reinterpret_cast<float4*>(jb.out_f32 + (int64_t)(row0 + rr) * jb.ldo + colb + cw) =
-                  *reinterpret_cast<const float4*>(stage + rr * 36 + cw);
-          }
-          __syncwarp();
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = v[j];
-          __syncwarp();
-          float* dst = jb.out_f32 + (int64_t)row0 * jb.ldo + colb + lane;
-          for (int rr = 0; rr < nrow; ++rr)
-            if (lane < ncol) dst[(int64_t)rr * jb.ldo] = stage[rr * 33 + lane];
-          __syncwarp();
-        }
-      }
-      if (jb.out_pack) {
-        constexpr int esz = PREC == 1 ? 2 : 1;
-        constexpr int words = 32 * esz / 4;  // per row: 16 (bf16) or 8 (e4m3)
-        constexpr int pitch = words + 4;
-        uint32_t pk[words];
-#pragma unroll
-        for (int w = 0; w < words; ++w) {
-          if (PREC == 1)
-            pk[w] = (__float_as_uint(v[2 * w]) >> 16) | (__float_as_uint(v[2 * w + 1]) & 0xFFFF0000u);
-          else if (have_codes)
-            pk[w] = e8[w];
-          else
-            pk[w] = enc_e4m3(v[4 * w]) | ((uint32_t)enc_e4m3(v[4 * w + 1]) << 8) |
-                    ((uint32_t)enc_e4m3(v[4 * w + 2]) << 16) | ((uint32_t)enc_e4m3(v[4 * w + 3]) << 24);
-        }
-        uint8_t* base = reinterpret_cast<uint8_t*>(jb.out_pack);
-        const bool vec = ncol == 32 && ((reinterpret_cast<uintptr_t>(base) & 15) == 0) &&
-                         ((int64_t)jb.ldo * esz) % 16 == 0 && (colb * esz) % 16 == 0;
-        if (vec) {
-#pragma unroll
-          for (int w = 0; w < words; w += 4)
-            *reinterpret_cast<uint4*>(sw + lane * pitch + w) = make_uint4(pk[w], pk[w + 1], pk[w + 2], pk[w + 3]);
-          __syncwarp();
-          constexpr int lanes_per_row = words / 4;  // 4 (bf16) or 2 (e4m3)
-          constexpr int rows_per_it = 32 / lanes_per_row;
-#pragma unroll
-          for (int it = 0; it < 32 / rows_per_it; ++it) {
-            const int rr = it * rows_per_it + lane / lanes_per_row, cw = (lane % lanes_per_row) * 4;
-            if (rr < nrow)
-              *reinterpret_cast<uint4*>(base + ((int64_t)(row0 + rr) * jb.ldo + colb) * esz + cw * 4) =
-                  *reinterpret_cast<const uint4*>(sw + rr * pitch + cw);
-          }
-          __syncwarp();
-        } else {
-#pragma unroll
-          for (int w = 0; w < words; ++w) sw[lane * (words + 1) + w] = pk[w];
-          __syncwarp();
-          for (int rr = 0; rr < nrow; ++rr) {
-            if (lane < ncol) {
-              const uint32_t wv = sw[rr * (words + 1) + lane * esz / 4];
-              const int64_t o = (int64_t)(row0 + rr) * jb.ldo + colb + lane;
-              if (PREC == 1) reinterpret_cast<uint16_t*>(base)[o] = (uint16_t)(wv >> (16 * (lane & 1)));
-              else base[o] = (uint8_t)(wv >> (8 * (lane & 3)));
-            }
-          }
-          __syncwarp();
-        }
-      }
-    }
-    if (cc == 0) flagged0 = fl;
-    else flagged1 = fl;
   }
-  const uint32_t flagged[2] = {flagged0, flagged1};
   if (L.out_ss && rvalid) {
-    atomicAdd(L.out_ss + jb.a_row0 + row, oss);
-    if (obad) atomicOr(L.out_bad + jb.a_row0 + row, 1u);
+    atomicAdd(L.out_ss + jb.a_row0 + row, st.oss);
+    if (st.obad) atomicOr(L.out_bad + jb.a_row0 + row, 1u);
   }
-  // Record the flagged bits of this warp's 32 x 64 part; the first part of a
-  // tile to flag anything lists the tile for the fixup kernel.
-  const int cnt = __popc(flagged[0]) + __popc(flagged[1]);
-  if (!__any_sync(0xffffffffu, cnt != 0)) return;
-  *reinterpret_cast<uint2*>(L.fix_mask + (size_t)tile * kFixWords + (q * 32 + lane) * 4 + half * 2) =
-      make_uint2(flagged[0], flagged[1]);
-  int total = cnt;
+  // Record the flagged bits of this warp's 32 x 32 part (word cq of each row;
+  // part bit q + 4 cq); the first part of a tile to flag anything lists the
+  // tile for the fixup kernel.
+  if (!__any_sync(0xffffffffu, fl != 0)) return;
+  L.fix_mask[(size_t)tile * kFixWords + (q * 32 + lane) * 4 + cq] = fl;
+  int total = __popc(fl);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
   if (lane == 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(L.fix_count + 2), (unsigned long long)total);
-    if (atomicOr(L.tile_mark + tile, 1u << (q + 4 * half)) == 0u)
+    if (atomicOr(L.tile_mark + tile, 1u << (q + 4 * cq)) == 0u)
       L.fix_tiles[atomicAdd(L.fix_count, 1u)] = (uint32_t)tile;
   }
 }
@@ -656,8 +675,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_arrive(&mfull[b]);  // count 32: every lane's stores are released
     }
-  } else {  // epilogue warps: lanes quarter (warp % 4), column half
-    const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
+  } else {  // epilogue warps: lanes quarter (warp % 4), 32-column chunk
+    const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;  // (half: the chunk index cq)
     uint32_t ti = 0;
     for (int tile = blockIdx.x; tile < L.total_tiles; tile += gridDim.x, ++ti) {
       const uint32_t b = ti % kBufs, bph = (ti / kBufs) & 1;
@@ -919,10 +938,11 @@ __global__ void __launch_bounds__(kFixRows) fix_plan_kernel(const __grid_constan
         parts = L.tile_mark[tile];
         if (parts) m = *reinterpret_cast<const uint4*>(L.fix_mask + (size_t)tile * kFixWords + rr * 4);
       }
+      // (word k of a row is valid where its 32 x 32 part, bit q + 4 k, flagged)
       wm[4 * ct + 0] = (parts >> q) & 1u ? m.x : 0u;
-      wm[4 * ct + 1] = (parts >> q) & 1u ? m.y : 0u;
-      wm[4 * ct + 2] = (parts >> (q + 4)) & 1u ? m.z : 0u;
-      wm[4 * ct + 3] = (parts >> (q + 4)) & 1u ? m.w : 0u;
+      wm[4 * ct + 1] = (parts >> (q + 4)) & 1u ? m.y : 0u;
+      wm[4 * ct + 2] = (parts >> (q + 8)) & 1u ? m.z : 0u;
+      wm[4 * ct + 3] = (parts >> (q + 12)) & 1u ? m.w : 0u;
     }
     int pc = 0;
 #pragma unroll
@@ -1301,7 +1321,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
             const int tile = jb.tile0 + (mt0 + rt) * tiles_n + nt0 + ct;
             const int rr = (r0 + i) & 127;
             const uint32_t parts = L.tile_mark[tile];
-            if ((parts >> ((rr >> 5) + 4 * ((w & 3) >> 1))) & 1u)
+            if ((parts >> ((rr >> 5) + 4 * (w & 3))) & 1u)
               wv[q] = L.fix_mask[(size_t)tile * kFixWords + rr * 4 + (w & 3)];
           }
         }

@@ -52,9 +52,9 @@ struct TcLaunch {
   int prec, epi;     // launch-uniform output rounding / GELU epilogue (== every job's)
   int n_jobs, total_tiles;
   uint32_t* fix_mask;   // [total_tiles][kFixWords] flagged bits, row r at r*4 (words = 32 cols);
-                        // valid for the 32 x 64 parts whose bit is set in tile_mark
+                        // valid for the 32 x 32 parts whose bit is set in tile_mark
   uint32_t* fix_tiles;  // [total_tiles] tiles with flagged elements
-  uint32_t* tile_mark;  // [total_tiles] flagged-part bits (q + 4*half); zero between launches
+  uint32_t* tile_mark;  // [total_tiles] flagged-part bits (row quarter q + 4 * column chunk); zero between launches
   int fix_g;            // tile-fixup unit: 2 (2 x 2-tile super-tiles, fix_st) or 1 (listed tiles)
   const int4* fix_st;   // [n_fix_st] the launch's 2 x 2-tile super-tiles {job, row tile, col tile, 0}
   int n_fix_st;
