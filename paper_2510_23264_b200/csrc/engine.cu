@@ -1193,7 +1193,7 @@ struct Engine {
     a.A = xq, a.B = wu, a.C = nullptr;
     a.M = (int)rows, a.N = V, a.K = D, a.lda = D, a.ldb = ldu, a.ldc = V, a.prec = P.unemb;
     if (!R.xbp.p) throw Error(2, "internal: fused KL without padded baselines");
-    KlFuse kf{R.xbp.as<float>(), R.ebp.as<double>(), part, nb, n_ct, n_ct * 128};
+    KlFuse kf{R.xbp.as<double>(), R.ebp.as<double>(), part, nb, n_ct, n_ct * 128};
     Prof pf(this, "gemm_unembed", 2.0 * (double)rows * V * D, 0);
     launch_gemm_unembed_kl(a, kf, st);
     return part;
@@ -1345,13 +1345,9 @@ struct Engine {
                      kl ? R.prob.as<double>() : nullptr, kl ? R.psum.as<double>() : nullptr);
           if (kl && opt_kl_fused) {  // the fused KL's 16-byte-aligned baseline rows
             const int ld = unembed_kl_col_tiles(g.V) * 128;
-            R.xbp.ensure((size_t)R.nb * ld * 4), R.ebp.ensure((size_t)R.nb * ld * 8);
-            CK(cudaMemsetAsync(R.xbp.p, 0, (size_t)R.nb * ld * 4, st));
-            CK(cudaMemsetAsync(R.ebp.p, 0, (size_t)R.nb * ld * 8, st));
-            CK(cudaMemcpy2DAsync(R.xbp.p, (size_t)ld * 4, R.logits.p, (size_t)g.V * 4, (size_t)g.V * 4, R.nb,
-                                 cudaMemcpyDeviceToDevice, st));
-            CK(cudaMemcpy2DAsync(R.ebp.p, (size_t)ld * 8, R.prob.p, (size_t)g.V * 8, (size_t)g.V * 8, R.nb,
-                                 cudaMemcpyDeviceToDevice, st));
+            R.xbp.ensure((size_t)R.nb * ld * 8), R.ebp.ensure((size_t)R.nb * ld * 8);
+            launch_pad_baselines(R.logits.as<float>(), R.prob.as<double>(), R.nb, g.V, ld, R.xbp.as<double>(),
+                                 R.ebp.as<double>(), st);
           }
           launched();
         }

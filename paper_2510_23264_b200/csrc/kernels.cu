@@ -807,13 +807,13 @@ __global__ void __launch_bounds__(256) gemm_exact_big_kernel(const GemmJob* __re
 
 // One 128 x 128 tile. MAP: logical row m of A and C is physical row
 // rowmap[m] (the exact recomputation of a device-built list of rows).
-// expm1 in double: Taylor polynomials for |d| < 2^-10 (degree 6) and
-// |d| < 2^-7 (degree 9), truncation < 2^-70 |d|; libdevice expm1 otherwise
+// expm1 in double: Taylor polynomials for |d| < 2^-10 (degree 4) and
+// |d| < 2^-7 (degree 9); libdevice expm1 otherwise. The KL needs each term
+// e expm1(d) to ~1e-10 of its e d^2 / 2 contribution: the degree-4
+// truncation d^5 / 120 is below 2e-11 of d^2 / 2 for |d| < 2^-10.
 __device__ __forceinline__ double expm1_small(double d) {
-  if (fabs(d) < 0.0009765625) {  // |d| < 2^-10: degree 6 (truncation < 2^-72 |d|)
-    double p = fma(d, 1.0 / 720.0, 1.0 / 120.0);
-    p = fma(p, d, 1.0 / 24.0);
-    p = fma(p, d, 1.0 / 6.0);
+  if (fabs(d) < 0.0009765625) {  // |d| < 2^-10: degree 4
+    double p = fma(d, 1.0 / 24.0, 1.0 / 6.0);
     p = fma(p, d, 0.5);
     p = fma(p, d, 1.0);
     return p * d;
@@ -930,22 +930,24 @@ __device__ __forceinline__ void x2_tile(const GemmJob& jb, int m0, int n0, const
       double T = 0.0, S = 0.0;
       if (gm < jb.M) {
         const int it = gm % kf->nb;
-        const float* xb = kf->xb + (int64_t)it * kf->ld + n0 + tx * 4;
+        const double* xb = kf->xb + (int64_t)it * kf->ld + n0 + tx * 4;  // (in double already)
         const double* eb = kf->eb + (int64_t)it * kf->ld + n0 + tx * 4;
-        const float4 xa = __ldg(reinterpret_cast<const float4*>(xb));
-        const float4 xc = __ldg(reinterpret_cast<const float4*>(xb + 64));
+        const double2 x0 = __ldg(reinterpret_cast<const double2*>(xb));
+        const double2 x1 = __ldg(reinterpret_cast<const double2*>(xb + 2));
+        const double2 x2 = __ldg(reinterpret_cast<const double2*>(xb + 64));
+        const double2 x3 = __ldg(reinterpret_cast<const double2*>(xb + 66));
         const double2 e0 = __ldg(reinterpret_cast<const double2*>(eb));
         const double2 e1 = __ldg(reinterpret_cast<const double2*>(eb + 2));
         const double2 e2 = __ldg(reinterpret_cast<const double2*>(eb + 64));
         const double2 e3 = __ldg(reinterpret_cast<const double2*>(eb + 66));
-        const float xbv[8] = {xa.x, xa.y, xa.z, xa.w, xc.x, xc.y, xc.z, xc.w};
+        const double xbv[8] = {x0.x, x0.y, x1.x, x1.y, x2.x, x2.y, x3.x, x3.y};
         const double ebv[8] = {e0.x, e0.y, e1.x, e1.y, e2.x, e2.y, e3.x, e3.y};
         double t2[2] = {0.0, 0.0}, s2[2] = {0.0, 0.0};  // two independent chains
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const f2_t pr = acc[i][j >> 1];
           const float x = round_p((j & 1) ? f2_hi(pr) : f2_lo(pr), jb.prec);
-          const double d = (double)x - (double)xbv[j];
+          const double d = (double)x - xbv[j];
           s2[j & 1] = fma(ebv[j], d, s2[j & 1]);
           t2[j & 1] = fma(ebv[j], expm1_small(d), t2[j & 1]);
         }
@@ -1018,6 +1020,23 @@ void launch_gemm_unembed_kl(const GemmJob& jb, const KlFuse& kf, cudaStream_t st
 }
 
 int unembed_kl_col_tiles(int V) { return (V + kXBN - 1) / kXBN; }
+
+// the fused KL's baselines: logits (as doubles) and exp(lp) per item, zero
+// padded to the 128-column pitch ld (16-byte aligned rows)
+__global__ void pad_baselines_kernel(const float* __restrict__ logits, const double* __restrict__ prob, int V,
+                                     int ld, double* __restrict__ xbd, double* __restrict__ ebd) {
+  const int it = blockIdx.y;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ld; c += gridDim.x * blockDim.x) {
+    const bool in = c < V;
+    xbd[(int64_t)it * ld + c] = in ? (double)logits[(int64_t)it * V + c] : 0.0;
+    ebd[(int64_t)it * ld + c] = in ? prob[(int64_t)it * V + c] : 0.0;
+  }
+}
+
+void launch_pad_baselines(const float* logits, const double* prob, int nb, int V, int ld, double* xbd,
+                          double* ebd, cudaStream_t st) {
+  if (nb > 0) pad_baselines_kernel<<<dim3((ld + 255) / 256, nb), 256, 0, st>>>(logits, prob, V, ld, xbd, ebd);
+}
 
 // ---- HeadBundle prefetch (pahq.cpp:93-165, 211-238), B200 form --------------
 // The FP32 masters are resident in HBM; what the next source group's

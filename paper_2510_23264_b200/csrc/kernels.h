@@ -116,16 +116,18 @@ void launch_lse(const float* base, int rows, int V, double* lse, int* nan_flag, 
                 double* p_out = nullptr, double* p_sum = nullptr);
 // Fused unembed + KL (kernels.cu, gemm_unembed_kl_kernel): per 128-column
 // tile partials (T, S) of the patched rows against the baseline item
-// (row % nb): xb [nb][ld] baseline logits, eb [nb][ld] exp(lp), both
-// zero-padded to ld = V rounded up to 128.
+// (row % nb): xb [nb][ld] baseline logits (as doubles), eb [nb][ld] exp(lp),
+// both zero-padded to ld = V rounded up to 128 (launch_pad_baselines).
 struct KlFuse {
-  const float* xb;
+  const double* xb;
   const double* eb;
   double2* part;  // [rows][n_ct]
   int nb, n_ct, ld;
 };
 void launch_gemm_unembed_kl(const GemmJob& jb, const KlFuse& kf, cudaStream_t st);
 int unembed_kl_col_tiles(int V);
+void launch_pad_baselines(const float* logits, const double* prob, int nb, int V, int ld, double* xbd,
+                          double* ebd, cudaStream_t st);
 // L2 prefetch (cp.async.bulk.prefetch.L2) of up to three column slices
 // (rows x cols floats at pitch ld floats; null: none) and two whole matrices;
 // addresses 16-byte aligned, sizes multiples of 16. Passed by value: no
