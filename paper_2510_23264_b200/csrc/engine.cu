@@ -400,6 +400,7 @@ struct Engine {
   // halves: when one fills, an event marks the end of the work that reads it
   // and the other half is reused once its own event has completed (long
   // done in steady state), so the host never drains the GPU to recycle it.
+  double host_blocked_ms = 0;  // host time waiting for the GPU to recycle staging (CQG_HOST_PROF)
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   bool stage_ev_set[2] = {false, false};
   int stage_half = 0;
@@ -421,7 +422,11 @@ struct Engine {
       CK(cudaEventRecord(stage_ev[stage_half], st));
       stage_ev_set[stage_half] = true;
       stage_half ^= 1;
-      if (stage_ev_set[stage_half]) CK(cudaEventSynchronize(stage_ev[stage_half]));
+      if (stage_ev_set[stage_half]) {
+        const auto t0 = std::chrono::steady_clock::now();
+        CK(cudaEventSynchronize(stage_ev[stage_half]));
+        host_blocked_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      }
       stage_off = (size_t)stage_half * half;
     }
   }
@@ -1952,6 +1957,10 @@ struct Engine {
     float dms = 0;
     CK(cudaEventElapsedTime(&dms, ev0, ev1));
     stats.ms_device = dms;
+    if (getenv("CQG_HOST_PROF"))  // where the host's time went (diagnostics only)
+      fprintf(stderr, "cqg host: baseline phases %.1f ms, pass phases %.1f ms, blocked on staging %.1f ms, device %.1f ms, launches %lld\n",
+              ms_base, ms_pass, host_blocked_ms, (double)dms, (long long)stats.kernel_launches);
+    host_blocked_ms = 0;
     collect_profile();
     stats.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
