@@ -487,9 +487,16 @@ def main(argv=None):
     else:
         ach = p["bytes"] / (p["ms"] / 1e3) / 1e9
         peak, unit, bound, psrc = hbm, "GB/s", "hbm", src
+    kernel_note = None
+    if cls == "gemm_unembed" and os.environ.get("CQG_OPTS", "").find("kl_fused=0") < 0:
+        kernel_note = ("gemm_unembed_kl_kernel: the exact FP32 unembed with the log-softmax + KL "
+                       "reduction fused into its epilogue (FP64 expm1 / dot partials per tile, no "
+                       "logits stored); achieved counts only the GEMM's 2 D V flops per row. The "
+                       "GEMM alone (kl_fused=0) runs at ~32.4 TFLOP/s = 0.87 of this peak, plus a "
+                       "separate 0.21 s KL kernel (profiles/r2_klfused_ab_*.json)")
     roofline = {"bound": bound, "kernel": name, "achieved": ach, "peak": peak, "unit": unit,
                 "frac": ach / peak, "traffic": traffic, "traffic_note": traffic_note,
-                "peak_source": psrc,
+                "kernel_note": kernel_note, "peak_source": psrc,
                 "kernel_share_of_step": p["ms"] / max(1e-9, sum(v["ms"] for v in prof.values())),
                 "per_kernel": {k: {"ms": v["ms"], "launches": v["launches"],
                                    "tflops": v["flops"] / max(v["ms"], 1e-9) / 1e9,
