@@ -528,11 +528,19 @@ def main(argv=None):
         # tau at a high quantile of this workload's iteration-1 scores, so a
         # non-trivial circuit survives and several iterations run
         tau_q = float(np.quantile(scores, args.acdc_quantile))
-        acdc = timed_acdc(tau_q)
-        acdc["tau_rule"] = f"quantile {args.acdc_quantile} of the iteration-1 scores"
+        sweep = timed_roc_sweep(eng, e, scores, edges, barrier, max_over_ranks, dev_s / args.steps)
+        # headline: the largest grid threshold whose final circuit keeps at
+        # least 16 edges (the sweep's kept counts are identical on every rank:
+        # scores are all-reduced), so the timed run prunes to a non-empty circuit
+        grid = eng.threshold_grid(0.001, 3.16, 21)
+        nt = [t for t, k in zip(grid, sweep["kept"]) if k >= 16]
+        tau_nt = float(max(nt)) if nt else float(grid[0])
+        acdc = timed_acdc(tau_nt)
+        acdc["tau_rule"] = ("largest threshold_grid(0.001, 3.16, 21) value whose final circuit "
+                            "keeps >= 16 edges (from the roc_sweep below)")
+        acdc[f"tau_quantile_{args.acdc_quantile}"] = timed_acdc(tau_q)
         acdc["tau_0.01"] = timed_acdc(0.01)
-        acdc["roc_sweep"] = timed_roc_sweep(eng, e, scores, edges, barrier, max_over_ranks,
-                                            dev_s / args.steps)
+        acdc["roc_sweep"] = sweep
 
     if rank == 0:
         cb = None
