@@ -63,10 +63,10 @@ def load_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def make_inputs(name):
+def make_inputs(name, weight_scale=0.0):
     c = CONFIGS[name]
     cfg = c["cfg"]
-    w = synth.random_weights(cfg, 1)
+    w = synth.random_weights(cfg, 1, weight_scale)
     if c["data"] == "ioi":
         ds = synth.ioi_dataset(cfg, c["items"], 1)
     elif c["data"] == "greater_than":
@@ -289,7 +289,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cfg, w, ds = make_inputs(args.config)
+    cfg, w, ds = make_inputs(args.config, getattr(args, "weight_scale", 0.0))
     try:
         cb = cpu_sample(cfg, w, ds, args.steps, args.warmup)
     except Exception as e:  # the oracle library always exists in-tree
@@ -358,6 +358,11 @@ def main(argv=None):
     ap.add_argument("--max-edges", type=int, default=0,
                     help="score an evenly strided sample of at most this many iteration-1 edges "
                          "(configs 4-5 on one GPU; reported in config.edges_sampled)")
+    ap.add_argument("--weight-scale", type=float, default=0.0,
+                    help="uniform half-width of the attention / MLP weight matrices (default: "
+                         "support.hpp's 0.8/sqrt(d)); larger values model trained-weight "
+                         "magnitudes: E4M3 weights leave the subnormal range and the "
+                         "certificate flags more elements")
     ap.add_argument("--acdc-quantile", type=float, default=0.99,
                     help="ACDC end-to-end threshold = this quantile of the iteration-1 scores "
                          "(a non-trivial circuit survives); tau=0.01 is timed as well")
@@ -377,7 +382,7 @@ def main(argv=None):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
-    cfg, w, ds = make_inputs(args.config)
+    cfg, w, ds = make_inputs(args.config, getattr(args, "weight_scale", 0.0))
     if args.items:
         ds = ds.subset(list(range(min(args.items, len(ds)))))
     items = len(ds)
@@ -458,7 +463,16 @@ def main(argv=None):
     e.set_option("profile", 1)
     e.score_edges(mask, edges, pol, True, eng.LOSS)
     prof = e.profile()
+    flagged = int(e.stats()["fallback_elems"])
     e.set_option("profile", 0)
+    # tensor-core output elements of the step (flops / 2K per GEMM class) and
+    # the share the certificate sent to the exact fixup
+    kdim = {"qkv": cfg.d_model, "wo": cfg.d_k, "mlp_in": cfg.d_model, "mlp_out": 4 * cfg.d_model}
+    tc_el = sum(v["flops"] / (2 * kdim[k.split("gemm_tc_")[1].split("_", 1)[1]])
+                for k, v in prof.items() if "gemm_tc_" in k)
+    certificate = {"flagged_elems_per_step": flagged, "tc_elems_per_step": int(tc_el),
+                   "flagged_share": flagged / tc_el if tc_el else None,
+                   "weight_scale": getattr(args, "weight_scale", 0.0) or "support.hpp default 0.8/sqrt(d)"}
     hbm, bf16, src = load_peaks()
     name, p = max(prof.items(), key=lambda kv: kv[1]["ms"])
     # FP32 CUDA-core rate for separately rounded mul + add (the reference's
@@ -567,7 +581,7 @@ def main(argv=None):
                        "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                        "parts": e2e_parts},
                "gpu_launches": int(launches), "wall_s": wall, "roofline": roofline,
-               "cpu_baseline": cb, "passes_per_step": passes_per_step,
+               "cpu_baseline": cb, "passes_per_step": passes_per_step, "certificate": certificate,
                "acdc_end_to_end": acdc, "acdc_toy_gpu_vs_cpu": toy}
         print(json.dumps(out))
     if dist:

@@ -536,3 +536,28 @@ def test_qkv_split_toy_acdc_matches_oracle():
     recs = [(s.edge, int(s.kept)) for it in r.iterations for s in it.scores]
     assert recs == [(int(a), int(k)) for (_, a, _, k) in want.records]
     e.close()
+
+
+@pytest.mark.parametrize("scale", [0.0, 0.15, 0.4])
+def test_trained_magnitude_weights_scores_match_oracle(scale):
+    """Weights larger than support.hpp's 0.8/sqrt(d) (trained-model
+    magnitudes: E4M3 weight codes leave the subnormal range, the E4M3
+    cert_all shortcut stops applying and the certificate flags far more
+    elements) still give the oracle's scores: every flagged element goes
+    through the exact fixup."""
+    from paper_2510_23264_b200 import synth
+    cfg = formats.ModelConfig(2, 4, 256, 64, 512, 16, 1, 1)
+    w = synth.random_weights(cfg, 3, scale)
+    ds = synth.random_dataset(cfg, 4, 5)
+    p = Port(cfg, w.mats)
+    e = eng.Engine(w)
+    e.set_dataset(ds, KL)
+    mask = np.ones(p.n_edges, bool)
+    edges = np.arange(p.n_edges, dtype=np.int32)
+    want = p.score_edges(ds, edges, Policy.head_quantized(), per_edge=True, metric=KL, mask=mask)
+    got = e.score_edges(mask, edges, eng.PrecisionPolicy.head_quantized(), True, 0)
+    flagged = e.stats()["fallback_elems"]
+    e.close()
+    assert close(got, want), (scale, np.max(np.abs(got - want)))
+    if scale >= 0.15:
+        assert flagged > 0, "the certificate path was not exercised"
