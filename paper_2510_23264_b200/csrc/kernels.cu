@@ -7,6 +7,7 @@
 // (gemm_tc.cu).
 #include <float.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "kernels.h"
 #include "numerics.cuh"
@@ -423,6 +424,112 @@ __global__ void __launch_bounds__(32 * kLnWarps) ln_warp_kernel(const LnJob* __r
 // row-major from shared memory (same arithmetic as ln_warp_kernel).
 constexpr int kLsWarps = 4;
 
+// The two sequential reductions of one row (kernels.cpp:127-142: mean, then
+// the mean of squared deviations, k ascending, no FMA) at FADD latency, from
+// a 16-byte aligned row in shared memory; inv = 1 / sqrt(var + eps).
+__device__ __forceinline__ void ln_row_stats(const float* row, int D, float& mean, float& inv) {
+  // sequential chains at FADD latency: 16-byte shared loads (rows are
+  // 16-byte aligned, P % 4 == 0), the next 16 elements loaded ahead of the
+  // dependent adds of the current 16
+  constexpr int U = 16;
+  float acc = 0.f;
+  float4 cur[U / 4], nxt[U / 4];
+  const int Dm = D & ~(U - 1);
+  if (Dm) {
+#pragma unroll
+    for (int k = 0; k < U / 4; ++k) cur[k] = reinterpret_cast<const float4*>(row)[k];
+  }
+  for (int c = 0; c < Dm; c += U) {
+    const bool more = c + U < Dm;
+#pragma unroll
+    for (int k = 0; k < U / 4; ++k)
+      nxt[k] = more ? reinterpret_cast<const float4*>(row + c + U)[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < U / 4; ++k) {
+      acc = __fadd_rn(acc, cur[k].x);
+      acc = __fadd_rn(acc, cur[k].y);
+      acc = __fadd_rn(acc, cur[k].z);
+      acc = __fadd_rn(acc, cur[k].w);
+    }
+#pragma unroll
+    for (int k = 0; k < U / 4; ++k) cur[k] = nxt[k];
+  }
+  for (int c = Dm; c < D; ++c) acc = __fadd_rn(acc, row[c]);
+  mean = __fdiv_rn(acc, (float)D);
+  acc = 0.f;
+  if (Dm) {
+#pragma unroll
+    for (int k = 0; k < U / 4; ++k) cur[k] = reinterpret_cast<const float4*>(row)[k];
+  }
+  for (int c = 0; c < Dm; c += U) {
+    const bool more = c + U < Dm;
+#pragma unroll
+    for (int k = 0; k < U / 4; ++k)
+      nxt[k] = more ? reinterpret_cast<const float4*>(row + c + U)[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < U / 4; ++k) {
+      const float xs[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const float d = __fsub_rn(xs[h], mean);
+        acc = __fadd_rn(acc, __fmul_rn(d, d));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U / 4; ++k) cur[k] = nxt[k];
+  }
+  for (int c = Dm; c < D; ++c) {
+    const float d = __fsub_rn(row[c], mean);
+    acc = __fadd_rn(acc, __fmul_rn(d, d));
+  }
+  acc = __fdiv_rn(acc, (float)D);
+  inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(acc, 1e-5f)));
+}
+
+// Normalisation of row r (job-local index grow) from shared memory by the
+// whole warp: y = gamma (x - mean) inv + beta, rounded at prec, the packed
+// tensor-core copy and the row norm of the rounded output (fused).
+__device__ __forceinline__ void ln_row_out(const LnJob& j, const float* row, int64_t grow, float m_r,
+                                           float i_r, const float* __restrict__ gamma,
+                                           const float* __restrict__ beta, int D, int prec, int lane) {
+  const int D4 = D >> 2;
+  const int64_t ob = grow * D;
+  float ss = 0.f;
+  bool bad = false;
+  for (int c4 = lane; c4 < D4; c4 += 32) {
+    const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c4);
+    const float4 bt = __ldg(reinterpret_cast<const float4*>(beta) + c4);
+    const float4 xv = reinterpret_cast<const float4*>(row)[c4];
+    const float gg[4] = {gm.x, gm.y, gm.z, gm.w}, bb[4] = {bt.x, bt.y, bt.z, bt.w};
+    const float xx[4] = {xv.x, xv.y, xv.z, xv.w};
+    float y[4], qv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      y[k] = __fadd_rn(__fmul_rn(gg[k], __fmul_rn(__fsub_rn(xx[k], m_r), i_r)), bb[k]);
+      qv[k] = round_p(y[k], prec);
+      ss = fmaf(qv[k], qv[k], ss);
+      bad = bad || bf16_fma_bad(qv[k]);
+    }
+    if (j.xln) reinterpret_cast<float4*>(j.xln + ob)[c4] = make_float4(y[0], y[1], y[2], y[3]);
+    if (j.xq) reinterpret_cast<float4*>(j.xq + ob)[c4] = make_float4(qv[0], qv[1], qv[2], qv[3]);
+    if (j.xqp) {
+      if (j.pack == 2)
+        reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(j.xqp) + ob)[c4] =
+            make_uint2(enc_bf16(qv[0]) | ((uint32_t)enc_bf16(qv[1]) << 16),
+                       enc_bf16(qv[2]) | ((uint32_t)enc_bf16(qv[3]) << 16));
+      else
+        reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(j.xqp) + ob)[c4] =
+            enc_e4m3(qv[0]) | ((uint32_t)enc_e4m3(qv[1]) << 8) | ((uint32_t)enc_e4m3(qv[2]) << 16) |
+            ((uint32_t)enc_e4m3(qv[3]) << 24);
+    }
+  }
+  if (j.xnorm) {
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    bad = __any_sync(0xffffffffu, bad) && j.pack == 2;
+    if (lane == 0) j.xnorm[grow] = bad ? -(sqrtf(ss) * 1.0001f) : sqrtf(ss) * 1.0001f;
+  }
+}
+
 template <int RW>
 __global__ void __launch_bounds__(32 * kLsWarps) ln_small_kernel(const LnJob* __restrict__ jobs,
                                                                  const float* __restrict__ gamma,
@@ -451,105 +558,56 @@ __global__ void __launch_bounds__(32 * kLsWarps) ln_small_kernel(const LnJob* __
   cp_async_wait<0>();
   __syncwarp();
   float mean = 0.f, inv = 0.f;
-  if (lane < nr) {
-    // sequential chains at FADD latency: 16-byte shared loads (rows are
-    // 16-byte aligned, P % 4 == 0), the next 16 elements loaded ahead of the
-    // dependent adds of the current 16
-    const float* row = t + lane * P;
-    constexpr int U = 16;
-    float acc = 0.f;
-    float4 cur[U / 4], nxt[U / 4];
-    const int Dm = D & ~(U - 1);
-    if (Dm) {
-#pragma unroll
-      for (int k = 0; k < U / 4; ++k) cur[k] = reinterpret_cast<const float4*>(row)[k];
-    }
-    for (int c = 0; c < Dm; c += U) {
-      const bool more = c + U < Dm;
-#pragma unroll
-      for (int k = 0; k < U / 4; ++k)
-        nxt[k] = more ? reinterpret_cast<const float4*>(row + c + U)[k] : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int k = 0; k < U / 4; ++k) {
-        acc = __fadd_rn(acc, cur[k].x);
-        acc = __fadd_rn(acc, cur[k].y);
-        acc = __fadd_rn(acc, cur[k].z);
-        acc = __fadd_rn(acc, cur[k].w);
-      }
-#pragma unroll
-      for (int k = 0; k < U / 4; ++k) cur[k] = nxt[k];
-    }
-    for (int c = Dm; c < D; ++c) acc = __fadd_rn(acc, row[c]);
-    mean = __fdiv_rn(acc, (float)D);
-    acc = 0.f;
-    if (Dm) {
-#pragma unroll
-      for (int k = 0; k < U / 4; ++k) cur[k] = reinterpret_cast<const float4*>(row)[k];
-    }
-    for (int c = 0; c < Dm; c += U) {
-      const bool more = c + U < Dm;
-#pragma unroll
-      for (int k = 0; k < U / 4; ++k)
-        nxt[k] = more ? reinterpret_cast<const float4*>(row + c + U)[k] : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int k = 0; k < U / 4; ++k) {
-        const float xs[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const float d = __fsub_rn(xs[h], mean);
-          acc = __fadd_rn(acc, __fmul_rn(d, d));
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < U / 4; ++k) cur[k] = nxt[k];
-    }
-    for (int c = Dm; c < D; ++c) {
-      const float d = __fsub_rn(row[c], mean);
-      acc = __fadd_rn(acc, __fmul_rn(d, d));
-    }
-    acc = __fdiv_rn(acc, (float)D);
-    inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(acc, 1e-5f)));
-  }
-  const int D4 = D >> 2;
+  if (lane < nr) ln_row_stats(t + lane * P, D, mean, inv);
   for (int r = 0; r < nr; ++r) {
     const float m_r = __shfl_sync(0xffffffffu, mean, r), i_r = __shfl_sync(0xffffffffu, inv, r);
-    const float* row = t + r * P;
-    const int64_t ob = (int64_t)(r0 + r) * D;
-    float ss = 0.f;
-    bool bad = false;
-    for (int c4 = lane; c4 < D4; c4 += 32) {
-      const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c4);
-      const float4 bt = __ldg(reinterpret_cast<const float4*>(beta) + c4);
-      const float4 xv = reinterpret_cast<const float4*>(row)[c4];
-      const float gg[4] = {gm.x, gm.y, gm.z, gm.w}, bb[4] = {bt.x, bt.y, bt.z, bt.w};
-      const float xx[4] = {xv.x, xv.y, xv.z, xv.w};
-      float y[4], qv[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        y[k] = __fadd_rn(__fmul_rn(gg[k], __fmul_rn(__fsub_rn(xx[k], m_r), i_r)), bb[k]);
-        qv[k] = round_p(y[k], prec);
-        ss = fmaf(qv[k], qv[k], ss);
-        bad = bad || bf16_fma_bad(qv[k]);
-      }
-      if (j.xln) reinterpret_cast<float4*>(j.xln + ob)[c4] = make_float4(y[0], y[1], y[2], y[3]);
-      if (j.xq) reinterpret_cast<float4*>(j.xq + ob)[c4] = make_float4(qv[0], qv[1], qv[2], qv[3]);
-      if (j.xqp) {
-        if (j.pack == 2)
-          reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(j.xqp) + ob)[c4] =
-              make_uint2(enc_bf16(qv[0]) | ((uint32_t)enc_bf16(qv[1]) << 16),
-                         enc_bf16(qv[2]) | ((uint32_t)enc_bf16(qv[3]) << 16));
-        else
-          reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(j.xqp) + ob)[c4] =
-              enc_e4m3(qv[0]) | ((uint32_t)enc_e4m3(qv[1]) << 8) | ((uint32_t)enc_e4m3(qv[2]) << 16) |
-              ((uint32_t)enc_e4m3(qv[3]) << 24);
-      }
-    }
-    if (j.xnorm) {
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      bad = __any_sync(0xffffffffu, bad) && j.pack == 2;
-      if (lane == 0) j.xnorm[r0 + r] = bad ? -(sqrtf(ss) * 1.0001f) : sqrtf(ss) * 1.0001f;
-    }
+    ln_row_out(j, t + r * P, r0 + r, m_r, i_r, gamma, beta, D, prec, lane);
   }
+}
+
+// Big launches (the patched passes: tens of thousands of rows): ln_small's
+// 4 chain lanes per warp left it issue-bound (ncu: 72% issue-active, 15% of
+// HBM; the chain loops cost ~1350 warp-instructions per row). Here a CTA of
+// kLlWarps warps stages 32 rows (~99 KB, two CTAs per SM), warp 0 runs all 32
+// rows' chains with one row per lane (conflict-free 16-byte loads: the row
+// pitch D + 4 puts lanes 0..7 of a quarter-warp on distinct bank quads), and
+// every warp then normalises a share of the rows. The chain phase of one CTA
+// overlaps the loads and normalisation of the other. Same arithmetic as
+// ln_small_kernel (ln_row_stats / ln_row_out): bit-identical outputs.
+constexpr int kLlWarps = 4, kLlRows = 32;
+constexpr size_t smem_cap_ll() { return sizeof(float) * kLlRows * (1024 + 4); }
+
+__global__ void __launch_bounds__(32 * kLlWarps) ln_lane_kernel(const LnJob* __restrict__ jobs,
+                                                                const float* __restrict__ gamma,
+                                                                const float* __restrict__ beta, int D,
+                                                                int prec) {
+  extern __shared__ float ll_sm[];
+  __shared__ float s_mean[kLlRows], s_inv[kLlRows];
+  const LnJob j = jobs[blockIdx.y];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.x * kLlRows;
+  if (r0 >= j.rows) return;
+  const int P = D + 4;
+  const int nr = min(kLlRows, j.rows - r0);
+  const bool a16 = (j.in_stride & 3) == 0 && (reinterpret_cast<uintptr_t>(j.in) & 15) == 0;
+  for (int r = warp; r < nr; r += kLlWarps) {
+    const float* src = j.in + (int64_t)(r0 + r) * j.in_stride;
+    if (a16)
+      for (int c = 4 * lane; c < D; c += 128) cp_async16(ll_sm + r * P + c, src + c);
+    else
+      for (int c = lane; c < D; c += 32) cp_async4(ll_sm + r * P + c, src + c);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  if (warp == 0 && lane < nr) {
+    float mean, inv;
+    ln_row_stats(ll_sm + lane * P, D, mean, inv);
+    s_mean[lane] = mean, s_inv[lane] = inv;
+  }
+  __syncthreads();
+  for (int r = warp; r < nr; r += kLlWarps)
+    ln_row_out(j, ll_sm + r * P, r0 + r, s_mean[r], s_inv[r], gamma, beta, D, prec, lane);
 }
 
 void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float* gamma,
@@ -559,6 +617,24 @@ void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float
   // Whole rows staged in shared memory: every row is read from HBM once (the
   // ring kernel below re-streams each row three times and thrashes L2 on big
   // launches), and the chains run at FADD latency.
+  const int64_t total_rows = (int64_t)max_rows * n_jobs;
+  // CQG_LN_LANE_MIN: launches with at least this many rows use ln_lane_kernel
+  // (0: never; tests set 1 to run it on every launch)
+  const char* e = getenv("CQG_LN_LANE_MIN");
+  const int64_t ll_min_rows = e ? atoll(e) : 4 * kLlRows * 148;
+  if ((D & 3) == 0 && D <= 1024 && ll_min_rows > 0 && total_rows >= ll_min_rows) {
+    const size_t smem = sizeof(float) * kLlRows * (D + 4);
+    static bool attr_l = false;
+    if (!attr_l) {
+      cudaFuncSetAttribute(ln_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap_ll());
+      attr_l = true;
+    }
+    for (int y0 = 0; y0 < n_jobs; y0 += 65535) {
+      dim3 grid((max_rows + kLlRows - 1) / kLlRows, (unsigned)std::min(65535, n_jobs - y0));
+      ln_lane_kernel<<<grid, 32 * kLlWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
+    }
+    return;
+  }
   if ((D & 3) == 0 && D <= 2048) {
     // rows per warp: 8 (4 for D > 1024) on big launches; fewer when the
     // launch would not give every SM several warps (the per-source baseline
@@ -807,29 +883,33 @@ __global__ void __launch_bounds__(256) gemm_exact_big_kernel(const GemmJob* __re
 
 // One 128 x 128 tile. MAP: logical row m of A and C is physical row
 // rowmap[m] (the exact recomputation of a device-built list of rows).
-// expm1 in double: Taylor polynomials for |d| < 2^-10 (degree 4) and
-// |d| < 2^-7 (degree 9); libdevice expm1 otherwise. The KL needs each term
-// e expm1(d) to ~1e-10 of its e d^2 / 2 contribution: the degree-4
-// truncation d^5 / 120 is below 2e-11 of d^2 / 2 for |d| < 2^-10.
-__device__ __forceinline__ double expm1_small(double d) {
-  if (fabs(d) < 0.0009765625) {  // |d| < 2^-10: degree 4
-    double p = fma(d, 1.0 / 24.0, 1.0 / 6.0);
-    p = fma(p, d, 0.5);
-    p = fma(p, d, 1.0);
-    return p * d;
-  }
-  if (fabs(d) < 0.0078125) {
-    double p = fma(d, 1.0 / 362880.0, 1.0 / 40320.0);
-    p = fma(p, d, 1.0 / 5040.0);
-    p = fma(p, d, 1.0 / 720.0);
-    p = fma(p, d, 1.0 / 120.0);
-    p = fma(p, d, 1.0 / 24.0);
-    p = fma(p, d, 1.0 / 6.0);
-    p = fma(p, d, 0.5);
-    p = fma(p, d, 1.0);
-    return p * d;
-  }
-  return expm1(d);
+// expm1 in double for the fused KL epilogue, branch-free for |d| < 8:
+//   d = k/128 + r (k = rint(128 d), r exact, |r| <= 2^-8),
+//   expm1(d) = m + (1 + m) expm1(r),  m = expm1(k/128) from a 2049-entry
+//   table (g_em1_tab, built once per device with libdevice expm1, <= 1 ulp),
+//   expm1(r) by its degree-6 Taylor polynomial (truncation r^7/7! < 3e-21).
+// Absolute error ~2^-52 |expm1(d)|: the KL's absolute error stays ~1e-16,
+// an order below the reference's own rounding of lse (2^-49). The warp no
+// longer diverges into libdevice expm1 (~80 instructions) whenever one lane's
+// |d| exceeds a polynomial range; |d| >= 8, Inf and NaN still go there.
+__device__ double g_em1_tab[2049];
+
+__global__ void em1_tab_kernel() {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 2049) g_em1_tab[i] = expm1((double)(i - 1024) * 0.0078125);
+}
+
+__device__ __forceinline__ double expm1_tab(double d) {
+  if (!(fabs(d) < 8.0)) return expm1(d);
+  const double kd = rint(d * 128.0);
+  const double r = fma(kd, -0.0078125, d);  // exact: k/128 and d are within 2^-8
+  double p = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p * r, r, r);
+  const double m = __ldg(&g_em1_tab[(int)kd + 1024]);
+  return fma(1.0 + m, p, m);
 }
 
 template <bool MAP, bool FUSE = false>
@@ -949,7 +1029,7 @@ __device__ __forceinline__ void x2_tile(const GemmJob& jb, int m0, int n0, const
           const float x = round_p((j & 1) ? f2_hi(pr) : f2_lo(pr), jb.prec);
           const double d = (double)x - xbv[j];
           s2[j & 1] = fma(ebv[j], d, s2[j & 1]);
-          t2[j & 1] = fma(ebv[j], expm1_small(d), t2[j & 1]);
+          t2[j & 1] = fma(ebv[j], expm1_tab(d), t2[j & 1]);
         }
         T = t2[0] + t2[1], S = s2[0] + s2[1];
       }
@@ -1015,6 +1095,14 @@ __global__ void __launch_bounds__(256, 2) gemm_unembed_kl_kernel(GemmJob jb, KlF
 
 void launch_gemm_unembed_kl(const GemmJob& jb, const KlFuse& kf, cudaStream_t st) {
   if (jb.M <= 0) return;
+  static bool tab_ready[64] = {};  // g_em1_tab is per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !tab_ready[dev]) {
+    em1_tab_kernel<<<(2049 + 255) / 256, 256, 0, st>>>();
+    cudaStreamSynchronize(st);  // once per device: engines on other streams see the table
+    tab_ready[dev] = true;
+  }
   const int tiles = ((jb.M + kXBM - 1) / kXBM) * ((jb.N + kXBN - 1) / kXBN);
   gemm_unembed_kl_kernel<<<tiles, 256, 0, st>>>(jb, kf, -0.0f);
 }

@@ -45,12 +45,20 @@ def load_case(name):
 
 
 @pytest.mark.parametrize("case,opts", [("gpt2s_ioi", {}), ("gpt2s_ioi", {"mem_budget": 1}),
-                                       ("gpt2m_slice", {}), ("pythia_slice", {})])
-def test_model_shapes_match_reference(case, opts):
+                                       ("gpt2s_ioi", {"env:CQG_LN_LANE_MIN": 1}),
+                                       ("gpt2m_slice", {}), ("gpt2m_slice", {"env:CQG_LN_LANE_MIN": 1}),
+                                       ("pythia_slice", {})])
+def test_model_shapes_match_reference(case, opts, monkeypatch):
+    """(env:CQG_LN_LANE_MIN=1 runs every layer norm through ln_lane_kernel,
+    the big-launch LN kernel, which the bench step uses but these small
+    golden cases would not reach.)"""
     cfg, w, ds, edges, want = load_case(case)
     e = eng.Engine(w)
     for k, v in opts.items():
-        e.set_option(k, v)
+        if k.startswith("env:"):
+            monkeypatch.setenv(k[4:], str(v))
+        else:
+            e.set_option(k, v)
     e.set_dataset(ds, eng.KL)
     mask = np.ones(e.n_edges, bool)
     got = e.score_edges(mask, edges, eng.PrecisionPolicy.head_quantized(), True, eng.LOSS)

@@ -130,8 +130,11 @@ def test_int8_images_bitexact(cfg):
 
 
 # --- forward (model.cpp:556-757), bitwise --------------------------------------
-@pytest.mark.parametrize("cfg", [TINY, SMALL, TOY])
-def test_forward_bitexact(cfg):
+@pytest.mark.parametrize("cfg,ln_lane", [(TINY, 0), (SMALL, 0), (TOY, 0), (SMALL, 1), (TOY, 1)])
+def test_forward_bitexact(cfg, ln_lane, monkeypatch):
+    """(ln_lane: every layer norm through ln_lane_kernel, CQG_LN_LANE_MIN=1)"""
+    if ln_lane:
+        monkeypatch.setenv("CQG_LN_LANE_MIN", "1")
     w, ds = make(cfg, 3, 2, 4)
     p = Port(cfg, w.mats)
     e = eng.Engine(w)
