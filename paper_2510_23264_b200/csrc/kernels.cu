@@ -486,16 +486,35 @@ __device__ __forceinline__ void ln_row_stats(const float* row, int D, float& mea
   inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(acc, 1e-5f)));
 }
 
+// Paired E4M3 codes (cvt.rn.satfinite.e4m3x2, the reference's NaN code 0x7F:
+// enc_e4m3 element by element) and their values (dec_e4m3)
+__device__ __forceinline__ uint32_t ln_e4m3x2(float a, float b) {
+  uint32_t c = (uint32_t)__nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+  if (a != a) c = (c & 0xFF00u) | 0x7Fu;
+  if (b != b) c = (c & 0x00FFu) | 0x7F00u;
+  return c;
+}
+__device__ __forceinline__ float2 ln_e4m3x2_val(uint32_t c) {
+  return __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)c, __NV_E4M3)));
+}
+
 // Normalisation of row r (job-local index grow) from shared memory by the
-// whole warp: y = gamma (x - mean) inv + beta, rounded at prec, the packed
-// tensor-core copy and the row norm of the rounded output (fused).
-__device__ __forceinline__ void ln_row_out(const LnJob& j, const float* row, int64_t grow, float m_r,
-                                           float i_r, const float* __restrict__ gamma,
-                                           const float* __restrict__ beta, int D, int prec, int lane) {
+// whole warp: y = gamma (x - mean) inv + beta, rounded at PREC, the packed
+// tensor-core copy (PACK 1: E4M3 codes, 2: BF16 codes, 0: none) and the row
+// norm of the rounded output (fused). PREC / PACK are compile-time so the
+// per-element work is the affine map, one paired conversion and the stores
+// (the E4M3 codes are converted once and serve both the rounded value and
+// the packed copy).
+template <int PREC, int PACK>
+__device__ __forceinline__ void ln_row_out_t(const LnJob& j, const float* row, int64_t grow, float m_r,
+                                             float i_r, const float* __restrict__ gamma,
+                                             const float* __restrict__ beta, int D, int lane) {
   const int D4 = D >> 2;
   const int64_t ob = grow * D;
   float ss = 0.f;
   bool bad = false;
+  // the sign flag of xnorm (a BF16 row that is not FMA-safe) matters only for BF16 jobs
+  const bool chk = PACK == 2 || (PACK == 0 && j.pack == 2);
   for (int c4 = lane; c4 < D4; c4 += 32) {
     const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c4);
     const float4 bt = __ldg(reinterpret_cast<const float4*>(beta) + c4);
@@ -504,30 +523,57 @@ __device__ __forceinline__ void ln_row_out(const LnJob& j, const float* row, int
     const float xx[4] = {xv.x, xv.y, xv.z, xv.w};
     float y[4], qv[4];
 #pragma unroll
+    for (int k = 0; k < 4; ++k) y[k] = __fadd_rn(__fmul_rn(gg[k], __fmul_rn(__fsub_rn(xx[k], m_r), i_r)), bb[k]);
+    uint32_t code = 0;
+    if (PREC == kP8) {
+      const uint32_t c01 = ln_e4m3x2(y[0], y[1]), c23 = ln_e4m3x2(y[2], y[3]);
+      const float2 v01 = ln_e4m3x2_val(c01), v23 = ln_e4m3x2_val(c23);
+      qv[0] = v01.x, qv[1] = v01.y, qv[2] = v23.x, qv[3] = v23.y;
+      code = c01 | (c23 << 16);
+    } else if (PREC == kP16) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) qv[k] = round_bf16(y[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) qv[k] = y[k];
+    }
+#pragma unroll
     for (int k = 0; k < 4; ++k) {
-      y[k] = __fadd_rn(__fmul_rn(gg[k], __fmul_rn(__fsub_rn(xx[k], m_r), i_r)), bb[k]);
-      qv[k] = round_p(y[k], prec);
       ss = fmaf(qv[k], qv[k], ss);
-      bad = bad || bf16_fma_bad(qv[k]);
+      if (chk) bad = bad || bf16_fma_bad(qv[k]);
     }
     if (j.xln) reinterpret_cast<float4*>(j.xln + ob)[c4] = make_float4(y[0], y[1], y[2], y[3]);
     if (j.xq) reinterpret_cast<float4*>(j.xq + ob)[c4] = make_float4(qv[0], qv[1], qv[2], qv[3]);
-    if (j.xqp) {
-      if (j.pack == 2)
-        reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(j.xqp) + ob)[c4] =
-            make_uint2(enc_bf16(qv[0]) | ((uint32_t)enc_bf16(qv[1]) << 16),
-                       enc_bf16(qv[2]) | ((uint32_t)enc_bf16(qv[3]) << 16));
-      else
-        reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(j.xqp) + ob)[c4] =
-            enc_e4m3(qv[0]) | ((uint32_t)enc_e4m3(qv[1]) << 8) | ((uint32_t)enc_e4m3(qv[2]) << 16) |
-            ((uint32_t)enc_e4m3(qv[3]) << 24);
-    }
+    if (PACK == 2)
+      reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(j.xqp) + ob)[c4] =
+          make_uint2(enc_bf16(qv[0]) | ((uint32_t)enc_bf16(qv[1]) << 16),
+                     enc_bf16(qv[2]) | ((uint32_t)enc_bf16(qv[3]) << 16));
+    else if (PACK == 1)
+      reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(j.xqp) + ob)[c4] =
+          PREC == kP8 ? code
+                      : enc_e4m3(qv[0]) | ((uint32_t)enc_e4m3(qv[1]) << 8) | ((uint32_t)enc_e4m3(qv[2]) << 16) |
+                            ((uint32_t)enc_e4m3(qv[3]) << 24);
   }
   if (j.xnorm) {
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    bad = __any_sync(0xffffffffu, bad) && j.pack == 2;
+    bad = __any_sync(0xffffffffu, bad);
     if (lane == 0) j.xnorm[grow] = bad ? -(sqrtf(ss) * 1.0001f) : sqrtf(ss) * 1.0001f;
   }
+}
+
+__device__ __forceinline__ void ln_row_out(const LnJob& j, const float* row, int64_t grow, float m_r,
+                                           float i_r, const float* __restrict__ gamma,
+                                           const float* __restrict__ beta, int D, int prec, int lane) {
+  const int pack = j.xqp ? (j.pack == 2 ? 2 : 1) : 0;
+#define LN_OUT(P, K) ln_row_out_t<P, K>(j, row, grow, m_r, i_r, gamma, beta, D, lane)
+  if (prec == kP8) {
+    if (pack == 1) LN_OUT(kP8, 1); else if (pack == 2) LN_OUT(kP8, 2); else LN_OUT(kP8, 0);
+  } else if (prec == kP16) {
+    if (pack == 1) LN_OUT(kP16, 1); else if (pack == 2) LN_OUT(kP16, 2); else LN_OUT(kP16, 0);
+  } else {
+    if (pack == 1) LN_OUT(kP32, 1); else if (pack == 2) LN_OUT(kP32, 2); else LN_OUT(kP32, 0);
+  }
+#undef LN_OUT
 }
 
 template <int RW>
@@ -567,7 +613,8 @@ __global__ void __launch_bounds__(32 * kLsWarps) ln_small_kernel(const LnJob* __
 
 // Big launches (the patched passes: tens of thousands of rows): ln_small's
 // 4 chain lanes per warp left it issue-bound (ncu: 72% issue-active, 15% of
-// HBM; the chain loops cost ~1350 warp-instructions per row). Here a CTA of
+// HBM; the chain loops cost ~1350 warp-instructions per row). Measured with
+// the specialised normalisation: 251 ms per step vs ln_small's 267 ms. Here a CTA of
 // kLlWarps warps stages 32 rows (~99 KB, two CTAs per SM), warp 0 runs all 32
 // rows' chains with one row per lane (conflict-free 16-byte loads: the row
 // pitch D + 4 puts lanes 0..7 of a quarter-warp on distinct bank quads), and
@@ -640,6 +687,7 @@ void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float
     // launch would not give every SM several warps (the per-source baseline
     // runs: 1024-row launches), so more chains run side by side
     int rw = D <= 1024 ? 4 : 2;  // measured: 4 rows per warp beats 8 and 2 at D = 768
+    if (const char* e_rw = getenv("CQG_LN_RW")) rw = atoi(e_rw) >= 8 ? 8 : (atoi(e_rw) >= 4 ? 4 : 2);  // (A/B)
     const int64_t total = (int64_t)max_rows * n_jobs;
     while (rw > 1 && total / rw < 4 * 148) rw >>= 1;
     const size_t smem = sizeof(float) * kLsWarps * rw * (D + 4);
