@@ -16,6 +16,12 @@ int cqg_diag_bf16_range(uint32_t lo, uint64_t count, uint16_t* out_host);
 /* which: 0 glibc-exact expf, 1 glibc-exact erff, 2 reference gelu
  * (kernels.cpp:226). */
 int cqg_diag_libm_range(int which, uint32_t lo, uint64_t count, float* out_host);
+/* The W_in epilogue's GELU of every BF16 code: out_lut = the full
+ * device-built table (round_bf16(gelu(x)), kernels.cpp:221-234, glibc-exact
+ * erff), out_code = gelu_code (shared-memory slice + closed forms),
+ * out_fast = the fast path's slice lookup for codes inside the slice
+ * (|x| in [2^-24, 8)), 0 elsewhere. */
+int cqg_diag_gelu_codes(uint16_t* out_lut, uint16_t* out_code, uint16_t* out_fast);
 /* One tensor-core GEMM C = round(A . B^T) (A: M x K, Bt: N x K, values on
  * the elem grid: 0 E4M3, 1 BF16) through the production tcgen05 kernel +
  * exactness fixup, and the same product through the exact sequential SIMT

@@ -28,6 +28,19 @@ int cqg_diag_e4m3_range(uint32_t lo, uint64_t count, uint8_t* out) {
 int cqg_diag_bf16_range(uint32_t lo, uint64_t count, uint16_t* out) {
   return run(count, out, [&](uint16_t* d) { cqg::launch_bf16_all(d, lo, count, 0); });
 }
+int cqg_diag_gelu_codes(uint16_t* out_lut, uint16_t* out_code, uint16_t* out_fast) {
+  uint16_t *lut, *o1, *o2;
+  if (cudaMalloc(&lut, 3 * 65536 * 2) != cudaSuccess) return 3;
+  o1 = lut + 65536, o2 = lut + 2 * 65536;
+  cqg::launch_gelu_lut(lut, 0);
+  cqg::launch_gelu_codes(lut, o1, o2, 0);
+  cudaError_t e = cudaMemcpy(out_lut, lut, 65536 * 2, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(out_code, o1, 65536 * 2, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(out_fast, o2, 65536 * 2, cudaMemcpyDeviceToHost);
+  cudaFree(lut);
+  return e == cudaSuccess ? 0 : 2;
+}
+
 int cqg_diag_libm_range(int which, uint32_t lo, uint64_t count, float* out) {
   return run(count, out, [&](float* d) { cqg::launch_libm_all(d, lo, count, which, 0); });
 }

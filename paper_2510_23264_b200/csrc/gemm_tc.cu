@@ -49,7 +49,8 @@ __host__ __device__ constexpr int split_of(int elem, int prec) { return elem == 
 __device__ __forceinline__ int split_kh(int nk) { return (nk + 1) >> 1; }
 constexpr size_t kSmemBytes = 1024 + (size_t)kStages * (kAStage + kBStage) + 256 +
                               kEpiWarps * kStageFloats * sizeof(float) + kAccBufs * kMetaBytes +
-                              2 * 2 * 13 * 128;  // GELU LUT slice (kGeluSm uint16)
+                              2 * 2 * 27 * 128;  // GELU LUT slice (kGeluSm uint16)
+static_assert(kSmemBytes <= 227 * 1024, "tcgen05 GEMM shared memory");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -238,15 +239,24 @@ __device__ __forceinline__ bool bf16_ambiguous(float acc, float m) {
   const float dl = __uint_as_float(ab) - __uint_as_float(ab & 0xFFFF0000u);
   const float h = __uint_as_float((ab & 0x7F800000u) - (8u << 23));  // 2^(e-8)
   const bool odd = ab >= 0x7F800000u || ab < (32u << 23);
-  return odd | !(fabsf(dl - h) > m * 1.001f);  // (covers the FP32 rounding of m)
+  return odd | !(fabsf(dl - h) > m);  // m carries the 1.001 guard for its own FP32 rounding
+}
+
+// RNE of an FP32 value to its BF16 grid (integer form). No NaN special case:
+// a NaN accumulator is always flagged (bf16_ambiguous: odd) and its element
+// recomputed and stored by the exact fixup.
+__device__ __forceinline__ float rne_bf16_bits(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return __uint_as_float((u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u);
 }
 
 // round_bf16 of a GELU input's code through the shared-memory slice of the
-// LUT (|x| in [2^-10, 8), both signs) and the closed forms outside it
+// LUT (|x| in [2^-24, 8), both signs) and the closed forms outside it
 // (checked against the full table for all 2^16 codes): x >= 8 -> x,
 // x <= -8 -> -0, |x| < 2^-10 -> round_bf16(0.5 x); Inf / NaN via the table.
-constexpr int kGeluE0 = 117, kGeluNE = 13;
+constexpr int kGeluE0 = 103, kGeluNE = 27;
 constexpr int kGeluSm = 2 * kGeluNE * 128;
+static_assert(2 * kGeluSm == 2 * 2 * 27 * 128, "kSmemBytes holds the GELU slice");
 __device__ __forceinline__ uint32_t gelu_code(uint32_t c, const uint16_t* lut_s, const uint16_t* lut_g) {
   const uint32_t E = (c >> 7) & 0xFFu;
   const uint32_t t = E - kGeluE0;
@@ -334,6 +344,7 @@ __device__ __forceinline__ uint32_t epilogue16(const TcLaunch& L, const TileMeta
   } else if (PREC == 1 && ncol > 0) {
     // BF16: RNE by integer add, certificate in integer form
     const float nas = na / sk;
+    const float ku1 = ku * 1.001f;  // (the guard for the FP32 rounding of the margin)
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {
       const float4 t4 = *reinterpret_cast<const float4*>(md.nb + c0 + j);
@@ -341,10 +352,10 @@ __device__ __forceinline__ uint32_t epilogue16(const TcLaunch& L, const TileMeta
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const float acc = __uint_as_float(r[j + t]);
-        v[j + t] = round_bf16(acc);
+        v[j + t] = rne_bf16_bits(acc);
         float sc = fabsf(acc);
         if (kSplitE == 2) sc = fmaxf(sc, h1[(j + t) & (kSplitE == 2 ? 15 : 0)]);
-        const float m = ku * fmaxf(sc, nas * nb4[t]);
+        const float m = ku1 * fmaxf(sc, nas * nb4[t]);
         if (bf16_ambiguous(acc, m)) fl |= 1u << (j + t);
       }
     }
@@ -383,9 +394,26 @@ __device__ __forceinline__ uint32_t epilogue16(const TcLaunch& L, const TileMeta
   }
   if (EPI == 1 && ncol > 0) {
     if (PREC == 1) {
+      // fast path: every code of the 16 inside the shared-memory slice
+      // (|x| in [2^-24, 8): all but ~1e-7 of the pre-activations) -> one
+      // lookup each; otherwise gelu_code's closed forms
+      uint32_t u[16];
+      bool all_in = true;
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        v[j] = __uint_as_float(gelu_code(__float_as_uint(v[j]) >> 16, gelu_s, L.gelu_lut) << 16);
+      for (int j = 0; j < 16; ++j) {
+        u[j] = (__float_as_uint(v[j]) >> 16 & 0x7FFFu) - (uint32_t)(kGeluE0 * 128);
+        all_in = all_in && u[j] < (uint32_t)(kGeluNE * 128);
+      }
+      if (all_in) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          v[j] = __uint_as_float(
+              (uint32_t)gelu_s[u[j] + (__float_as_uint(v[j]) >> 31) * (uint32_t)(kGeluNE * 128)] << 16);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          v[j] = __uint_as_float(gelu_code(__float_as_uint(v[j]) >> 16, gelu_s, L.gelu_lut) << 16);
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = round_out(gelu_ref(v[j]), PREC);
@@ -556,7 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* stage_all = reinterpret_cast<float*>(smem + kStages * (kAStage + kBStage) + 256);
   TileMeta* meta = reinterpret_cast<TileMeta*>(stage_all + (size_t)kEpiWarps * kStageFloats);
   uint16_t* gelu_s = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(meta) + kAccBufs * kMetaBytes);
-  if (EPI == 1 && PREC == 1)  // the GELU LUT slice |x| in [2^-10, 8) (made visible by the barrier below)
+  if (EPI == 1 && PREC == 1)  // the GELU LUT slice |x| in [2^-24, 8) (made visible by the barrier below)
     for (int i = threadIdx.x; i < kGeluSm; i += blockDim.x) {
       const int sg = i / (kGeluNE * 128), rem = i % (kGeluNE * 128);
       gelu_s[i] = L.gelu_lut[(sg << 15) | ((kGeluE0 + rem / 128) << 7) | (rem % 128)];
@@ -1674,6 +1702,28 @@ void launch_gemm_fixup_blk(const TcLaunch& L, const TcJob* d_jobs, cudaStream_t 
 }
 
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st) { gelu_lut_kernel<<<256, 256, 0, st>>>(lut); }
+
+// (diagnostics) the epilogue's GELU of all 2^16 BF16 codes: the shared-memory
+// slice built as in gemm_tc_kernel, out[c] = gelu_code(c) (closed forms +
+// slice), out_fast[c] = the fast path's lookup for codes inside the slice
+// (0 elsewhere); both must equal the full table lut[c].
+__global__ void gelu_codes_kernel(const uint16_t* lut, uint16_t* out, uint16_t* out_fast) {
+  __shared__ uint16_t gs[kGeluSm];
+  for (int i = threadIdx.x; i < kGeluSm; i += blockDim.x) {
+    const int sg = i / (kGeluNE * 128), rem = i % (kGeluNE * 128);
+    gs[i] = lut[(sg << 15) | ((kGeluE0 + rem / 128) << 7) | (rem % 128)];
+  }
+  __syncthreads();
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < 65536; c += gridDim.x * blockDim.x) {
+    out[c] = (uint16_t)gelu_code((uint32_t)c, gs, lut);
+    const uint32_t u = ((uint32_t)c & 0x7FFFu) - (uint32_t)(kGeluE0 * 128);
+    out_fast[c] = u < (uint32_t)(kGeluNE * 128) ? gs[u + ((uint32_t)c >> 15) * (uint32_t)(kGeluNE * 128)] : 0;
+  }
+}
+
+void launch_gelu_codes(const uint16_t* lut, uint16_t* out, uint16_t* out_fast, cudaStream_t st) {
+  gelu_codes_kernel<<<64, 256, 0, st>>>(lut, out, out_fast);
+}
 
 void launch_split_rows(const float* x, int rows, int D, int ldx, uint16_t* out, float* anorm,
                        cudaStream_t st) {

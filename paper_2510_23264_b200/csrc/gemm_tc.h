@@ -95,6 +95,7 @@ bool tc_make_map_sw32(CUtensorMap* map, const void* base, uint64_t rows, uint64_
                       uint64_t pitch_bytes);
 // lut[b] = enc_bf16(round_bf16(gelu_ref(dec_bf16(b)))) (glibc-exact erff)
 void launch_gelu_lut(uint16_t* lut, cudaStream_t st);
+void launch_gelu_codes(const uint16_t* lut, uint16_t* out, uint16_t* out_fast, cudaStream_t st);
 // ||row|| of a packed [rows][K] operand (elements starting at col k0)
 void launch_rownorm(const uint8_t* A, int64_t lda, int elem, int rows, int k0, int K, float* out,
                     cudaStream_t st);

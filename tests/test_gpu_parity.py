@@ -164,6 +164,22 @@ def test_forward_bitexact(cfg, ln_lane, monkeypatch):
     e.close()
 
 
+def test_epilogue_gelu_codes_exhaustive():
+    """The tcgen05 W_in epilogue's GELU (gemm_tc.cu gelu_code and its
+    shared-memory fast path) equals the full device table for all 2^16 BF16
+    codes (the table itself is pinned by test_glibc_libm_restatements_exhaustive)."""
+    lib = eng.load_library()
+    lut, code, fast = (np.zeros(65536, np.uint16) for _ in range(3))
+    v = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    lib.cqg_diag_gelu_codes.argtypes = [C.c_void_p] * 3
+    assert lib.cqg_diag_gelu_codes(v(lut), v(code), v(fast)) == 0
+    assert np.array_equal(code, lut)
+    c = np.arange(65536, dtype=np.uint32)
+    inside = ((c & 0x7FFF) >> 7 >= 103) & ((c & 0x7FFF) >> 7 < 130)
+    assert inside.sum() == 2 * 27 * 128
+    assert np.array_equal(fast[inside], lut[inside])
+
+
 # --- tensor-core GEMM with the exactness certificate + fixup -----------------------
 def _tc_gemm(elem, prec, epi, A, Bt):
     lib = eng.load_library()
