@@ -271,6 +271,17 @@ __device__ __forceinline__ uint32_t gelu_code(uint32_t c, const uint16_t* lut_s,
   return r;
 }
 
+// The rare half-chunks with a code outside the slice: out of line, so the
+// closed forms' registers do not weigh on the fast path's allocation
+struct F16 {
+  float x[16];
+};
+__device__ __noinline__ F16 gelu16_slow(F16 v, const uint16_t* gelu_s, const uint16_t* lut) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v.x[j] = __uint_as_float(gelu_code(__float_as_uint(v.x[j]) >> 16, gelu_s, lut) << 16);
+  return v;
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
@@ -410,9 +421,12 @@ __device__ __forceinline__ uint32_t epilogue16(const TcLaunch& L, const TileMeta
           v[j] = __uint_as_float(
               (uint32_t)gelu_s[u[j] + (__float_as_uint(v[j]) >> 31) * (uint32_t)(kGeluNE * 128)] << 16);
       } else {
+        F16 t;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          v[j] = __uint_as_float(gelu_code(__float_as_uint(v[j]) >> 16, gelu_s, L.gelu_lut) << 16);
+        for (int j = 0; j < 16; ++j) t.x[j] = v[j];
+        t = gelu16_slow(t, gelu_s, L.gelu_lut);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = t.x[j];
       }
     } else {
 #pragma unroll
