@@ -1457,16 +1457,40 @@ __global__ void __launch_bounds__(128) attention_warp_kernel(const AttnJob* __re
     pr[i * lds + j] = __fmul_rn(acc, scale);
   }
   __syncwarp();
+  // softmax per query row (kernels.cpp:167-219 order: max, exp, sequential
+  // den, divide). The max and the den chains run one row per lane; the exps
+  // and the divisions are independent per (i, j) and run over the causal
+  // pairs, all lanes busy (row i's max / den parked in its spare column S).
   for (int i = q0 + lane; i < S; i += 32) {
-    float* p = pr + i * lds;
+    const float* p = pr + i * lds;
     float mx = -INFINITY;
     for (int j = 0; j <= i; ++j) mx = (mx < p[j]) ? p[j] : mx;
+    pr[i * lds + S] = mx;
+  }
+  __syncwarp();
+  for (int pi = lane; pi < np; pi += 32) {
+    const int pp = p0 + pi;
+    int i = (int)((sqrtf(8.f * pp + 1.f) - 1.f) * 0.5f);
+    while (i * (i + 1) / 2 > pp) --i;
+    while ((i + 1) * (i + 2) / 2 <= pp) ++i;
+    const int j = pp - i * (i + 1) / 2;
+    pr[i * lds + j] = glibc_expf(__fsub_rn(pr[i * lds + j], pr[i * lds + S]));
+  }
+  __syncwarp();
+  for (int i = q0 + lane; i < S; i += 32) {
+    const float* p = pr + i * lds;
     float den = 0.f;
-    for (int j = 0; j <= i; ++j) {
-      p[j] = glibc_expf(__fsub_rn(p[j], mx));
-      den = __fadd_rn(den, p[j]);
-    }
-    for (int j = 0; j <= i; ++j) p[j] = __fdiv_rn(p[j], den);
+    for (int j = 0; j <= i; ++j) den = __fadd_rn(den, p[j]);
+    pr[i * lds + S] = den;
+  }
+  __syncwarp();
+  for (int pi = lane; pi < np; pi += 32) {
+    const int pp = p0 + pi;
+    int i = (int)((sqrtf(8.f * pp + 1.f) - 1.f) * 0.5f);
+    while (i * (i + 1) / 2 > pp) --i;
+    while ((i + 1) * (i + 2) / 2 <= pp) ++i;
+    const int j = pp - i * (i + 1) / 2;
+    pr[i * lds + j] = __fdiv_rn(pr[i * lds + j], pr[i * lds + S]);
   }
   __syncwarp();
   for (int i = q0; i < S; ++i) {
