@@ -1443,18 +1443,32 @@ __global__ void __launch_bounds__(128) attention_warp_kernel(const AttnJob* __re
   const float scale = __fdiv_rn(1.0f, __fsqrt_rn((float)dk));
   // scores for the causal pairs (i, j <= i), i >= q0
   const int p0 = q0 * (q0 + 1) / 2, np = S * (S + 1) / 2 - p0;
-  for (int pi = lane; pi < np; pi += 32) {
-    const int pp = p0 + pi;
-    int i = (int)((sqrtf(8.f * pp + 1.f) - 1.f) * 0.5f);
+  // two pairs per lane at a time (independent chains: twice the ILP of the
+  // FADD-latency-bound dot products; each chain keeps dot_col's order)
+  auto pair_ij = [&](int pp, int& i, int& j) {
+    i = (int)((sqrtf(8.f * pp + 1.f) - 1.f) * 0.5f);
     while (i * (i + 1) / 2 > pp) --i;
     while ((i + 1) * (i + 2) / 2 <= pp) ++i;
-    const int j = pp - i * (i + 1) / 2;
-    const float* qi = q + i * ldk;
-    const float* kj = k + j * ldk;
-    float acc = 0.f;
+    j = pp - i * (i + 1) / 2;
+  };
+  for (int pa = lane; pa < np; pa += 64) {
+    const int pb = pa + 32;
+    const bool two = pb < np;
+    int ia, ja, ib, jb2;
+    pair_ij(p0 + pa, ia, ja);
+    pair_ij(p0 + (two ? pb : pa), ib, jb2);
+    const float* qa = q + ia * ldk;
+    const float* ka = k + ja * ldk;
+    const float* qb = q + ib * ldk;
+    const float* kb = k + jb2 * ldk;
+    float acc_a = 0.f, acc_b = 0.f;
 #pragma unroll 16
-    for (int t = 0; t < dk; ++t) acc = __fadd_rn(acc, __fmul_rn(qi[t], kj[t]));
-    pr[i * lds + j] = __fmul_rn(acc, scale);
+    for (int t = 0; t < dk; ++t) {
+      acc_a = __fadd_rn(acc_a, __fmul_rn(qa[t], ka[t]));
+      acc_b = __fadd_rn(acc_b, __fmul_rn(qb[t], kb[t]));
+    }
+    pr[ia * lds + ja] = __fmul_rn(acc_a, scale);
+    if (two) pr[ib * lds + jb2] = __fmul_rn(acc_b, scale);
   }
   __syncwarp();
   // softmax per query row (kernels.cpp:167-219 order: max, exp, sequential
@@ -1493,28 +1507,55 @@ __global__ void __launch_bounds__(128) attention_warp_kernel(const AttnJob* __re
     pr[i * lds + j] = __fdiv_rn(pr[i * lds + j], pr[i * lds + S]);
   }
   __syncwarp();
-  for (int i = q0; i < S; ++i) {
-    const float* p = pr + i * lds;
-    float acc[NT];
+  // P.V: two query rows per iteration (rows i and i + 1: independent chains
+  // and interleaved row-norm reductions); each chain is j ascending
+  for (int i0 = q0; i0 < S; i0 += 2) {
+    const bool two = i0 + 1 < S;
+    const int i1 = two ? i0 + 1 : i0;
+    const float* p0r = pr + i0 * lds;
+    const float* p1r = pr + i1 * lds;
+    float acc0[NT], acc1[NT];
 #pragma unroll
-    for (int c = 0; c < NT; ++c) acc[c] = 0.f;
-    for (int j = 0; j <= i; ++j) {
-      const float pj = p[j];
+    for (int c = 0; c < NT; ++c) acc0[c] = 0.f, acc1[c] = 0.f;
+    for (int j = 0; j <= i0; ++j) {
+      const float pj0 = p0r[j], pj1 = p1r[j];
 #pragma unroll
-      for (int c = 0; c < NT; ++c) acc[c] = __fadd_rn(acc[c], __fmul_rn(pj, v[j * ldk + lane + 32 * c]));
+      for (int c = 0; c < NT; ++c) {
+        const float vj = v[j * ldk + lane + 32 * c];
+        acc0[c] = __fadd_rn(acc0[c], __fmul_rn(pj0, vj));
+        acc1[c] = __fadd_rn(acc1[c], __fmul_rn(pj1, vj));
+      }
     }
-    const int64_t zr = (int64_t)item * (S - q0) + (i - q0);
-    float ss = 0.f;
+    if (two) {  // row i1's last term (j = i1)
+      const float pj1 = p1r[i1];
+#pragma unroll
+      for (int c = 0; c < NT; ++c) acc1[c] = __fadd_rn(acc1[c], __fmul_rn(pj1, v[i1 * ldk + lane + 32 * c]));
+    }
+    float ss0 = 0.f, ss1 = 0.f;
+    const int64_t zr0 = (int64_t)item * (S - q0) + (i0 - q0), zr1 = zr0 + 1;
 #pragma unroll
     for (int c = 0; c < NT; ++c) {
-      const float zv = round_p(acc[c], jb.prec);
-      if (jb.z) jb.z[zr * jb.ldz + lane + 32 * c] = zv;
-      if (jb.z8) jb.z8[zr * jb.ldz + lane + 32 * c] = enc_e4m3(zv);
-      ss = fmaf(zv, zv, ss);
+      const float z0 = round_p(acc0[c], jb.prec), z1 = round_p(acc1[c], jb.prec);
+      if (jb.z) {
+        jb.z[zr0 * jb.ldz + lane + 32 * c] = z0;
+        if (two) jb.z[zr1 * jb.ldz + lane + 32 * c] = z1;
+      }
+      if (jb.z8) {
+        jb.z8[zr0 * jb.ldz + lane + 32 * c] = enc_e4m3(z0);
+        if (two) jb.z8[zr1 * jb.ldz + lane + 32 * c] = enc_e4m3(z1);
+      }
+      ss0 = fmaf(z0, z0, ss0);
+      ss1 = fmaf(z1, z1, ss1);
     }
     if (jb.znorm) {  // the row norm rownorm_kernel would compute (E4M3: no FMA-safety bit)
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (lane == 0) jb.znorm[zr] = sqrtf(ss) * 1.0001f;
+      for (int o = 16; o > 0; o >>= 1) {
+        ss0 += __shfl_xor_sync(0xffffffffu, ss0, o);
+        ss1 += __shfl_xor_sync(0xffffffffu, ss1, o);
+      }
+      if (lane == 0) {
+        jb.znorm[zr0] = sqrtf(ss0) * 1.0001f;
+        if (two) jb.znorm[zr1] = sqrtf(ss1) * 1.0001f;
+      }
     }
   }
 }
