@@ -613,17 +613,19 @@ __global__ void __launch_bounds__(32 * kLsWarps) ln_small_kernel(const LnJob* __
 
 // Big launches (the patched passes: tens of thousands of rows): ln_small's
 // 4 chain lanes per warp left it issue-bound (ncu: 72% issue-active, 15% of
-// HBM; the chain loops cost ~1350 warp-instructions per row). Measured with
-// the specialised normalisation: 251 ms per step vs ln_small's 267 ms. Here a CTA of
-// kLlWarps warps stages 32 rows (~99 KB, two CTAs per SM), warp 0 runs all 32
-// rows' chains with one row per lane (conflict-free 16-byte loads: the row
-// pitch D + 4 puts lanes 0..7 of a quarter-warp on distinct bank quads), and
-// every warp then normalises a share of the rows. The chain phase of one CTA
-// overlaps the loads and normalisation of the other. Same arithmetic as
-// ln_small_kernel (ln_row_stats / ln_row_out): bit-identical outputs.
+// HBM; the chain loops cost ~1350 warp-instructions per row). Here a CTA of
+// kLlWarps warps stages ROWS rows, warp 0 runs all their chains with one row
+// per lane (conflict-free 16-byte loads: the row pitch D + 4 puts lanes 0..7
+// of a quarter-warp on distinct bank quads), and every warp then normalises
+// a share of the rows. The chain phase of one CTA overlaps the loads and
+// normalisation of the others. ROWS = 24 (74 KB, three CTAs per SM: 228 ms
+// per step) by default, 32 (99 KB, two CTAs: 251 ms) with
+// CQG_LN_LANE_ROWS=32; ln_small: 267 ms. Same arithmetic as ln_small_kernel
+// (ln_row_stats / ln_row_out): bit-identical outputs.
 constexpr int kLlWarps = 4, kLlRows = 32;
 constexpr size_t smem_cap_ll() { return sizeof(float) * kLlRows * (1024 + 4); }
 
+template <int kLlRows>
 __global__ void __launch_bounds__(32 * kLlWarps) ln_lane_kernel(const LnJob* __restrict__ jobs,
                                                                 const float* __restrict__ gamma,
                                                                 const float* __restrict__ beta, int D,
@@ -670,15 +672,21 @@ void launch_layernorm(const LnJob* d_jobs, int n_jobs, int max_rows, const float
   const char* e = getenv("CQG_LN_LANE_MIN");
   const int64_t ll_min_rows = e ? atoll(e) : 4 * kLlRows * 148;
   if ((D & 3) == 0 && D <= 1024 && ll_min_rows > 0 && total_rows >= ll_min_rows) {
-    const size_t smem = sizeof(float) * kLlRows * (D + 4);
+    // rows per CTA: 24 (three CTAs per SM; measured 228 ms per step) or,
+    // CQG_LN_LANE_ROWS=32, 32 (two CTAs per SM; 251 ms)
+    const char* er = getenv("CQG_LN_LANE_ROWS");
+    const int rows = er && atoi(er) == 32 ? 32 : 24;
+    const size_t smem = sizeof(float) * rows * (D + 4);
     static bool attr_l = false;
     if (!attr_l) {
-      cudaFuncSetAttribute(ln_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap_ll());
+      cudaFuncSetAttribute(ln_lane_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap_ll());
+      cudaFuncSetAttribute(ln_lane_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap_ll());
       attr_l = true;
     }
     for (int y0 = 0; y0 < n_jobs; y0 += 65535) {
-      dim3 grid((max_rows + kLlRows - 1) / kLlRows, (unsigned)std::min(65535, n_jobs - y0));
-      ln_lane_kernel<<<grid, 32 * kLlWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
+      dim3 grid((max_rows + rows - 1) / rows, (unsigned)std::min(65535, n_jobs - y0));
+      if (rows == 24) ln_lane_kernel<24><<<grid, 32 * kLlWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
+      else ln_lane_kernel<32><<<grid, 32 * kLlWarps, smem, st>>>(d_jobs + y0, gamma, beta, D, prec);
     }
     return;
   }
