@@ -110,6 +110,56 @@ __device__ __forceinline__ void load_out16(const void* b, int t, int64_t i, floa
   }
 }
 
+// Raw bytes of one op's 16 node-output elements (F32: 4 x 16 B, BF16: 2, E4M3: 1).
+struct Raw16 { uint4 q[4]; };
+
+__device__ __forceinline__ void load_raw16(const void* b, int t, int64_t i, Raw16& r) {
+  const uint4* p = reinterpret_cast<const uint4*>(b);
+  if (t == kOutF32) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) r.q[q] = __ldg(p + 4 * i + q);
+  } else if (t == kOutE4M3) {
+    r.q[0] = __ldg(p + i);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) r.q[q] = __ldg(p + 2 * i + q);
+  }
+}
+
+__device__ __forceinline__ void decode_raw16(const Raw16& r, int t, float (&v)[16]) {
+  if (t == kOutF32) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      v[4 * q] = __uint_as_float(r.q[q].x), v[4 * q + 1] = __uint_as_float(r.q[q].y);
+      v[4 * q + 2] = __uint_as_float(r.q[q].z), v[4 * q + 3] = __uint_as_float(r.q[q].w);
+    }
+  } else if (t == kOutE4M3) {
+    const uint32_t ww[4] = {r.q[0].x, r.q[0].y, r.q[0].z, r.q[0].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 lo = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(ww[q] & 0xFFFFu), __NV_E4M3)));
+      const float2 hi = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(ww[q] >> 16), __NV_E4M3)));
+      v[4 * q] = lo.x, v[4 * q + 1] = lo.y, v[4 * q + 2] = hi.x, v[4 * q + 3] = hi.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t ww[4] = {r.q[q].x, r.q[q].y, r.q[q].z, r.q[q].w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        v[8 * q + 2 * h] = __uint_as_float(ww[h] << 16);
+        v[8 * q + 2 * h + 1] = __uint_as_float(ww[h] & 0xFFFF0000u);
+      }
+    }
+  }
+}
+
+// kPipe: the next op's node-output bytes are loaded before this op's prefix
+// store, so one op's HBM/L2 latency overlaps the previous op's add + store
+// (the compiler cannot hoist them itself: the dst store may alias as far as it
+// knows). Node outputs are read-only during a fold (they were already read
+// with ld.global.nc), so the reordering does not change any value.
+template <bool kPipe>
 __global__ void __launch_bounds__(256) fold16_kernel(const FoldOp* __restrict__ ops,
                                                      const FoldProg* __restrict__ progs,
                                                      int64_t n_elems) {
@@ -120,11 +170,27 @@ __global__ void __launch_bounds__(256) fold16_kernel(const FoldOp* __restrict__ 
     float r[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) r[k] = 0.f;
+    Raw16 nxt;
+    int tn = 0;
+    if (kPipe && p.op_begin < p.op_end) {
+      tn = ops[p.op_begin].btype;
+      load_raw16(ops[p.op_begin].b, tn, i, nxt);
+    }
     for (int o = p.op_begin; o < p.op_end; ++o) {
       const float* a = ops[o].a;
       float* d = ops[o].dst;
       float bv[16];
-      load_out16(ops[o].b, ops[o].btype, i, bv);
+      if (kPipe) {
+        const Raw16 cur = nxt;
+        const int tc = tn;
+        if (o + 1 < p.op_end) {
+          tn = ops[o + 1].btype;
+          load_raw16(ops[o + 1].b, tn, i, nxt);
+        }
+        decode_raw16(cur, tc, bv);
+      } else {
+        load_out16(ops[o].b, ops[o].btype, i, bv);
+      }
       if (a != CQG_REG_PREV) {
         if (a == nullptr) {
 #pragma unroll
@@ -147,6 +213,15 @@ __global__ void __launch_bounds__(256) fold16_kernel(const FoldOp* __restrict__ 
   }
 }
 
+// CQG_FOLD_PIPE=1 selects the pipelined fold. Measured slower (fold 352 ->
+// 475 ms per step, profiles/r2_fold_pipe_ab_*.json): the extra raw buffer
+// takes the kernel from 48 to 70 registers, 5 -> 3 CTAs per SM, and the lost
+// warps cost more latency hiding than the one-op lookahead gains. Off by default.
+static bool fold_pipe() {
+  const char* e = getenv("CQG_FOLD_PIPE");
+  return e && e[0] == '1';
+}
+
 void launch_fold(const FoldOp* d_ops, const FoldProg* d_progs, int n_progs, int64_t n_elems,
                  cudaStream_t st) {
   if (n_progs <= 0) return;
@@ -154,7 +229,8 @@ void launch_fold(const FoldOp* d_ops, const FoldProg* d_progs, int n_progs, int6
     int gx = (int)std::min<int64_t>((n_elems / 16 + 255) / 256, 4096);
     for (int y0 = 0; y0 < n_progs; y0 += 65535) {
       dim3 grid(gx, (unsigned)std::min(65535, n_progs - y0));
-      fold16_kernel<<<grid, 256, 0, st>>>(d_ops, d_progs + y0, n_elems);
+      if (fold_pipe()) fold16_kernel<true><<<grid, 256, 0, st>>>(d_ops, d_progs + y0, n_elems);
+      else fold16_kernel<false><<<grid, 256, 0, st>>>(d_ops, d_progs + y0, n_elems);
     }
     return;
   }

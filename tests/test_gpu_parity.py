@@ -131,11 +131,14 @@ def test_int8_images_bitexact(cfg):
 
 # --- forward (model.cpp:556-757), bitwise --------------------------------------
 @pytest.mark.parametrize("cfg,ln_lane", [(TINY, 0), (SMALL, 0), (TOY, 0), (SMALL, 24), (TOY, 24),
-                                         (SMALL, 32), (TOY, 32)])
+                                         (SMALL, 32), (TOY, 32), (SMALL, -1), (TOY, -1)])
 def test_forward_bitexact(cfg, ln_lane, monkeypatch):
     """(ln_lane: every layer norm through ln_lane_kernel with 24 or 32 rows
-    per CTA, CQG_LN_LANE_MIN=1, CQG_LN_LANE_ROWS)"""
-    if ln_lane:
+    per CTA, CQG_LN_LANE_MIN=1, CQG_LN_LANE_ROWS; -1: the pipelined fold
+    option, CQG_FOLD_PIPE=1)"""
+    if ln_lane < 0:
+        monkeypatch.setenv("CQG_FOLD_PIPE", "1")
+    elif ln_lane:
         monkeypatch.setenv("CQG_LN_LANE_MIN", "1")
         monkeypatch.setenv("CQG_LN_LANE_ROWS", str(ln_lane))
     w, ds = make(cfg, 3, 2, 4)
