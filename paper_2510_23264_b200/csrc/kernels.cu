@@ -160,9 +160,9 @@ __device__ __forceinline__ void decode_raw16(const Raw16& r, int t, float (&v)[1
 // knows). Node outputs are read-only during a fold (they were already read
 // with ld.global.nc), so the reordering does not change any value.
 template <bool kPipe>
-__global__ void __launch_bounds__(256) fold16_kernel(const FoldOp* __restrict__ ops,
-                                                     const FoldProg* __restrict__ progs,
-                                                     int64_t n_elems) {
+__device__ __forceinline__ void fold16_body(const FoldOp* __restrict__ ops,
+                                            const FoldProg* __restrict__ progs,
+                                            int64_t n_elems) {
   const FoldProg p = progs[blockIdx.y];
   const int64_t n16 = n_elems >> 4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16;
@@ -213,10 +213,24 @@ __global__ void __launch_bounds__(256) fold16_kernel(const FoldOp* __restrict__ 
   }
 }
 
-// CQG_FOLD_PIPE=1 selects the pipelined fold. Measured slower (fold 352 ->
-// 475 ms per step, profiles/r2_fold_pipe_ab_*.json): the extra raw buffer
-// takes the kernel from 48 to 70 registers, 5 -> 3 CTAs per SM, and the lost
-// warps cost more latency hiding than the one-op lookahead gains. Off by default.
+__global__ void __launch_bounds__(256) fold16_kernel(const FoldOp* __restrict__ ops,
+                                                     const FoldProg* __restrict__ progs,
+                                                     int64_t n_elems) {
+  fold16_body<false>(ops, progs, n_elems);
+}
+
+// Registers capped for four CTAs per SM.
+__global__ void __launch_bounds__(256, 4) fold16_pipe_kernel(const FoldOp* __restrict__ ops,
+                                                             const FoldProg* __restrict__ progs,
+                                                             int64_t n_elems) {
+  fold16_body<true>(ops, progs, n_elems);
+}
+
+// CQG_FOLD_PIPE=1 selects the pipelined fold. Measured slower: uncapped it
+// takes 70 registers (3 CTAs per SM), fold 352 -> 475 ms per step
+// (profiles/r2_fold_pipe_ab_*.json); capped at 64 for 4 CTAs per SM it is
+// still 457 ms (profiles/r2_fold_pipe4_ab_*.json). The one-op lookahead does
+// not pay for the warps it costs. Off by default.
 static bool fold_pipe() {
   const char* e = getenv("CQG_FOLD_PIPE");
   return e && e[0] == '1';
@@ -229,8 +243,8 @@ void launch_fold(const FoldOp* d_ops, const FoldProg* d_progs, int n_progs, int6
     int gx = (int)std::min<int64_t>((n_elems / 16 + 255) / 256, 4096);
     for (int y0 = 0; y0 < n_progs; y0 += 65535) {
       dim3 grid(gx, (unsigned)std::min(65535, n_progs - y0));
-      if (fold_pipe()) fold16_kernel<true><<<grid, 256, 0, st>>>(d_ops, d_progs + y0, n_elems);
-      else fold16_kernel<false><<<grid, 256, 0, st>>>(d_ops, d_progs + y0, n_elems);
+      if (fold_pipe()) fold16_pipe_kernel<<<grid, 256, 0, st>>>(d_ops, d_progs + y0, n_elems);
+      else fold16_kernel<<<grid, 256, 0, st>>>(d_ops, d_progs + y0, n_elems);
     }
     return;
   }
